@@ -1,0 +1,179 @@
+/*
+ * parnn_b200 — C ABI of the B200-native model-averaging DNN trainer.
+ *
+ * Drop-in boundary for the reference's trainer path (namespace parnn in
+ * /root/reference/proj). The reference has no FFI of its own; every entry
+ * point below names the reference interface it replaces (file:line). All
+ * functions return PARNN_OK (0) or PARNN_ERR (-1); on error
+ * parnn_last_error() returns the message (thread-local), whose text follows
+ * the reference's parnn::Error message for the same condition.
+ *
+ * Conventions: model parameters are fp64 host vectors in the reference's
+ * canonical flatten order [W0 row-major, b0, W1, b1, ...]
+ * (network.hpp:59-66); matrices are row-major fp64; labels int32.
+ */
+#ifndef PARNN_B200_H
+#define PARNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARNN_OK 0
+#define PARNN_ERR (-1)
+
+enum parnn_precision { PARNN_BF16 = 0, PARNN_TF32 = 1 };
+enum parnn_optimizer { PARNN_SGD = 0, PARNN_NGSGD = 1 };    /* parallel.hpp:14-18 */
+enum parnn_lr_variant { PARNN_NEWBOB = 0, PARNN_EXPONENTIAL = 1 }; /* optimizer.hpp:57 */
+enum parnn_activation { PARNN_SIGMOID = 0, PARNN_TANH = 1 };   /* network.hpp:16 */
+
+typedef struct parnn_ctx parnn_ctx;
+typedef struct parnn_dataset parnn_dataset;
+typedef struct parnn_replica parnn_replica;
+typedef struct parnn_comm parnn_comm;
+typedef struct parnn_rbm parnn_rbm;
+
+const char* parnn_last_error(void);
+const char* parnn_version(void);
+
+/* ---------------- host primitives (bit-exact with the reference) -------- */
+/* Rng::next_u64 stream (rng.cpp:30-41, seeded rng.cpp:25-28) */
+int parnn_rng_u64(uint64_t seed, uint64_t n, uint64_t* out);
+/* Rng::uniform (rng.cpp:43-45) */
+int parnn_rng_uniform(uint64_t seed, uint64_t n, double* out);
+/* Rng::gaussian_vector (rng.cpp:60-84) */
+int parnn_rng_gaussian(uint64_t seed, uint64_t n, double mean, double stddev, double* out);
+/* shuffled_indices (data.cpp:162-168, data.hpp:53-55) */
+int parnn_shuffled_indices(uint64_t n, uint64_t seed, uint64_t* out);
+/* partition_data (parallel.cpp:61-77): m*floor(n/m) row ids, shard-major */
+int parnn_partition_rows(uint64_t n, uint64_t m, uint64_t seed, uint64_t* out);
+/* minibatches (data.cpp:185-203): floor(n/b)*b shard positions, batch-major */
+int parnn_minibatch_rows(uint64_t n, uint64_t b, uint64_t seed, uint64_t* out);
+/* generate_synthetic + split_cv + feature_stats/standardize_in_place
+ * (data.cpp:124-242); buffers sized classes*per_class rows. */
+int parnn_make_data(uint64_t classes, uint64_t dim, uint64_t per_class, double separation, uint64_t seed,
+                    double cv_fraction, uint64_t split_seed, int standardize, double* train_x, int32_t* train_y,
+                    uint64_t* n_train, double* cv_x, int32_t* cv_y, uint64_t* n_cv);
+/* param_count (network.cpp:32-38) */
+uint64_t parnn_param_count(const uint64_t* dims, int ndims);
+/* init_random (network.cpp:40-60) with Rng(seed) */
+int parnn_init_random(const uint64_t* dims, int ndims, uint64_t seed, double* params);
+/* exponential_lr (optimizer.cpp:198-203) */
+int parnn_exponential_lr(double lr_init, uint64_t planned_epochs, double progress, double* lr);
+/* newbob_next (optimizer.cpp:181-196) over a CV-accuracy sequence: lr/stop per epoch >= 2 */
+int parnn_newbob_sequence(double lr_init, const double* accs, uint64_t n, double* lr_out, int* stop_out);
+/* scale_lr_for_workers (optimizer.cpp:205-208) */
+int parnn_scale_lr_for_workers(double lr_init, uint64_t workers, double* lr);
+/* save_model / load_model, PARNNET1 (network.cpp:291-369) */
+int parnn_save_model(const char* path, const uint64_t* dims, int ndims, int activation, const double* params);
+int parnn_load_model(const char* path, uint64_t* dims, int* ndims, int* activation, double* params,
+                     uint64_t capacity);
+/* allreduce_average on host vectors (parallel.cpp:40-59), fixed midpoint tree */
+int parnn_allreduce_average_host(const double* contributions, uint64_t m, uint64_t len, double* out);
+
+/* ---------------- device runtime ---------------------------------------- */
+int parnn_ctx_create(int device, parnn_ctx** out);
+int parnn_ctx_destroy(parnn_ctx* ctx);
+int parnn_ctx_sync(parnn_ctx* ctx);
+
+/* Device-resident Dataset (data.hpp:17-26): features n x d, labels. */
+int parnn_dataset_create(parnn_ctx* ctx, const double* x, const int32_t* y, uint64_t n, uint64_t d,
+                         uint64_t classes, parnn_dataset** out);
+int parnn_dataset_destroy(parnn_dataset* ds);
+
+/* One worker's model + NG state + workspaces (WorkerState, parallel.cpp:81-91). */
+int parnn_replica_create(parnn_ctx* ctx, const uint64_t* dims, int ndims, int activation, int precision,
+                         int optimizer, uint64_t minibatch, uint64_t max_steps, double ng_decay,
+                         double ng_smoothing, parnn_replica** out);
+int parnn_replica_destroy(parnn_replica* r);
+/* unflatten / flatten (network.cpp:238-272) */
+int parnn_replica_set_params(parnn_replica* r, const double* params, uint64_t n);
+int parnn_replica_get_params(parnn_replica* r, double* params, uint64_t n);
+/* NgState factors: per layer r_in (din^2) then r_out (dout^2) (optimizer.hpp:22-34) */
+int parnn_replica_get_ng_state(parnn_replica* r, double* factors, uint64_t n);
+int parnn_replica_set_ng_state(parnn_replica* r, const double* factors, uint64_t n, uint64_t update_count);
+/* Build the step's GEMM plans + CUDA graph against a training dataset. */
+int parnn_replica_bind(parnn_replica* r, parnn_dataset* train);
+/* Upload one epoch: steps*minibatch dataset row ids (Dataset::select order) and per-step lr. */
+int parnn_replica_upload_epoch(parnn_replica* r, const uint32_t* rows, const float* lrs, uint64_t steps);
+/* Enqueue `steps` minibatch updates: forward -> cross_entropy -> backward ->
+ * [ng_update_state -> ng_precondition] -> sgd_step_in_place
+ * (parallel.cpp:117-130). Asynchronous. */
+int parnn_replica_step(parnn_replica* r, uint64_t steps);
+/* Wait and raise the reference's errors (cholesky pivot, non-finite gradient). */
+int parnn_replica_sync(parnn_replica* r);
+/* Per-step batch CE (cross_entropy, network.cpp:145-160) of the current epoch. */
+int parnn_replica_ce(parnn_replica* r, double* out, uint64_t steps);
+/* forward (network.cpp:119-143): last-layer pre-activations for given rows. */
+int parnn_replica_forward(parnn_replica* r, parnn_dataset* ds, const uint32_t* rows, uint64_t b, float* z_out);
+/* accuracy (network.cpp:274-289) on a whole dataset */
+int parnn_replica_accuracy(parnn_replica* r, parnn_dataset* ds, double* acc);
+/* number of device kernels one step launches */
+int parnn_replica_kernels_per_step(parnn_replica* r, uint64_t* n);
+
+/* ---------------- averaging / multi-GPU ---------------------------------- */
+/* NCCL communicator across processes (one per GPU). */
+int parnn_comm_unique_id(unsigned char out[128]);
+int parnn_comm_create(parnn_ctx* ctx, const unsigned char id[128], int nranks, int rank, parnn_comm** out);
+int parnn_comm_destroy(parnn_comm* c);
+/* allreduce_average (parallel.cpp:40-59) over the local replicas (+ comm):
+ * every replica is replaced by the mean over m_total workers. */
+int parnn_average(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_t m_total);
+
+/* ---------------- the train loop ----------------------------------------- */
+/* ParallelPlan (parallel.hpp:22-27) + TrainOptions (parallel.hpp:31-38) + placement. */
+typedef struct {
+    uint64_t workers;        /* m */
+    uint64_t avg_frequency;  /* n */
+    uint64_t minibatch;      /* B */
+    uint64_t base_seed;
+    int optimizer;           /* parnn_optimizer */
+    int lr_schedule;         /* parnn_lr_variant */
+    double lr_init;
+    uint64_t epochs;
+    double ng_decay;
+    double ng_smoothing;
+    int precision;           /* parnn_precision */
+    int activation;          /* parnn_activation */
+    uint64_t rank0;          /* first global rank hosted by this process */
+    uint64_t local_workers;  /* ranks hosted here (0 = all m) */
+    int serial;              /* serial_train semantics (parallel.cpp:285-294) */
+} parnn_train_config;
+
+/* train_parallel / serial_train (parallel.cpp:163-294). metrics_out holds up
+ * to `epochs` rows of 7 doubles: {epoch, lr, train_ce, cv_accuracy,
+ * wall_seconds, workers, avg_events} (EpochMetrics, parallel.hpp:40-48). */
+int parnn_train(parnn_ctx* ctx, parnn_comm* comm, const parnn_train_config* cfg, const uint64_t* dims, int ndims,
+                const double* params0, parnn_dataset* train, parnn_dataset* cv, double* params_out,
+                double* metrics_out, uint64_t* epochs_run);
+
+/* ---------------- RBM CD-1 pretraining (pretrain.hpp) -------------------- */
+/* RbmParams packed as [W (h x v) row-major, v_bias (v), h_bias (h)]. */
+int parnn_rbm_create(parnn_ctx* ctx, uint64_t visible, uint64_t hidden, int gaussian, uint64_t batch, int precision,
+                     parnn_rbm** out);
+int parnn_rbm_destroy(parnn_rbm* r);
+int parnn_rbm_set_params(parnn_rbm* r, const double* p);
+int parnn_rbm_get_params(parnn_rbm* r, double* p);
+/* cd1_update (pretrain.cpp:123-125) on `b` rows of a host batch.
+ * sampling: 0 counter-based Philox Bernoulli(seed, counter), 1 threshold_half
+ * (pretrain.cpp:71-77), 2 host-provided uniforms (u_host, b*h values). */
+int parnn_rbm_cd1(parnn_rbm* r, const double* batch, uint64_t b, double lr, int sampling, uint64_t seed,
+                  uint64_t counter, const double* u_host);
+/* hidden_probs (pretrain.cpp:37-45) for n rows */
+int parnn_rbm_hidden_probs(parnn_rbm* r, const double* x, uint64_t n, double* out);
+/* reconstruction_error (pretrain.cpp:127-136) */
+int parnn_rbm_reconstruction_error(parnn_rbm* r, const double* x, uint64_t n, double* out);
+/* greedy_pretrain (pretrain.cpp:162-207): host Rng(seed) drives rbm_init,
+ * shuffles and the output-layer init exactly as the reference; Bernoulli
+ * draws use the counter-based device RNG (statistical parity only). */
+int parnn_greedy_pretrain(parnn_ctx* ctx, const uint64_t* dims, int ndims, const double* data, uint64_t n,
+                          uint64_t epochs, double lr_gaussian, double lr_bernoulli, uint64_t batch, uint64_t seed,
+                          int precision, double* params_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,442 @@
+// extern "C" boundary (include/parnn_b200.h). Never throws across the ABI:
+// every entry point converts exceptions into PARNN_ERR + parnn_last_error().
+#include "../../include/parnn_b200.h"
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "host.h"
+#include "parallel.h"
+#include "rbm.h"
+
+using namespace pnb;
+
+struct parnn_ctx {
+    std::unique_ptr<Context> c;
+};
+struct parnn_dataset {
+    std::unique_ptr<DeviceDataset> d;
+};
+struct parnn_replica {
+    std::unique_ptr<Replica> r;
+};
+struct parnn_comm {
+    std::unique_ptr<Comm> c;
+};
+struct parnn_rbm {
+    std::unique_ptr<RbmDevice> r;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return PARNN_OK;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+    } catch (...) {
+        g_err = "unknown error";
+    }
+    return PARNN_ERR;
+}
+
+void need(const void* p, const char* what) {
+    if (!p) throw std::runtime_error(std::string(what) + ": null pointer");
+}
+
+std::vector<long> to_dims(const uint64_t* dims, int nd) {
+    need(dims, "dims");
+    if (nd < 2) throw std::runtime_error("init_random: need at least 2 dims, got " + std::to_string(nd));
+    std::vector<long> v;
+    for (int i = 0; i < nd; ++i) v.push_back(static_cast<long>(dims[i]));
+    return v;
+}
+
+uint64_t padded_factor_count(const Replica& r) {
+    uint64_t n = 0;
+    for (int l = 0; l < r.L; ++l) n += r.dims[l] * r.dims[l] + r.dims[l + 1] * r.dims[l + 1];
+    return n;
+}
+
+uint64_t flat_count(const Replica& r) {
+    uint64_t n = 0;
+    for (int l = 0; l < r.L; ++l) n += r.dims[l] * r.dims[l + 1] + r.dims[l + 1];
+    return n;
+}
+}  // namespace
+
+extern "C" {
+
+const char* parnn_last_error(void) { return g_err.c_str(); }
+const char* parnn_version(void) { return "parnn_b200 0.1 (sm_100a)"; }
+
+int parnn_rng_u64(uint64_t seed, uint64_t n, uint64_t* out) {
+    return guarded([&] {
+        host::Rng r(seed);
+        for (uint64_t i = 0; i < n; ++i) out[i] = r.next_u64();
+    });
+}
+
+int parnn_rng_uniform(uint64_t seed, uint64_t n, double* out) {
+    return guarded([&] {
+        host::Rng r(seed);
+        for (uint64_t i = 0; i < n; ++i) out[i] = r.uniform();
+    });
+}
+
+int parnn_rng_gaussian(uint64_t seed, uint64_t n, double mean, double stddev, double* out) {
+    return guarded([&] {
+        host::Rng r(seed);
+        for (uint64_t i = 0; i < n; ++i) out[i] = r.gaussian(mean, stddev);
+    });
+}
+
+int parnn_shuffled_indices(uint64_t n, uint64_t seed, uint64_t* out) {
+    return guarded([&] {
+        const auto v = host::shuffled_indices(n, seed);
+        std::memcpy(out, v.data(), n * 8);
+    });
+}
+
+int parnn_partition_rows(uint64_t n, uint64_t m, uint64_t seed, uint64_t* out) {
+    return guarded([&] {
+        const auto v = host::partition_rows(n, m, seed);
+        std::memcpy(out, v.data(), v.size() * 8);
+    });
+}
+
+int parnn_minibatch_rows(uint64_t n, uint64_t b, uint64_t seed, uint64_t* out) {
+    return guarded([&] {
+        const auto v = host::minibatch_rows(n, b, seed);
+        std::memcpy(out, v.data(), v.size() * 8);
+    });
+}
+
+int parnn_make_data(uint64_t classes, uint64_t dim, uint64_t per_class, double sep, uint64_t seed, double cv_fraction,
+                    uint64_t split_seed, int standardize, double* train_x, int32_t* train_y, uint64_t* n_train,
+                    double* cv_x, int32_t* cv_y, uint64_t* n_cv) {
+    return guarded([&] {
+        const host::HostData all = host::generate_synthetic(classes, dim, per_class, sep, seed);
+        host::HostData tr, cv;
+        host::split_cv(all, cv_fraction, split_seed, tr, cv);
+        if (standardize) {
+            std::vector<double> mu, sd;
+            host::feature_stats(tr, mu, sd);
+            host::standardize(tr, mu, sd);
+            host::standardize(cv, mu, sd);
+        }
+        *n_train = tr.n;
+        *n_cv = cv.n;
+        if (train_x) std::memcpy(train_x, tr.x.data(), tr.x.size() * 8);
+        if (train_y) std::memcpy(train_y, tr.y.data(), tr.y.size() * 4);
+        if (cv_x) std::memcpy(cv_x, cv.x.data(), cv.x.size() * 8);
+        if (cv_y) std::memcpy(cv_y, cv.y.data(), cv.y.size() * 4);
+    });
+}
+
+uint64_t parnn_param_count(const uint64_t* dims, int nd) {
+    return host::param_count(std::vector<uint64_t>(dims, dims + nd));
+}
+
+int parnn_init_random(const uint64_t* dims, int nd, uint64_t seed, double* params) {
+    return guarded([&] {
+        host::Rng r(seed);
+        const auto p = host::init_random(std::vector<uint64_t>(dims, dims + nd), r);
+        std::memcpy(params, p.data(), p.size() * 8);
+    });
+}
+
+int parnn_exponential_lr(double lr_init, uint64_t epochs, double progress, double* lr) {
+    return guarded([&] { *lr = host::exponential_lr(host::make_schedule(false, lr_init, epochs), progress); });
+}
+
+int parnn_newbob_sequence(double lr_init, const double* accs, uint64_t n, double* lr_out, int* stop_out) {
+    return guarded([&] {
+        host::Schedule s = host::make_schedule(true, lr_init, 15);
+        for (uint64_t i = 1; i < n; ++i) stop_out[i - 1] = host::newbob_next(s, accs[i - 1], accs[i], &lr_out[i - 1]);
+    });
+}
+
+int parnn_scale_lr_for_workers(double lr_init, uint64_t workers, double* lr) {
+    return guarded([&] { *lr = host::scale_lr_for_workers(lr_init, workers); });
+}
+
+int parnn_save_model(const char* path, const uint64_t* dims, int nd, int act, const double* params) {
+    return guarded([&] {
+        std::vector<uint64_t> d(dims, dims + nd);
+        host::save_model(path, d, act, std::vector<double>(params, params + host::param_count(d)));
+    });
+}
+
+int parnn_load_model(const char* path, uint64_t* dims, int* nd, int* act, double* params, uint64_t cap) {
+    return guarded([&] {
+        std::vector<uint64_t> d;
+        std::vector<double> p;
+        host::load_model(path, d, *act, p);
+        if (static_cast<uint64_t>(*nd) < d.size()) throw std::runtime_error("load_model: dims buffer too small");
+        if (p.size() > cap) throw std::runtime_error("load_model: params buffer too small");
+        *nd = static_cast<int>(d.size());
+        std::memcpy(dims, d.data(), d.size() * 8);
+        std::memcpy(params, p.data(), p.size() * 8);
+    });
+}
+
+int parnn_allreduce_average_host(const double* c, uint64_t m, uint64_t len, double* out) {
+    return guarded([&] {
+        if (m == 0) throw std::runtime_error("allreduce_average: m must be >= 1");
+        std::vector<const double*> v;
+        for (uint64_t r = 0; r < m; ++r) v.push_back(c + r * len);
+        const auto a = host::allreduce_average(v, len);
+        std::memcpy(out, a.data(), len * 8);
+    });
+}
+
+int parnn_ctx_create(int device, parnn_ctx** out) {
+    return guarded([&] {
+        auto* c = new parnn_ctx;
+        c->c.reset(new Context(device));
+        *out = c;
+    });
+}
+
+int parnn_ctx_destroy(parnn_ctx* c) {
+    return guarded([&] { delete c; });
+}
+
+int parnn_ctx_sync(parnn_ctx* c) {
+    return guarded([&] { CUDA_THROW(cudaDeviceSynchronize()); });
+}
+
+int parnn_dataset_create(parnn_ctx* ctx, const double* x, const int32_t* y, uint64_t n, uint64_t d, uint64_t classes,
+                         parnn_dataset** out) {
+    return guarded([&] {
+        need(ctx, "dataset");
+        auto* p = new parnn_dataset;
+        p->d.reset(new DeviceDataset(ctx->c.get(), x, y, static_cast<long>(n), static_cast<long>(d),
+                                     static_cast<long>(classes)));
+        *out = p;
+    });
+}
+
+int parnn_dataset_destroy(parnn_dataset* ds) {
+    return guarded([&] { delete ds; });
+}
+
+int parnn_replica_create(parnn_ctx* ctx, const uint64_t* dims, int nd, int act, int prec, int opt, uint64_t minibatch,
+                         uint64_t max_steps, double decay, double smoothing, parnn_replica** out) {
+    return guarded([&] {
+        need(ctx, "replica");
+        if (decay <= 0.0 || decay >= 1.0)
+            throw std::runtime_error("ng_init: decay must be in (0,1), got " + std::to_string(decay));
+        if (smoothing <= 0.0) throw std::runtime_error("ng_init: smoothing must be positive, got " + std::to_string(smoothing));
+        auto* p = new parnn_replica;
+        p->r.reset(new Replica(ctx->c.get(), to_dims(dims, nd), act, static_cast<Precision>(prec),
+                               opt ? OPT_NG_KRON : OPT_SGD, static_cast<long>(minibatch), static_cast<long>(max_steps),
+                               decay, smoothing));
+        *out = p;
+    });
+}
+
+int parnn_replica_destroy(parnn_replica* r) {
+    return guarded([&] { delete r; });
+}
+
+int parnn_replica_set_params(parnn_replica* r, const double* p, uint64_t n) {
+    return guarded([&] {
+        if (n != flat_count(*r->r))
+            throw std::runtime_error("unflatten: vector length " + std::to_string(n) + " does not match model size " +
+                                     std::to_string(flat_count(*r->r)));
+        r->r->set_params(p);
+    });
+}
+
+int parnn_replica_get_params(parnn_replica* r, double* p, uint64_t n) {
+    return guarded([&] {
+        if (n < flat_count(*r->r)) throw std::runtime_error("flatten: output buffer too small");
+        r->r->get_params(p);
+    });
+}
+
+int parnn_replica_get_ng_state(parnn_replica* r, double* f, uint64_t n) {
+    return guarded([&] {
+        if (n < padded_factor_count(*r->r)) throw std::runtime_error("ng_state: output buffer too small");
+        r->r->get_ng_state(f);
+    });
+}
+
+int parnn_replica_set_ng_state(parnn_replica* r, const double* f, uint64_t n, uint64_t t) {
+    return guarded([&] {
+        if (n != padded_factor_count(*r->r)) throw std::runtime_error("ng_state: factor count mismatch");
+        r->r->set_ng_state(f, static_cast<long>(t));
+    });
+}
+
+int parnn_replica_bind(parnn_replica* r, parnn_dataset* ds) {
+    return guarded([&] { r->r->bind(ds->d.get()); });
+}
+
+int parnn_replica_upload_epoch(parnn_replica* r, const uint32_t* rows, const float* lrs, uint64_t steps) {
+    return guarded([&] {
+        Replica& R = *r->r;
+        if (!R.bound) throw std::runtime_error("replica: bind a dataset first");
+        for (uint64_t i = 0; i < steps * R.B; ++i)
+            if (rows[i] >= static_cast<uint64_t>(R.bound->n))
+                throw std::runtime_error("Dataset::select: index " + std::to_string(rows[i]) + " out of range " +
+                                         std::to_string(R.bound->n));
+        for (uint64_t i = 0; i < steps; ++i)
+            if (lrs[i] < 0.f) throw std::runtime_error("sgd_step: negative learning rate " + std::to_string(lrs[i]));
+        R.upload_epoch(rows, lrs, static_cast<long>(steps));
+    });
+}
+
+int parnn_replica_step(parnn_replica* r, uint64_t steps) {
+    return guarded([&] {
+        for (uint64_t i = 0; i < steps; ++i) r->r->run_step(r->r->stream);
+    });
+}
+
+int parnn_replica_sync(parnn_replica* r) {
+    return guarded([&] { r->r->check_errors(); });
+}
+
+int parnn_replica_ce(parnn_replica* r, double* out, uint64_t steps) {
+    return guarded([&] {
+        CUDA_THROW(cudaStreamSynchronize(r->r->stream));
+        CUDA_THROW(cudaMemcpy(out, r->r->d_ce, steps * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int parnn_replica_forward(parnn_replica* r, parnn_dataset* ds, const uint32_t* rows, uint64_t b, float* z) {
+    return guarded([&] {
+        if (!r->r->bound) r->r->bind(ds->d.get());
+        r->r->forward_only(ds->d.get(), rows, static_cast<long>(b), z);
+    });
+}
+
+int parnn_replica_accuracy(parnn_replica* r, parnn_dataset* ds, double* acc) {
+    return guarded([&] { *acc = r->r->accuracy(ds->d.get()); });
+}
+
+int parnn_replica_kernels_per_step(parnn_replica* r, uint64_t* n) {
+    return guarded([&] {
+        Replica& R = *r->r;
+        if (!R.graph) throw std::runtime_error("replica: no step graph");
+        *n = static_cast<uint64_t>(R.kernels_per_step);
+    });
+}
+
+int parnn_comm_unique_id(unsigned char out[128]) {
+    return guarded([&] { nccl_unique_id(out); });
+}
+
+int parnn_comm_create(parnn_ctx* ctx, const unsigned char id[128], int nranks, int rank, parnn_comm** out) {
+    return guarded([&] {
+        auto* p = new parnn_comm;
+        p->c.reset(new Comm(ctx->c.get(), id, nranks, rank));
+        *out = p;
+    });
+}
+
+int parnn_comm_destroy(parnn_comm* c) {
+    return guarded([&] { delete c; });
+}
+
+int parnn_average(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_t m_total) {
+    return guarded([&] {
+        if (n_local <= 0) throw std::runtime_error("allreduce_average: m must be >= 1");
+        std::vector<Replica*> v;
+        for (int i = 0; i < n_local; ++i) v.push_back(reps[i]->r.get());
+        Averager a(v[0]->ctx, v, comm ? comm->c.get() : nullptr, static_cast<long>(m_total));
+        a.run();
+        for (Replica* r : v) CUDA_THROW(cudaStreamSynchronize(r->stream));
+    });
+}
+
+int parnn_train(parnn_ctx* ctx, parnn_comm* comm, const parnn_train_config* c, const uint64_t* dims, int nd,
+                const double* params0, parnn_dataset* train_set, parnn_dataset* cv, double* params_out,
+                double* metrics_out, uint64_t* epochs_run) {
+    return guarded([&] {
+        need(ctx, "train");
+        need(train_set, "train dataset");
+        need(c, "train config");
+        TrainConfig t;
+        t.workers = c->workers;
+        t.avg_frequency = c->avg_frequency;
+        t.minibatch = c->minibatch;
+        t.base_seed = c->base_seed;
+        t.optimizer = c->optimizer;
+        t.newbob = c->lr_schedule == PARNN_NEWBOB;
+        t.lr_init = c->lr_init;
+        t.epochs = c->epochs;
+        t.ng_decay = c->ng_decay;
+        t.ng_smoothing = c->ng_smoothing;
+        t.precision = c->precision;
+        t.activation = c->activation;
+        t.rank0 = c->rank0;
+        t.local = c->local_workers;
+        t.serial = c->serial;
+        std::vector<EpochRec> met;
+        pnb::train(ctx->c.get(), comm ? comm->c.get() : nullptr, t, to_dims(dims, nd), params0, train_set->d.get(),
+              cv ? cv->d.get() : nullptr, params_out, met);
+        for (size_t e = 0; e < met.size(); ++e) {
+            const EpochRec& m = met[e];
+            double* row = metrics_out + 7 * e;
+            row[0] = m.epoch;
+            row[1] = m.lr;
+            row[2] = m.train_ce;
+            row[3] = m.cv_accuracy;
+            row[4] = m.wall_seconds;
+            row[5] = m.workers;
+            row[6] = m.avg_events;
+        }
+        *epochs_run = met.size();
+    });
+}
+
+int parnn_rbm_create(parnn_ctx* ctx, uint64_t v, uint64_t h, int gaussian, uint64_t batch, int prec, parnn_rbm** out) {
+    return guarded([&] {
+        auto* p = new parnn_rbm;
+        p->r.reset(new RbmDevice(ctx->c.get(), static_cast<long>(v), static_cast<long>(h), gaussian != 0,
+                                 static_cast<long>(batch), static_cast<Precision>(prec)));
+        *out = p;
+    });
+}
+
+int parnn_rbm_destroy(parnn_rbm* r) {
+    return guarded([&] { delete r; });
+}
+
+int parnn_rbm_set_params(parnn_rbm* r, const double* p) {
+    return guarded([&] { r->r->set_params(p); });
+}
+
+int parnn_rbm_get_params(parnn_rbm* r, double* p) {
+    return guarded([&] { r->r->get_params(p); });
+}
+
+int parnn_rbm_cd1(parnn_rbm* r, const double* batch, uint64_t b, double lr, int sampling, uint64_t seed,
+                  uint64_t counter, const double* u) {
+    return guarded([&] { r->r->cd1_host(batch, static_cast<long>(b), lr, sampling, seed, counter, u); });
+}
+
+int parnn_rbm_hidden_probs(parnn_rbm* r, const double* x, uint64_t n, double* out) {
+    return guarded([&] { r->r->hidden_probs_host(x, static_cast<long>(n), out); });
+}
+
+int parnn_rbm_reconstruction_error(parnn_rbm* r, const double* x, uint64_t n, double* out) {
+    return guarded([&] { *out = r->r->reconstruction_error_host(x, static_cast<long>(n)); });
+}
+
+int parnn_greedy_pretrain(parnn_ctx* ctx, const uint64_t* dims, int nd, const double* data, uint64_t n, uint64_t epochs,
+                          double lr_g, double lr_b, uint64_t batch, uint64_t seed, int prec, double* params_out) {
+    return guarded([&] {
+        greedy_pretrain(ctx->c.get(), to_dims(dims, nd), data, static_cast<long>(n), epochs, lr_g, lr_b,
+                        static_cast<long>(batch), seed, static_cast<Precision>(prec), params_out);
+    });
+}
+
+}  // extern "C"

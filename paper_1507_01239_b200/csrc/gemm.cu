@@ -1,0 +1,123 @@
+// Host side of the tcgen05 GEMM: TMA tensor-map construction, tile-shape
+// selection and launch. See gemm.cuh for the kernel.
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "gemm.cuh"
+#include "runtime.h"
+
+namespace pnb {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw std::runtime_error("gemm: cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2D row-major tensor [outer x inner] with row pitch ld (elements), box
+// {box_inner, box_outer}, 128-B swizzle, zero OOB fill.
+CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer, uint64_t ld,
+                      uint32_t box_inner, uint32_t box_outer, bool mn_major = false) {
+    CUtensorMap m;
+    const uint64_t esz = f32 ? 4 : 2;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * esz) & 15))
+        throw std::runtime_error("gemm: TMA operand must be 16-byte aligned (base " +
+                                 std::to_string(reinterpret_cast<uintptr_t>(base)) + ", ld " + std::to_string(ld) + ")");
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {ld * esz};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                              const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              (f32 && mn_major) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("gemm: cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
+template <int BN>
+constexpr int stages_for() {
+    return BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+}
+
+using KernelFn = void (*)(CUtensorMap, CUtensorMap, int, int, int, GemmEpi);
+
+template <typename T, int BN, bool AMN, bool BMN>
+KernelFn kernel_ptr(int* smem) {
+    constexpr int ST = stages_for<BN>();
+    *smem = GemmSmem<BN, ST, T>::kBytes;
+    auto k = &gemm_tc_kernel<T, BN, ST, AMN, BMN>;
+    static bool configured = false;
+    if (!configured) {
+        CUDA_THROW(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem));
+        configured = true;
+    }
+    return reinterpret_cast<KernelFn>(k);
+}
+
+template <typename T, int BN>
+KernelFn pick_major(bool amn, bool bmn, int* smem) {
+    if (!amn && !bmn) return kernel_ptr<T, BN, false, false>(smem);
+    if (amn && bmn) return kernel_ptr<T, BN, true, true>(smem);
+    if (!amn && bmn) return kernel_ptr<T, BN, false, true>(smem);
+    return kernel_ptr<T, BN, true, false>(smem);
+}
+
+template <typename T>
+KernelFn pick(int bn, bool amn, bool bmn, int* smem) {
+    switch (bn) {
+        case 256: return pick_major<T, 256>(amn, bmn, smem);
+        case 128: return pick_major<T, 128>(amn, bmn, smem);
+        default: return pick_major<T, 64>(amn, bmn, smem);
+    }
+}
+
+}  // namespace
+
+int choose_bn(int M, int N, int num_sms) {
+    const int mt = (M + 127) / 128;
+    for (int bn : {256, 128}) {
+        const long tiles = long(mt) * ((N + bn - 1) / bn);
+        if (tiles >= (num_sms * 3) / 4) return bn;
+    }
+    return 64;
+}
+
+void gemm_plan(GemmPlan& p, bool f32, bool a_mn, const void* A, long lda, bool b_mn, const void* B, long ldb,
+               int M, int N, int K, const GemmEpi& ep, int num_sms, int force_bn) {
+    if (M <= 0 || N <= 0 || K <= 0) throw std::runtime_error("gemm: empty problem");
+    const int bn = force_bn ? force_bn : choose_bn(M, N, num_sms);
+    const uint32_t atom = f32 ? 32 : 64;  // elements per 128-B row
+    const uint32_t bk = atom;
+    // A(m,k): K-major buffer [M x K] or MN-major buffer [K x M].
+    p.ta = a_mn ? make_tmap(A, f32, M, K, lda, atom, bk, true) : make_tmap(A, f32, K, M, lda, bk, 128);
+    p.tb = b_mn ? make_tmap(B, f32, N, K, ldb, atom, bk, true) : make_tmap(B, f32, K, N, ldb, bk, bn);
+    p.M = M;
+    p.N = N;
+    p.K = K;
+    p.ep = ep;
+    p.grid = dim3((N + bn - 1) / bn, (M + 127) / 128, 1);
+    p.fn = reinterpret_cast<void*>(f32 ? pick<float>(bn, a_mn, b_mn, &p.smem) : pick<__nv_bfloat16>(bn, a_mn, b_mn, &p.smem));
+    p.bn = bn;
+}
+
+void gemm_launch(const GemmPlan& p, cudaStream_t s) {
+    auto fn = reinterpret_cast<KernelFn>(p.fn);
+    fn<<<p.grid, 128, p.smem, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.ep);
+    CUDA_THROW(cudaGetLastError());
+}
+
+}  // namespace pnb

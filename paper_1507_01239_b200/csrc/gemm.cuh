@@ -1,0 +1,353 @@
+// tcgen05 / TMEM / TMA GEMM for sm_100a with the trainer's fused epilogues.
+//
+//   D[m, n] = sum_k A(m, k) * B(n, k)          (fp32 accumulate in TMEM)
+//
+// A and B are row-major device buffers read by TMA in either of two
+// orientations (template flags):
+//   K-major : the buffer is [rows x K] with K contiguous   (box {128 B, rows})
+//   MN-major: the buffer is [K x rows] with rows contiguous (box {128 B, BK})
+// which covers every product of the path without transposed copies
+// (SURVEY §7 "Operand majors"):
+//   forward  Z  = A_prev . W^T      A K-major,  B K-major   (network.cpp:94-101)
+//   dW       G  = dz^T . A_prev     A MN-major, B MN-major  (network.cpp:201-202)
+//   dA       dA = dz . W            A K-major,  B MN-major  (network.cpp:214)
+//   moments  C  = X^T . X           A MN-major, B MN-major  (optimizer.cpp:97-100)
+//
+// Operands are BF16 (kind::f16) or FP32 read as TF32 (kind::tf32). One CTA
+// computes one 128 x BN tile: warp 0 lane 0 issues TMA into a STAGES-deep
+// smem ring, warp 1 lane 0 issues tcgen05.mma (128 x BN x 16|8) into TMEM,
+// then all four warps drain TMEM (tcgen05.ld 32x32b) through the epilogue.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include "ptx.cuh"
+
+namespace pnb {
+
+enum EpiMode : int {
+    EPI_FWD_ACT = 0,     // out(T)   = act(acc + bias[n])
+    EPI_FWD_LINEAR = 1,  // out32    = acc + bias[n]
+    EPI_GRAD = 2,        // out32    = alpha * acc            (+ finite flag)
+    EPI_GRAD_SGD = 3,    // g = alpha*acc; W32 -= lr*g; shadow = bf16(W32)  (+ flag)
+    EPI_ACTGRAD = 4,     // out(T)   = acc * act'(aux[m, n])
+    EPI_EMA = 5,         // out32    = beta * out32 + alpha * acc
+    EPI_AXPY = 6,        // out32   += alpha * acc; shadow = bf16(out32)   (CD-1 update)
+};
+
+struct GemmEpi {
+    int mode = 0;
+    int act = 0;  // 0 sigmoid, 1 tanh (network.cpp:64-73), 2 identity
+    float out_scale = 1.f;  // FWD_ACT: multiplies the activated value (CD-1 stores -neg)
+    void* out = nullptr;  // T-typed output (FWD_ACT, ACTGRAD)
+    long ld_out = 0;
+    float* out32 = nullptr;  // fp32 output / master params (FWD_LINEAR, GRAD, GRAD_SGD, EMA)
+    long ld_out32 = 0;
+    __nv_bfloat16* shadow = nullptr;  // bf16 operand shadow of out32 (GRAD_SGD, bf16 mode)
+    long ld_shadow = 0;
+    const float* bias = nullptr;
+    const void* aux = nullptr;  // T-typed activations for ACTGRAD
+    long ld_aux = 0;
+    float alpha = 1.f;
+    float beta = 0.f;
+    const float* coef = nullptr;  // EMA: device {beta, alpha} overriding the scalars
+    const float* lr = nullptr;  // device scalar array indexed by *step
+    const int* step = nullptr;
+    unsigned* flag = nullptr;  // bit `flag_bit` set on a non-finite gradient
+    unsigned flag_bit = 0;
+};
+
+template <typename T>
+struct OpTraits;
+template <>
+struct OpTraits<__nv_bfloat16> {
+    static constexpr bool kTf32 = false;
+    static constexpr uint32_t kFmt = 1;
+};
+template <>
+struct OpTraits<float> {
+    static constexpr bool kTf32 = true;
+    static constexpr uint32_t kFmt = 2;
+};
+
+__device__ __forceinline__ float act_fwd(int act, float z) {
+    return act == 0 ? 1.f / (1.f + expf(-z)) : (act == 1 ? tanhf(z) : z);
+}
+__device__ __forceinline__ float act_grad(int act, float a) {
+    return act == 0 ? a * (1.f - a) : 1.f - a * a;
+}
+
+template <typename T>
+__device__ __forceinline__ float ld_as_float(const T* p);
+template <>
+__device__ __forceinline__ float ld_as_float<float>(const float* p) {
+    return *p;
+}
+template <>
+__device__ __forceinline__ float ld_as_float<__nv_bfloat16>(const __nv_bfloat16* p) {
+    return __bfloat162float(*p);
+}
+template <typename T>
+__device__ __forceinline__ void st_from_float(T* p, float v);
+template <>
+__device__ __forceinline__ void st_from_float<float>(float* p, float v) {
+    *p = v;
+}
+template <>
+__device__ __forceinline__ void st_from_float<__nv_bfloat16>(__nv_bfloat16* p, float v) {
+    *p = __float2bfloat16_rn(v);
+}
+
+// 32 consecutive values of one row -> memory, vectorised when aligned.
+template <typename T>
+__device__ __forceinline__ void store_row32(T* dst, const float (&v)[32], int valid) {
+    if (valid == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        if constexpr (sizeof(T) == 4) {
+            float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                uint32_t w[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * i + 2 * j], v[8 * i + 2 * j + 1]);
+                    w[j] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                d4[i] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+    } else {
+        for (int j = 0; j < valid; ++j) st_from_float<T>(dst + j, v[j]);
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void load_row32(const T* src, float (&v)[32], int valid) {
+    if (valid == 32 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        if constexpr (sizeof(T) == 4) {
+            const float4* s4 = reinterpret_cast<const float4*>(src);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float4 f = s4[i];
+                v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
+            }
+        } else {
+            const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                uint4 u = s4[i];
+                uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&w[j]);
+                    float2 f = __bfloat1622float2(h);
+                    v[8 * i + 2 * j] = f.x;
+                    v[8 * i + 2 * j + 1] = f.y;
+                }
+            }
+        }
+    } else {
+        for (int j = 0; j < 32; ++j) v[j] = j < valid ? ld_as_float<T>(src + j) : 0.f;
+    }
+}
+
+template <int BN, int STAGES, typename T>
+struct GemmSmem {
+    static constexpr int kElem = sizeof(T);
+    static constexpr int kBK = 128 / kElem;    // K per stage (one 128-B swizzle row)
+    static constexpr int kUK = 32 / kElem;     // K per tcgen05.mma
+    static constexpr int kAtom = 128 / kElem;  // MN elements per 128-B atom
+    static constexpr int kABytes = 128 * 128;
+    static constexpr int kBBytes = BN * 128;
+    static constexpr int kStage = kABytes + kBBytes;
+    static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <typename T, int BN, int STAGES, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(128, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   int M, int N, int K, GemmEpi ep) {
+    using S = GemmSmem<BN, STAGES, T>;
+    constexpr bool kTf32 = OpTraits<T>::kTf32;
+    static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
+    uint64_t* empty = full + STAGES;
+    uint64_t* done = empty + STAGES;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * 128;
+    const int n0 = blockIdx.x * BN;
+    const int nk = (K + S::kBK - 1) / S::kBK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        fence_barrier_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 1) tmem_alloc<(BN < 32 ? 32 : BN)>(tslot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer ----------------
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % STAGES;
+            if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+            uint8_t* sa = smem + s * S::kStage;
+            uint8_t* sb = sa + S::kABytes;
+            mbar_arrive_expect_tx(&full[s], S::kStage);
+            const int k0 = kb * S::kBK;
+            if constexpr (!A_MN) {
+                tma_load_2d(sa, &tmA, &full[s], k0, m0);
+            } else {
+#pragma unroll
+                for (int a = 0; a < 128 / S::kAtom; ++a)
+                    tma_load_2d(sa + a * (S::kBK * 128), &tmA, &full[s], m0 + a * S::kAtom, k0);
+            }
+            if constexpr (!B_MN) {
+                tma_load_2d(sb, &tmB, &full[s], k0, n0);
+            } else {
+#pragma unroll
+                for (int a = 0; a < BN / S::kAtom; ++a)
+                    tma_load_2d(sb + a * (S::kBK * 128), &tmB, &full[s], n0 + a * S::kAtom, k0);
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t idesc = make_idesc(OpTraits<T>::kFmt, A_MN ? 1 : 0, B_MN ? 1 : 0, 128, BN);
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % STAGES;
+            mbar_wait(&full[s], (kb / STAGES) & 1);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + s * S::kStage);
+            const uint32_t sb = sa + S::kABytes;
+#pragma unroll
+            for (int k = 0; k < S::kBK / S::kUK; ++k) {
+                constexpr uint32_t kMnLayout = kTf32 ? 1 : 2;      // BASE32B for TF32 MN-major
+                constexpr uint32_t kMnSbo = kTf32 ? 512 : 1024;
+                const uint64_t ad = A_MN ? smem_desc_sw128(sa + k * S::kUK * 128, S::kBK * 128, kMnSbo, kMnLayout)
+                                         : smem_desc_sw128(sa + k * 32, 16, 1024);
+                const uint64_t bd = B_MN ? smem_desc_sw128(sb + k * S::kUK * 128, S::kBK * 128, kMnSbo, kMnLayout)
+                                         : smem_desc_sw128(sb + k * 32, 16, 1024);
+                umma<kTf32>(tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
+            umma_commit(&empty[s]);
+        }
+        umma_commit(done);
+    }
+    __syncwarp();
+
+    // ---------------- epilogue: TMEM -> registers -> global ----------------
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int row = m0 + warp * 32 + lane;
+    const bool row_ok = row < M;
+    float lr = 0.f;
+    if (ep.mode == EPI_GRAD_SGD) lr = ep.lr[ep.step ? *ep.step : 0];
+    bool bad = false;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+        const int n = n0 + c * 32;
+        if (n >= N) break;  // warp-uniform
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 32, r);
+        tmem_ld_wait();
+        if (!row_ok) continue;
+        const int valid = min(32, N - n);
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        switch (ep.mode) {
+            case EPI_FWD_ACT: {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    v[j] = ep.out_scale * act_fwd(ep.act, v[j] + (j < valid ? ep.bias[n + j] : 0.f));
+                store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
+                break;
+            }
+            case EPI_FWD_LINEAR: {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] += (j < valid ? ep.bias[n + j] : 0.f);
+                store_row32<float>(ep.out32 + row * ep.ld_out32 + n, v, valid);
+                break;
+            }
+            case EPI_GRAD: {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    v[j] *= ep.alpha;
+                    bad |= !isfinite(v[j]);
+                }
+                store_row32<float>(ep.out32 + row * ep.ld_out32 + n, v, valid);
+                break;
+            }
+            case EPI_GRAD_SGD: {
+                float w[32];
+                float* wp = ep.out32 + row * ep.ld_out32 + n;
+                load_row32<float>(wp, w, valid);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float g = v[j] * ep.alpha;
+                    bad |= (j < valid) && !isfinite(g);
+                    w[j] -= lr * g;
+                }
+                store_row32<float>(wp, w, valid);
+                if (ep.shadow) store_row32<__nv_bfloat16>(ep.shadow + row * ep.ld_shadow + n, w, valid);
+                break;
+            }
+            case EPI_ACTGRAD: {
+                float a[32];
+                load_row32<T>(static_cast<const T*>(ep.aux) + row * ep.ld_aux + n, a, valid);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] *= act_grad(ep.act, a[j]);
+                store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
+                break;
+            }
+            case EPI_EMA: {
+                float o[32];
+                float* op = ep.out32 + row * ep.ld_out32 + n;
+                const float beta = ep.coef ? ep.coef[0] : ep.beta;
+                const float alpha = ep.coef ? ep.coef[1] : ep.alpha;
+                if (beta != 0.f) load_row32<float>(op, o, valid);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) o[j] = (beta != 0.f ? beta * o[j] : 0.f) + alpha * v[j];
+                store_row32<float>(op, o, valid);
+                break;
+            }
+            case EPI_AXPY: {
+                float w[32];
+                float* wp = ep.out32 + row * ep.ld_out32 + n;
+                load_row32<float>(wp, w, valid);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) w[j] += ep.alpha * v[j];
+                store_row32<float>(wp, w, valid);
+                if (ep.shadow) store_row32<__nv_bfloat16>(ep.shadow + row * ep.ld_shadow + n, w, valid);
+                break;
+            }
+            default:
+                break;
+        }
+    }
+    if (bad && ep.flag) atomicOr(ep.flag, 1u << ep.flag_bit);
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<(BN < 32 ? 32 : BN)>(tmem);
+}
+
+}  // namespace pnb

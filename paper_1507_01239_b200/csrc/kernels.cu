@@ -1,0 +1,223 @@
+// HBM-bound helper kernels of the trainer step: minibatch gather, fused
+// softmax + cross-entropy + (p - onehot), CE reduction, bias gradient with the
+// fused SGD update, dtype conversion and the CV argmax.
+#include <cfloat>
+
+#include "runtime.h"
+
+namespace pnb {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) {
+    return v;
+}
+template <>
+__device__ __forceinline__ float to_f<bf16>(bf16 v) {
+    return __bfloat162float(v);
+}
+
+// Dataset::select / minibatches row gather (data.cpp:12-25, 185-203): one
+// CTA per batch row, 16-byte vector copies (rows are 128-B aligned, zero padded).
+__global__ void gather_kernel(const uint4* __restrict__ x, long ldx_v, const int32_t* __restrict__ y,
+                              const uint32_t* __restrict__ rows, const int* __restrict__ step, long B,
+                              long nvec, uint4* __restrict__ out, long ldo_v, int32_t* __restrict__ yout) {
+    const long b = blockIdx.x;
+    const long st = step ? *step : 0;
+    const uint32_t src = rows[st * B + b];
+    const uint4* xs = x + src * ldx_v;
+    uint4* o = out + b * ldo_v;
+    for (long j = threadIdx.x; j < nvec; j += blockDim.x) o[j] = xs[j];
+    if (threadIdx.x == 0) yout[b] = y[src];
+}
+
+__device__ __forceinline__ float block_reduce_max(float v, float* sh) {
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffff, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = l < (blockDim.x >> 5) ? sh[l] : -FLT_MAX;
+        for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffff, v, o));
+        if (l == 0) sh[32] = v;
+    }
+    __syncthreads();
+    v = sh[32];
+    __syncthreads();
+    return v;
+}
+
+__device__ __forceinline__ float block_reduce_sum(float v, float* sh) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = l < (blockDim.x >> 5) ? sh[l] : 0.f;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+        if (l == 0) sh[32] = v;
+    }
+    __syncthreads();
+    v = sh[32];
+    __syncthreads();
+    return v;
+}
+
+// softmax_rows + cross_entropy + dz init (network.cpp:76-92, 145-160, 194-197):
+// per row, max-subtracted softmax, CE_i = lse_i - z_{i,y}, dz = p - onehot.
+template <typename T>
+__global__ void softmax_ce_kernel(const float* __restrict__ z, long ldz, long C, const int32_t* __restrict__ y,
+                                  T* __restrict__ dz, long lddz, float* __restrict__ ce_rows) {
+    __shared__ float sh[33];
+    const long i = blockIdx.x;
+    const float* zr = z + i * ldz;
+    float m = -FLT_MAX;
+    for (long j = threadIdx.x; j < C; j += blockDim.x) m = fmaxf(m, zr[j]);
+    m = block_reduce_max(m, sh);
+    float s = 0.f;
+    for (long j = threadIdx.x; j < C; j += blockDim.x) s += expf(zr[j] - m);
+    s = block_reduce_sum(s, sh);
+    const float inv = 1.f / s;
+    const int lab = y[i];
+    T* dr = dz + i * lddz;
+    for (long j = threadIdx.x; j < C; j += blockDim.x) {
+        float p = expf(zr[j] - m) * inv;
+        if (j == lab) p -= 1.f;
+        dr[j] = static_cast<T>(p);
+    }
+    if (threadIdx.x == 0) ce_rows[i] = logf(s) + m - zr[lab];
+}
+
+// Deterministic batch-mean CE into d_ce[*step]; optionally advances the step.
+__global__ void ce_reduce_kernel(const float* __restrict__ ce_rows, long B, double* __restrict__ d_ce,
+                                 int* __restrict__ step, int advance) {
+    __shared__ double sh[256];
+    double acc = 0.0;
+    for (long i = threadIdx.x; i < B; i += blockDim.x) acc += ce_rows[i];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int st = *step;
+        d_ce[st] = sh[0] / static_cast<double>(B);
+        if (advance) *step = st + 1;
+    }
+}
+
+// db = colsum(dz)/B (network.cpp:203-208); finite check (optimizer.cpp:26-28);
+// SGD b -= lr*db (optimizer.cpp:32-34) when bias != null; db stored when gb != null.
+template <typename T>
+__global__ void bias_grad_kernel(const T* __restrict__ dz, long lddz, long B, long C, float* __restrict__ bias,
+                                 float* __restrict__ gb, const float* __restrict__ lr, const int* __restrict__ step,
+                                 unsigned* __restrict__ flags, unsigned bit) {
+    __shared__ float sh[8][33];
+    const long j = blockIdx.x * 32 + threadIdx.x;
+    float acc = 0.f;
+    if (j < C)
+        for (long b = threadIdx.y; b < B; b += 8) acc += to_f<T>(dz[b * lddz + j]);
+    sh[threadIdx.y][threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.y == 0 && j < C) {
+        float s = 0.f;
+        for (int r = 0; r < 8; ++r) s += sh[r][threadIdx.x];
+        const float g = s * (1.f / static_cast<float>(B));
+        if (!isfinite(g) && flags) atomicOr(flags, 1u << bit);
+        if (gb) gb[j] = g;
+        if (bias) bias[j] -= lr[step ? *step : 0] * g;
+    }
+}
+
+__global__ void f32_to_bf16_rows_kernel(const float* __restrict__ src, long ld, long rows, long cols,
+                                        bf16* __restrict__ dst) {
+    const long total = rows * ld;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+        const long c = i % ld;
+        dst[i] = __float2bfloat16_rn(c < cols ? src[i] : 0.f);
+    }
+}
+
+__global__ void argmax_correct_kernel(const float* __restrict__ z, long ldz, long C, const int32_t* __restrict__ y,
+                                      unsigned long long* correct) {
+    // accuracy (network.cpp:274-289): first maximum wins (strict >).
+    __shared__ float sv[256];
+    __shared__ int si[256];
+    const long i = blockIdx.x;
+    const float* zr = z + i * ldz;
+    float best = -FLT_MAX;
+    int bi = 0x7fffffff;
+    for (long j = threadIdx.x; j < C; j += blockDim.x) {
+        const float v = zr[j];
+        if (v > best) { best = v; bi = (int)j; }
+    }
+    sv[threadIdx.x] = best;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (threadIdx.x < o) {
+            const float v2 = sv[threadIdx.x + o];
+            const int i2 = si[threadIdx.x + o];
+            if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 < si[threadIdx.x])) {
+                sv[threadIdx.x] = v2;
+                si[threadIdx.x] = i2;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && si[0] == y[i]) atomicAdd(correct, 1ull);
+}
+
+}  // namespace
+
+void launch_gather(const void* x, long ldx, const int32_t* y, const uint32_t* rows, const int* step, long B, long d,
+                   void* out, long ldo, int32_t* yout, bool f32, cudaStream_t s) {
+    const long per = f32 ? 4 : 8;  // elements per uint4
+    const long nvec = (pad32(d) + per - 1) / per;
+    gather_kernel<<<B, 128, 0, s>>>(static_cast<const uint4*>(x), ldx / per, y, rows, step, B, nvec,
+                                    static_cast<uint4*>(out), ldo / per, yout);
+}
+
+void launch_softmax_ce(const float* z, long ldz, long B, long C, const int32_t* y, void* dz, long lddz,
+                       float* ce_rows, bool f32, cudaStream_t s) {
+    if (f32)
+        softmax_ce_kernel<float><<<B, 256, 0, s>>>(z, ldz, C, y, static_cast<float*>(dz), lddz, ce_rows);
+    else
+        softmax_ce_kernel<bf16><<<B, 256, 0, s>>>(z, ldz, C, y, static_cast<bf16*>(dz), lddz, ce_rows);
+}
+
+void launch_ce_reduce(const float* ce_rows, long B, double* d_ce, int* step, int advance, cudaStream_t s) {
+    ce_reduce_kernel<<<1, 256, 0, s>>>(ce_rows, B, d_ce, step, advance);
+}
+
+void launch_bias_grad(const void* dz, long lddz, long B, long C, bool f32, float* bias, float* gb, const float* lr,
+                      const int* step, unsigned* flags, unsigned bit, cudaStream_t s) {
+    dim3 grid((C + 31) / 32), block(32, 8);
+    if (f32)
+        bias_grad_kernel<float><<<grid, block, 0, s>>>(static_cast<const float*>(dz), lddz, B, C, bias, gb, lr, step,
+                                                       flags, bit);
+    else
+        bias_grad_kernel<bf16><<<grid, block, 0, s>>>(static_cast<const bf16*>(dz), lddz, B, C, bias, gb, lr, step,
+                                                      flags, bit);
+}
+
+void launch_f32_to_bf16_rows(const float* src, long ld, long rows, long cols, bf16* dst, cudaStream_t s) {
+    const long total = rows * ld;
+    const int blocks = (int)std::min<long>((total + 255) / 256, 148L * 16);
+    if (total > 0) f32_to_bf16_rows_kernel<<<blocks, 256, 0, s>>>(src, ld, rows, cols, dst);
+}
+
+void launch_convert_dataset(const float* x32, long n, long ld, bf16* x16, cudaStream_t s) {
+    launch_f32_to_bf16_rows(x32, ld, n, ld, x16, s);
+}
+
+void launch_argmax_correct(const float* z, long ldz, long B, long C, const int32_t* y, unsigned long long* correct,
+                           cudaStream_t s) {
+    argmax_correct_kernel<<<B, 256, 0, s>>>(z, ldz, C, y, correct);
+}
+
+}  // namespace pnb

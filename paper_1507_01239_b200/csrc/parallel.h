@@ -1,0 +1,64 @@
+// Cross-replica averaging and the multi-GPU communicator (NCCL over NVLink).
+#pragma once
+#include <cstring>
+#include <vector>
+
+#include "runtime.h"
+
+namespace pnb {
+
+struct Comm {
+    Context* ctx;
+    void* comm = nullptr;  // ncclComm_t
+    int nranks = 1, rank = 0;
+    double* dscratch = nullptr;
+    Comm(Context* c, const unsigned char id[128], int nranks, int rank);
+    ~Comm();
+    double allreduce_sum(double v);
+};
+
+void nccl_unique_id(unsigned char out[128]);
+
+// Replaces every local replica's parameters with the mean over all m workers
+// (local replicas + every other process in `comm`).
+struct Averager {
+    Context* ctx;
+    std::vector<Replica*> reps;
+    Comm* comm;
+    long m_total;
+    long n = 0;
+    float** d_src = nullptr;
+    bf16** d_shadow = nullptr;
+    float* scratch = nullptr;
+    float** d_scratch_ptr = nullptr;
+    cudaEvent_t ev_done = nullptr;
+    std::vector<cudaEvent_t> ev_rep;
+    Averager(Context* c, const std::vector<Replica*>& reps, Comm* comm, long m_total);
+    ~Averager();
+    void run();
+};
+
+struct TrainConfig {
+    uint64_t workers = 1, avg_frequency = 10, minibatch = 128, base_seed = 0;
+    int optimizer = 1;   // 0 sgd, 1 ngsgd (parallel.hpp:31-38 default)
+    int newbob = 0;      // 0 exponential (default), 1 newbob
+    double lr_init = 0.32;
+    uint64_t epochs = 15;
+    double ng_decay = 0.95, ng_smoothing = 4.0;
+    int precision = PREC_BF16;
+    int activation = 0;
+    uint64_t rank0 = 0;   // first global worker rank hosted by this process
+    uint64_t local = 0;   // workers hosted by this process (0 = all)
+    int serial = 0;       // serial_train semantics (errors not wrapped)
+};
+
+struct EpochRec {
+    double epoch, lr, train_ce, cv_accuracy, wall_seconds, workers, avg_events;
+};
+
+// train_loop (parallel.cpp:163-275) for the workers this process hosts.
+void train(Context* ctx, Comm* comm, const TrainConfig& cfg, const std::vector<long>& dims, const double* params0,
+           DeviceDataset* train_ds, DeviceDataset* cv_ds, double* params_out, std::vector<EpochRec>& metrics,
+           double* step_seconds = nullptr);
+
+}  // namespace pnb

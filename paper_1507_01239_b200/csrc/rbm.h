@@ -1,0 +1,45 @@
+// RBM CD-1 pretraining on device (pretrain.hpp / pretrain.cpp).
+#pragma once
+#include <vector>
+
+#include "runtime.h"
+
+namespace pnb {
+
+struct RbmDevice {
+    Context* ctx;
+    cudaStream_t stream = nullptr;
+    long v, h, B;
+    bool gaussian;
+    Precision prec;
+    long ldv, ldh;
+    float* W = nullptr;  // [h x ldv] fp32 master
+    bf16* Ws = nullptr;  // bf16 operand copy
+    float* vb = nullptr;
+    float* hb = nullptr;
+    void* XR = nullptr;  // [2B x ldv] op dtype: batch rows, then reconstruction rows
+    void* PN = nullptr;  // [2B x ldh] op dtype: pos probs, then -neg probs
+    void* HS = nullptr;  // [B x ldh] op dtype: hidden samples
+    double* u_dev = nullptr;  // injected uniforms [B x h]
+    double* red = nullptr;    // reduction scratch
+    long planned_b = -1;
+    GemmPlan g_pos, g_recon, g_neg, g_upd;
+
+    RbmDevice(Context* c, long visible, long hidden, bool gaussian, long batch, Precision p);
+    ~RbmDevice();
+    bool f32() const { return prec == PREC_TF32; }
+    void set_params(const double* p);  // [W, v_bias, h_bias]
+    void get_params(double* p);
+    void plan(long b);
+    // one CD-1 update on the b rows already in XR[0:b)
+    void cd1(long b, double lr, int sampling, uint64_t seed, uint64_t counter);
+    void cd1_host(const double* batch, long b, double lr, int sampling, uint64_t seed, uint64_t counter,
+                  const double* u);
+    void hidden_probs_host(const double* x, long n, double* out);
+    double reconstruction_error_host(const double* x, long n);
+};
+
+void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* data, long n, uint64_t epochs,
+                     double lr_g, double lr_b, long batch, uint64_t seed, Precision prec, double* params_out);
+
+}  // namespace pnb

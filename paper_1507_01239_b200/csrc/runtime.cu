@@ -1,0 +1,453 @@
+// Contexts, device-resident datasets and replicas; the fused minibatch step
+// (worker_epoch's body, parallel.cpp:117-130) as one CUDA graph.
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+#include "runtime.h"
+
+namespace pnb {
+
+namespace {
+
+template <typename T>
+T* dalloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    CUDA_THROW(cudaMalloc(&p, n * sizeof(T)));
+    CUDA_THROW(cudaMemset(p, 0, n * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+void dfree(void* p) {
+    if (p) cudaFree(p);
+}
+
+// EMA coefficients of ema_update (optimizer.cpp:64-75) for t = ++(*t_dev):
+// coef = {keep, add / B}; t == 1 assigns the batch moment.
+__global__ void ng_coeff_kernel(long* t_dev, double rho, double inv_b, float* coef) {
+    const long t = *t_dev + 1;
+    *t_dev = t;
+    double keep = 0.0, add = 1.0;
+    if (t > 1) {
+        const double denom = 1.0 - pow(rho, (double)t);
+        keep = rho * (1.0 - pow(rho, (double)(t - 1))) / denom;
+        add = (1.0 - rho) / denom;
+    }
+    coef[0] = (float)keep;
+    coef[1] = (float)(add * inv_b);
+}
+
+// Record the first step whose gradients were non-finite, then clear the
+// per-step bits (so the host can name the layer the reference would).
+__global__ void flags_latch_kernel(unsigned* flags, const int* step) {
+    if (flags[0] && !flags[1]) {
+        flags[1] = flags[0];
+        flags[2] = (unsigned)*step;
+    }
+    flags[0] = 0;
+}
+
+}  // namespace
+
+Context::Context(int dev) : device(dev) {
+    CUDA_THROW(cudaSetDevice(dev));
+    CUDA_THROW(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_THROW(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+}
+
+Context::~Context() {
+    if (stream) cudaStreamDestroy(stream);
+}
+
+DeviceDataset::DeviceDataset(Context* c, const double* x, const int32_t* labels, long n_, long d_, long classes_)
+    : ctx(c), n(n_), d(d_), ld(pad32(d_)), classes(classes_) {
+    CUDA_THROW(cudaSetDevice(c->device));
+    std::vector<float> h(static_cast<size_t>(n * ld), 0.f);
+    for (long i = 0; i < n; ++i)
+        for (long j = 0; j < d; ++j) h[i * ld + j] = static_cast<float>(x[i * d + j]);
+    for (long i = 0; i < n; ++i)
+        if (labels[i] < 0 || labels[i] >= classes)
+            throw std::runtime_error("dataset: label " + std::to_string(labels[i]) + " at row " + std::to_string(i) +
+                                     " out of range [0, " + std::to_string(classes) + ")");
+    x32 = dalloc<float>(h.size());
+    y = dalloc<int32_t>(n);
+    CUDA_THROW(cudaMemcpy(x32, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_THROW(cudaMemcpy(y, labels, n * 4, cudaMemcpyHostToDevice));
+}
+
+DeviceDataset::~DeviceDataset() {
+    dfree(x32);
+    dfree(x16);
+    dfree(y);
+}
+
+const void* DeviceDataset::features(Precision p) {
+    if (p == PREC_TF32) return x32;
+    if (!x16) {
+        x16 = dalloc<bf16>(static_cast<size_t>(n * ld));
+        launch_convert_dataset(x32, n, ld, x16, ctx->stream);
+        CUDA_THROW(cudaStreamSynchronize(ctx->stream));
+    }
+    return x16;
+}
+
+Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision p, Optimizer o, long batch,
+                 long max_steps_, double decay, double smoothing)
+    : ctx(c), dims(dims_), act(act_), prec(p), opt(o), B(batch), max_steps(max_steps_), ng_decay(decay),
+      ng_smoothing(smoothing) {
+    if (dims.size() < 2) throw std::runtime_error("replica: need at least 2 dims");
+    for (long d : dims)
+        if (d <= 0) throw std::runtime_error("replica: zero layer dimension");
+    if (B <= 0) throw std::runtime_error("replica: minibatch must be >= 1");
+    CUDA_THROW(cudaSetDevice(c->device));
+    CUDA_THROW(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    L = static_cast<int>(dims.size()) - 1;
+    long off = 0;
+    for (int l = 0; l < L; ++l) {
+        ldw.push_back(pad32(dims[l]));
+        w_off.push_back(off);
+        off += dims[l + 1] * ldw[l];
+        b_off.push_back(off);
+        off += pad32(dims[l + 1]);
+    }
+    n_pad = off;
+    params = dalloc<float>(n_pad);
+    if (!f32()) wshadow = dalloc<bf16>(n_pad);
+    if (opt == OPT_NG_KRON) grads = dalloc<float>(n_pad);
+    for (int l = 0; l <= L; ++l) ld_act.push_back(pad32(dims[l]));
+    for (int l = 0; l < L; ++l) acts.push_back(f32() ? (void*)dalloc<float>(B * ld_act[l]) : (void*)dalloc<bf16>(B * ld_act[l]));
+    acts.push_back(nullptr);  // the last layer keeps Z (fp32) in zout
+    zout = dalloc<float>(B * ld_act[L]);
+    for (int l = 0; l < L; ++l)
+        dz.push_back(f32() ? (void*)dalloc<float>(B * ld_act[l + 1]) : (void*)dalloc<bf16>(B * ld_act[l + 1]));
+    if (opt == OPT_NG_KRON) {
+        long max_out = 0, max_in = 0, max_t = 0;
+        for (int l = 0; l < L; ++l) {
+            r_in.push_back(dalloc<float>(dims[l] * pad32(dims[l])));
+            r_out.push_back(dalloc<float>(dims[l + 1] * pad32(dims[l + 1])));
+            max_out = std::max(max_out, dims[l + 1] * pad32(dims[l + 1]));
+            max_in = std::max(max_in, dims[l] * pad32(dims[l]));
+            max_t = std::max(max_t, dims[l + 1] * pad32(dims[l] + 1) + dims[l] * pad32(dims[l + 1]));
+        }
+        chol_a = dalloc<float>(max_out);
+        chol_b = dalloc<float>(max_in);
+        tbuf = dalloc<float>(max_t);
+    }
+    scal = dalloc<double>(16 * (L + 1) + 512);
+    d_step = dalloc<int>(4);
+    d_lr = dalloc<float>(std::max<long>(max_steps, 1));
+    d_rows = dalloc<uint32_t>(std::max<long>(max_steps, 1) * B);
+    d_ybatch = dalloc<int32_t>(B);
+    ce_rows = dalloc<float>(B);
+    d_ce = dalloc<double>(std::max<long>(max_steps, 1));
+    d_flags = dalloc<unsigned>(4);
+    d_err = dalloc<DevErr>(1);
+}
+
+Replica::~Replica() {
+    if (stream) cudaStreamSynchronize(stream);
+    if (graph) cudaGraphExecDestroy(graph);
+    dfree(params);
+    dfree(wshadow);
+    dfree(grads);
+    for (void* p : acts) dfree(p);
+    dfree(zout);
+    for (void* p : dz) dfree(p);
+    for (float* p : r_in) dfree(p);
+    for (float* p : r_out) dfree(p);
+    dfree(chol_a);
+    dfree(chol_b);
+    dfree(tbuf);
+    dfree(scal);
+    dfree(d_step);
+    dfree(d_lr);
+    dfree(d_rows);
+    dfree(d_ybatch);
+    dfree(ce_rows);
+    dfree(d_ce);
+    dfree(d_flags);
+    dfree(d_err);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+void Replica::sync_shadow(cudaStream_t s) {
+    if (!wshadow) return;
+    for (int l = 0; l < L; ++l)
+        launch_f32_to_bf16_rows(params + w_off[l], ldw[l], dims[l + 1], dims[l], wshadow + w_off[l], s);
+}
+
+void Replica::set_params(const double* flat) {
+    std::vector<float> h(static_cast<size_t>(n_pad), 0.f);
+    long pos = 0;
+    for (int l = 0; l < L; ++l) {
+        for (long r = 0; r < dims[l + 1]; ++r)
+            for (long c = 0; c < dims[l]; ++c) h[w_off[l] + r * ldw[l] + c] = static_cast<float>(flat[pos++]);
+        for (long r = 0; r < dims[l + 1]; ++r) h[b_off[l] + r] = static_cast<float>(flat[pos++]);
+    }
+    CUDA_THROW(cudaSetDevice(ctx->device));
+    CUDA_THROW(cudaMemcpy(params, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    sync_shadow(stream);
+    CUDA_THROW(cudaStreamSynchronize(stream));
+}
+
+void Replica::get_params(double* flat) const {
+    std::vector<float> h(static_cast<size_t>(n_pad));
+    CUDA_THROW(cudaSetDevice(ctx->device));
+    CUDA_THROW(cudaStreamSynchronize(stream));
+    CUDA_THROW(cudaMemcpy(h.data(), params, h.size() * 4, cudaMemcpyDeviceToHost));
+    long pos = 0;
+    for (int l = 0; l < L; ++l) {
+        for (long r = 0; r < dims[l + 1]; ++r)
+            for (long c = 0; c < dims[l]; ++c) flat[pos++] = h[w_off[l] + r * ldw[l] + c];
+        for (long r = 0; r < dims[l + 1]; ++r) flat[pos++] = h[b_off[l] + r];
+    }
+}
+
+// factors: per layer r_in (din x din) then r_out (dout x dout), row-major.
+void Replica::get_ng_state(double* f) const {
+    if (opt != OPT_NG_KRON) throw std::runtime_error("replica: not an NG-SGD replica");
+    CUDA_THROW(cudaStreamSynchronize(stream));
+    long pos = 0;
+    for (int l = 0; l < L; ++l) {
+        for (int side = 0; side < 2; ++side) {
+            const long n = side == 0 ? dims[l] : dims[l + 1];
+            const long ld = pad32(n);
+            std::vector<float> h(static_cast<size_t>(n * ld));
+            CUDA_THROW(cudaMemcpy(h.data(), side == 0 ? r_in[l] : r_out[l], h.size() * 4, cudaMemcpyDeviceToHost));
+            for (long i = 0; i < n; ++i)
+                for (long j = 0; j < n; ++j) f[pos++] = h[i * ld + j];
+        }
+    }
+}
+
+void Replica::set_ng_state(const double* f, long t) {
+    if (opt != OPT_NG_KRON) throw std::runtime_error("replica: not an NG-SGD replica");
+    long pos = 0;
+    for (int l = 0; l < L; ++l) {
+        for (int side = 0; side < 2; ++side) {
+            const long n = side == 0 ? dims[l] : dims[l + 1];
+            const long ld = pad32(n);
+            std::vector<float> h(static_cast<size_t>(n * ld), 0.f);
+            for (long i = 0; i < n; ++i)
+                for (long j = 0; j < n; ++j) h[i * ld + j] = static_cast<float>(f[pos++]);
+            CUDA_THROW(cudaMemcpy(side == 0 ? r_in[l] : r_out[l], h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+        }
+    }
+    ng_t = t;
+    long tt = t;
+    CUDA_THROW(cudaMemcpy(reinterpret_cast<char*>(scal) + 8 * (16 * (L + 1) + 500), &tt, 8, cudaMemcpyHostToDevice));
+}
+
+void Replica::bind(DeviceDataset* ds) {
+    if (ds->d != dims[0])
+        throw std::runtime_error("forward: input has " + std::to_string(ds->d) + " columns, model expects " +
+                                 std::to_string(dims[0]));
+    if (ds->classes > dims[L])
+        throw std::runtime_error("dataset: " + std::to_string(ds->classes) + " classes exceed output dim " +
+                                 std::to_string(dims[L]));
+    bound = ds;
+    ds->features(prec);  // materialise the operand-typed copy before graph capture
+    const bool F = f32();
+    const int sms = ctx->num_sms;
+    fwd.assign(L, GemmPlan());
+    dw.assign(L, GemmPlan());
+    da.assign(L, GemmPlan());
+    mom_in.assign(L, GemmPlan());
+    mom_out.assign(L, GemmPlan());
+    float* coef = reinterpret_cast<float*>(scal + 16 * (L + 1) + 480);
+    for (int l = 0; l < L; ++l) {
+        const long din = dims[l], dout = dims[l + 1];
+        const void* W = F ? static_cast<const void*>(params + w_off[l]) : static_cast<const void*>(wshadow + w_off[l]);
+        GemmEpi e;
+        e.act = act;
+        if (l + 1 < L) {
+            e.mode = EPI_FWD_ACT;
+            e.out = acts[l + 1];
+            e.ld_out = ld_act[l + 1];
+        } else {
+            e.mode = EPI_FWD_LINEAR;
+            e.out32 = zout;
+            e.ld_out32 = ld_act[L];
+        }
+        e.bias = params + b_off[l];
+        gemm_plan(fwd[l], F, false, acts[l], ld_act[l], false, W, ldw[l], B, dout, din, e, sms);
+
+        // dW = dz^T A_prev / B  (M = dout, N = din, K = B)
+        GemmEpi g;
+        g.alpha = 1.f / static_cast<float>(B);
+        g.flag = d_flags;
+        g.flag_bit = 2 * l;
+        if (opt == OPT_SGD) {
+            g.mode = EPI_GRAD_SGD;
+            g.out32 = params + w_off[l];
+            g.ld_out32 = ldw[l];
+            g.shadow = wshadow ? wshadow + w_off[l] : nullptr;
+            g.ld_shadow = ldw[l];
+            g.lr = d_lr;
+            g.step = d_step;
+        } else {
+            g.mode = EPI_GRAD;
+            g.out32 = grads + w_off[l];
+            g.ld_out32 = ldw[l];
+        }
+        gemm_plan(dw[l], F, true, dz[l], ld_act[l + 1], true, acts[l], ld_act[l], dout, din, B, g, sms);
+
+        if (l > 0) {
+            // dz_{l-1} = (dz_l W_l) * act'(A_{l-1})   (M = B, N = din, K = dout)
+            GemmEpi a;
+            a.mode = EPI_ACTGRAD;
+            a.act = act;
+            a.out = dz[l - 1];
+            a.ld_out = ld_act[l];
+            a.aux = acts[l];
+            a.ld_aux = ld_act[l];
+            gemm_plan(da[l], F, false, dz[l], ld_act[l + 1], true, W, ldw[l], B, din, dout, a, sms);
+        }
+        if (opt == OPT_NG_KRON) {
+            GemmEpi m;
+            m.mode = EPI_EMA;
+            m.coef = coef;
+            m.out32 = r_in[l];
+            m.ld_out32 = pad32(din);
+            gemm_plan(mom_in[l], F, true, acts[l], ld_act[l], true, acts[l], ld_act[l], din, din, B, m, sms);
+            m.out32 = r_out[l];
+            m.ld_out32 = pad32(dout);
+            gemm_plan(mom_out[l], F, true, dz[l], ld_act[l + 1], true, dz[l], ld_act[l + 1], dout, dout, B, m, sms);
+        }
+    }
+    if (graph) {
+        cudaGraphExecDestroy(graph);
+        graph = nullptr;
+    }
+    if (use_graph) {
+        cudaStream_t s = stream;
+        cudaGraph_t g;
+        CUDA_THROW(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_step(s);
+        } catch (...) {
+            cudaStreamEndCapture(s, &g);
+            throw;
+        }
+        CUDA_THROW(cudaStreamEndCapture(s, &g));
+        size_t nodes = 0;
+        CUDA_THROW(cudaGraphGetNodes(g, nullptr, &nodes));
+        kernels_per_step = static_cast<long>(nodes);
+        CUDA_THROW(cudaGraphInstantiate(&graph, g, 0));
+        cudaGraphDestroy(g);
+    }
+}
+
+void Replica::enqueue_step(cudaStream_t s) {
+    const bool F = f32();
+    DeviceDataset* ds = bound;
+    launch_gather(ds->features(prec), ds->ld, ds->y, d_rows, d_step, B, dims[0], acts[0], ld_act[0], d_ybatch, F, s);
+    for (int l = 0; l < L; ++l) gemm_launch(fwd[l], s);
+    launch_softmax_ce(zout, ld_act[L], B, dims[L], d_ybatch, dz[L - 1], ld_act[L], ce_rows, F, s);
+    const bool ng = opt == OPT_NG_KRON;
+    for (int l = L - 1; l >= 0; --l) {
+        launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
+                         ng ? grads + b_off[l] : nullptr, d_lr, d_step, d_flags, 2 * l + 1, s);
+        if (l > 0) gemm_launch(da[l], s);  // reads W_l before its update below
+        gemm_launch(dw[l], s);
+    }
+    if (ng) {
+        float* coef = reinterpret_cast<float*>(scal + 16 * (L + 1) + 480);
+        long* tdev = reinterpret_cast<long*>(scal + 16 * (L + 1) + 500);
+        ng_coeff_kernel<<<1, 1, 0, s>>>(tdev, ng_decay, 1.0 / static_cast<double>(B), coef);
+        for (int l = 0; l < L; ++l) {
+            gemm_launch(mom_in[l], s);
+            gemm_launch(mom_out[l], s);
+        }
+        for (int l = 0; l < L; ++l) {
+            ng_precondition_layer(*this, l, s);
+            ng_apply_update(*this, l, s);
+        }
+    }
+    flags_latch_kernel<<<1, 1, 0, s>>>(d_flags, d_step);
+    launch_ce_reduce(ce_rows, B, d_ce, d_step, 1, s);
+}
+
+void Replica::upload_epoch(const uint32_t* rows, const float* lrs, long steps) {
+    if (steps > max_steps) throw std::runtime_error("replica: epoch has more steps than max_steps");
+    cudaStream_t s = stream;
+    CUDA_THROW(cudaMemcpyAsync(d_rows, rows, steps * B * 4, cudaMemcpyHostToDevice, s));
+    CUDA_THROW(cudaMemcpyAsync(d_lr, lrs, steps * 4, cudaMemcpyHostToDevice, s));
+    CUDA_THROW(cudaMemsetAsync(d_step, 0, 4, s));
+}
+
+void Replica::run_step(cudaStream_t s) {
+    if (!bound) throw std::runtime_error("replica: no dataset bound");
+    if (graph)
+        CUDA_THROW(cudaGraphLaunch(graph, s));
+    else
+        enqueue_step(s);
+}
+
+void Replica::check_errors() {
+    DevErr e;
+    unsigned f[4];
+    CUDA_THROW(cudaStreamSynchronize(stream));
+    CUDA_THROW(cudaMemcpy(&e, d_err, sizeof(e), cudaMemcpyDeviceToHost));
+    CUDA_THROW(cudaMemcpy(f, d_flags, sizeof(f), cudaMemcpyDeviceToHost));
+    // Reference order: ng_precondition (Cholesky) throws before sgd_step's checks.
+    if (e.chol_failed) {
+        std::ostringstream os;
+        os << "cholesky_solve: non-positive-definite pivot " << e.chol_value << " at index " << e.chol_index;
+        throw std::runtime_error(os.str());
+    }
+    const unsigned bits = f[1] | f[0];
+    if (bits) {
+        for (int l = 0; l < L; ++l) {
+            if (bits & (1u << (2 * l))) throw std::runtime_error("sgd_step: non-finite weight gradient in layer " + std::to_string(l));
+            if (bits & (1u << (2 * l + 1))) throw std::runtime_error("sgd_step: non-finite bias gradient in layer " + std::to_string(l));
+        }
+    }
+}
+
+double Replica::accuracy(DeviceDataset* ds) {
+    if (ds->n == 0) throw std::runtime_error("accuracy: empty feature matrix");
+    if (ds->d != dims[0])
+        throw std::runtime_error("forward: input has " + std::to_string(ds->d) + " columns, model expects " +
+                                 std::to_string(dims[0]));
+    if (!bound) throw std::runtime_error("replica: bind a training dataset first");
+    cudaStream_t s = stream;
+    const bool F = f32();
+    uint32_t* rows = dalloc<uint32_t>(ds->n);
+    std::vector<uint32_t> h(ds->n);
+    for (long i = 0; i < ds->n; ++i) h[i] = static_cast<uint32_t>(i);
+    unsigned long long* correct = dalloc<unsigned long long>(1);
+    CUDA_THROW(cudaMemcpyAsync(rows, h.data(), ds->n * 4, cudaMemcpyHostToDevice, s));
+    for (long c0 = 0; c0 < ds->n; c0 += B) {
+        const long cb = std::min(B, ds->n - c0);
+        launch_gather(ds->features(prec), ds->ld, ds->y, rows + c0, nullptr, cb, dims[0], acts[0], ld_act[0], d_ybatch,
+                      F, s);
+        for (int l = 0; l < L; ++l) gemm_launch(fwd[l], s);
+        launch_argmax_correct(zout, ld_act[L], cb, dims[L], d_ybatch, correct, s);
+    }
+    unsigned long long hc = 0;
+    CUDA_THROW(cudaMemcpyAsync(&hc, correct, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_THROW(cudaStreamSynchronize(s));
+    dfree(rows);
+    dfree(correct);
+    return static_cast<double>(hc) / static_cast<double>(ds->n);
+}
+
+// Forward for `b` given dataset rows (test hook): returns the last layer's Z.
+void Replica::forward_only(DeviceDataset* ds, const uint32_t* rows_h, long b, float* zh) {
+    if (b > B) throw std::runtime_error("forward: batch larger than the replica's minibatch");
+    cudaStream_t s = stream;
+    uint32_t* rows = dalloc<uint32_t>(b);
+    CUDA_THROW(cudaMemcpyAsync(rows, rows_h, b * 4, cudaMemcpyHostToDevice, s));
+    launch_gather(ds->features(prec), ds->ld, ds->y, rows, nullptr, b, dims[0], acts[0], ld_act[0], d_ybatch, f32(), s);
+    for (int l = 0; l < L; ++l) gemm_launch(fwd[l], s);
+    std::vector<float> h(static_cast<size_t>(b * ld_act[L]));
+    CUDA_THROW(cudaMemcpyAsync(h.data(), zout, h.size() * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_THROW(cudaStreamSynchronize(s));
+    for (long i = 0; i < b; ++i)
+        for (long j = 0; j < dims[L]; ++j) zh[i * dims[L] + j] = h[i * ld_act[L] + j];
+    dfree(rows);
+}
+
+}  // namespace pnb

@@ -1,0 +1,160 @@
+// Device runtime of the B200 trainer: contexts, device-resident datasets,
+// replicas (one model + NG state + workspaces on one GPU) and the fused
+// per-minibatch step. Everything here is C++; the C ABI (capi.cpp) wraps it.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gemm.cuh"
+
+#define CUDA_THROW(x)                                                                              \
+    do {                                                                                           \
+        cudaError_t e_ = (x);                                                                      \
+        if (e_ != cudaSuccess)                                                                     \
+            throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" + \
+                                     __FILE__ + ":" + std::to_string(__LINE__) + ")");             \
+    } while (0)
+
+namespace pnb {
+
+using bf16 = __nv_bfloat16;
+
+struct GemmPlan {
+    CUtensorMap ta, tb;
+    dim3 grid;
+    int smem = 0, M = 0, N = 0, K = 0, bn = 0;
+    GemmEpi ep;
+    void* fn = nullptr;
+};
+
+int choose_bn(int M, int N, int num_sms);
+void gemm_plan(GemmPlan& p, bool f32, bool a_mn, const void* A, long lda, bool b_mn, const void* B, long ldb,
+               int M, int N, int K, const GemmEpi& ep, int num_sms, int force_bn = 0);
+void gemm_launch(const GemmPlan& p, cudaStream_t s);
+
+enum Precision : int { PREC_BF16 = 0, PREC_TF32 = 1 };
+enum Optimizer : int { OPT_SGD = 0, OPT_NG_KRON = 1 };
+
+inline long pad32(long v) { return (v + 31) / 32 * 32; }
+
+struct Context {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    explicit Context(int dev);
+    ~Context();
+};
+
+struct DeviceDataset {
+    Context* ctx;
+    long n = 0, d = 0, ld = 0, classes = 0;
+    float* x32 = nullptr;  // [n x ld] fp32 (zero padded)
+    bf16* x16 = nullptr;   // [n x ld] bf16 copy, created on first bf16 use
+    int32_t* y = nullptr;
+    DeviceDataset(Context* c, const double* x, const int32_t* labels, long n, long d, long classes);
+    ~DeviceDataset();
+    const void* features(Precision p);
+};
+
+// Host-visible error record written by device kernels (pivot failures).
+struct DevErr {
+    int chol_failed;  // 1 if any Cholesky pivot failed
+    int chol_index;
+    float chol_value;
+    int pad;
+};
+
+struct Replica {
+    Context* ctx;
+    cudaStream_t stream = nullptr;  // private stream: local replicas step concurrently
+    std::vector<long> dims;  // input, hidden..., output
+    int L = 0;
+    int act = 0;
+    Precision prec = PREC_BF16;
+    Optimizer opt = OPT_SGD;
+    long B = 0;  // minibatch (fixed per replica)
+    long max_steps = 0;
+    double ng_decay = 0.95, ng_smoothing = 4.0;
+    long ng_t = 0;  // EMA update count (same for every layer)
+
+    // padded flat parameter layout: per layer W [dout x ldw] then b [pad32(dout)]
+    std::vector<long> ldw, w_off, b_off;
+    long n_pad = 0;  // floats in the padded parameter buffer
+    float* params = nullptr;
+    bf16* wshadow = nullptr;  // bf16 operand copy of the weights (bf16 mode), same offsets
+    float* grads = nullptr;   // padded fp32 gradients (NG mode: G then preconditioned)
+
+    // activations: act[0] = gathered input batch; act[l+1] = output of layer l (hidden only)
+    std::vector<void*> acts;
+    std::vector<long> ld_act;
+    float* zout = nullptr;  // last layer pre-activation [B x ld_act[L]]
+    std::vector<void*> dz;  // per layer [B x ld_act[l+1]] (op dtype)
+    std::vector<float*> r_in, r_out;  // NG factors [n x pad32(n)]
+    float* chol_a = nullptr;  // Cholesky workspace (largest factor)
+    float* chol_b = nullptr;
+    float* tbuf = nullptr;    // transpose / solve workspace (largest W)
+    double* scal = nullptr;   // per-layer scalars: traces, norms (device)
+
+    // per-epoch device state
+    int* d_step = nullptr;
+    float* d_lr = nullptr;        // [max_steps]
+    uint32_t* d_rows = nullptr;   // [max_steps * B] dataset row ids
+    int32_t* d_ybatch = nullptr;  // [B]
+    float* ce_rows = nullptr;     // [B]
+    double* d_ce = nullptr;       // [max_steps] batch-mean CE
+    unsigned* d_flags = nullptr;  // non-finite weight/bias grad bits (2 per layer)
+    DevErr* d_err = nullptr;
+
+    DeviceDataset* bound = nullptr;  // dataset the plans/graph were built for
+    std::vector<GemmPlan> fwd, dw, da, mom_in, mom_out;
+    cudaGraphExec_t graph = nullptr;
+    bool use_graph = true;
+    long kernels_per_step = 0;
+
+    Replica(Context* c, const std::vector<long>& dims, int act, Precision p, Optimizer o, long batch,
+            long max_steps, double decay, double smoothing);
+    ~Replica();
+
+    bool f32() const { return prec == PREC_TF32; }
+    size_t esz() const { return f32() ? 4 : 2; }
+    void set_params(const double* flat);  // canonical flatten order (network.cpp:238-248)
+    void get_params(double* flat) const;
+    void set_ng_state(const double* factors, long t);
+    void get_ng_state(double* factors) const;
+
+    void bind(DeviceDataset* ds);  // build GEMM plans + graph for this dataset
+    void upload_epoch(const uint32_t* rows, const float* lrs, long steps);
+    void run_step(cudaStream_t s);  // one minibatch (graph or eager)
+    void enqueue_step(cudaStream_t s);
+    void sync_shadow(cudaStream_t s);  // recompute bf16 copy after external param writes
+    void check_errors();               // throws the reference's messages
+
+    // debug/test hooks
+    void forward_only(DeviceDataset* ds, const uint32_t* rows, long b, float* zout_host);
+    double accuracy(DeviceDataset* ds);
+};
+
+// ----------------------------------------------------------- kernels.cu
+void launch_gather(const void* x, long ldx, const int32_t* y, const uint32_t* rows, const int* step, long B,
+                   long d, void* out, long ldo, int32_t* yout, bool f32, cudaStream_t s);
+void launch_softmax_ce(const float* z, long ldz, long B, long C, const int32_t* y, void* dz, long lddz,
+                       float* ce_rows, bool f32, cudaStream_t s);
+void launch_ce_reduce(const float* ce_rows, long B, double* d_ce, int* step, int advance, cudaStream_t s);
+void launch_bias_grad(const void* dz, long lddz, long B, long C, bool f32, float* bias, float* gb, const float* lr,
+                      const int* step, unsigned* flags, unsigned bit, cudaStream_t s);
+void launch_f32_to_bf16_rows(const float* src, long ld, long rows, long cols, bf16* dst, cudaStream_t s);
+void launch_convert_dataset(const float* x32, long n, long ld, bf16* x16, cudaStream_t s);
+void launch_argmax_correct(const float* z, long ldz, long B, long C, const int32_t* y, unsigned long long* correct,
+                           cudaStream_t s);
+
+// NG kron-full (SIMT fp32, ng.cu)
+void ng_precondition_layer(Replica& r, int l, cudaStream_t s);
+void ng_apply_update(Replica& r, int l, cudaStream_t s);
+
+}  // namespace pnb
