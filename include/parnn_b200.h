@@ -25,7 +25,9 @@ extern "C" {
 #define PARNN_OK 0
 #define PARNN_ERR (-1)
 
-enum parnn_precision { PARNN_BF16 = 0, PARNN_TF32 = 1 };
+/* GEMM operand precision (fp32 accumulation always): BF16, TF32, or FP32 =
+ * fp32-accurate 3xTF32 split on the tensor cores (the parity mode). */
+enum parnn_precision { PARNN_BF16 = 0, PARNN_TF32 = 1, PARNN_FP32 = 2 };
 enum parnn_optimizer { PARNN_SGD = 0, PARNN_NGSGD = 1 };    /* parallel.hpp:14-18 */
 enum parnn_lr_variant { PARNN_NEWBOB = 0, PARNN_EXPONENTIAL = 1 }; /* optimizer.hpp:57 */
 enum parnn_activation { PARNN_SIGMOID = 0, PARNN_TANH = 1 };   /* network.hpp:16 */
@@ -113,6 +115,15 @@ int parnn_replica_forward(parnn_replica* r, parnn_dataset* ds, const uint32_t* r
 int parnn_replica_accuracy(parnn_replica* r, parnn_dataset* ds, double* acc);
 /* number of device kernels one step launches */
 int parnn_replica_kernels_per_step(parnn_replica* r, uint64_t* n);
+/* Device time (CUDA events on the replica's stream) of `steps` graph launches. */
+int parnn_replica_time_steps(parnn_replica* r, uint64_t steps, double* ms);
+/* Eager profiled steps: per-region average ms (events between launches on the
+ * replica stream) and algorithmic flops; names newline-separated "kind:layer". */
+int parnn_replica_profile(parnn_replica* r, uint64_t steps, char* names, uint64_t names_cap, double* ms,
+                          double* flops, uint64_t cap, uint64_t* n_regions);
+/* Overwrite dataset rows [row0, row0+n) from host fp32 features (+ labels):
+ * the per-step host->device input copy of the end-to-end path. */
+int parnn_dataset_write_f32(parnn_dataset* ds, const float* x, const int32_t* y, uint64_t row0, uint64_t n);
 
 /* ---------------- averaging / multi-GPU ---------------------------------- */
 /* NCCL communicator across processes (one per GPU). */
@@ -122,6 +133,11 @@ int parnn_comm_destroy(parnn_comm* c);
 /* allreduce_average (parallel.cpp:40-59) over the local replicas (+ comm):
  * every replica is replaced by the mean over m_total workers. */
 int parnn_average(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_t m_total);
+/* worker_epoch's inner loop (parallel.cpp:106-137) for benchmarking: `steps`
+ * minibatch updates on every local replica with an averaging event every
+ * avg_frequency updates (and one closing the window); device time in ms. */
+int parnn_run_steps(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_t m_total, uint64_t steps,
+                    uint64_t avg_frequency, double* ms);
 
 /* ---------------- the train loop ----------------------------------------- */
 /* ParallelPlan (parallel.hpp:22-27) + TrainOptions (parallel.hpp:31-38) + placement. */

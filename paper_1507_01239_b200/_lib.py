@@ -70,10 +70,14 @@ SIGNATURES = [
     ("parnn_replica_forward", c_int, [vp, vp, vp, c_u64, vp]),
     ("parnn_replica_accuracy", c_int, [vp, vp, vp]),
     ("parnn_replica_kernels_per_step", c_int, [vp, vp]),
+    ("parnn_replica_time_steps", c_int, [vp, c_u64, vp]),
+    ("parnn_replica_profile", c_int, [vp, c_u64, vp, c_u64, vp, vp, c_u64, vp]),
+    ("parnn_dataset_write_f32", c_int, [vp, vp, vp, c_u64, c_u64]),
     ("parnn_comm_unique_id", c_int, [vp]),
     ("parnn_comm_create", c_int, [vp, vp, c_int, c_int, vp]),
     ("parnn_comm_destroy", c_int, [vp]),
     ("parnn_average", c_int, [vp, c_int, vp, c_u64]),
+    ("parnn_run_steps", c_int, [vp, c_int, vp, c_u64, c_u64, c_u64, vp]),
     ("parnn_train", c_int, [vp, vp, vp, vp, c_int, vp, vp, vp, vp, vp, vp]),
     ("parnn_rbm_create", c_int, [vp, c_u64, c_u64, c_int, c_u64, c_int, vp]),
     ("parnn_rbm_destroy", c_int, [vp]),

@@ -329,6 +329,61 @@ int parnn_replica_kernels_per_step(parnn_replica* r, uint64_t* n) {
     });
 }
 
+int parnn_replica_time_steps(parnn_replica* r, uint64_t steps, double* ms) {
+    return guarded([&] { *ms = r->r->time_steps(static_cast<long>(steps)); });
+}
+
+int parnn_replica_profile(parnn_replica* r, uint64_t steps, char* names, uint64_t names_cap, double* ms,
+                          double* flops, uint64_t cap, uint64_t* n_regions) {
+    return guarded([&] {
+        std::vector<std::string> nm;
+        std::vector<double> t, f;
+        r->r->profile_steps(static_cast<long>(steps), nm, t, f);
+        std::string joined;
+        for (auto& x : nm) joined += x + "\n";
+        if (joined.size() + 1 > names_cap || nm.size() > cap) throw std::runtime_error("profile: buffers too small");
+        std::memcpy(names, joined.c_str(), joined.size() + 1);
+        for (size_t i = 0; i < nm.size(); ++i) {
+            ms[i] = t[i];
+            flops[i] = f[i];
+        }
+        *n_regions = nm.size();
+    });
+}
+
+int parnn_run_steps(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_t m_total, uint64_t steps,
+                    uint64_t avg_frequency, double* ms) {
+    return guarded([&] {
+        if (n_local <= 0) throw std::runtime_error("run_steps: no replicas");
+        if (avg_frequency == 0) throw std::runtime_error("train_parallel: avg_frequency must be >= 1");
+        std::vector<Replica*> v;
+        for (int i = 0; i < n_local; ++i) v.push_back(reps[i]->r.get());
+        Context* ctx = v[0]->ctx;
+        Averager avg(ctx, v, comm ? comm->c.get() : nullptr, static_cast<long>(m_total));
+        cudaEvent_t a, b;
+        CUDA_THROW(cudaEventCreate(&a));
+        CUDA_THROW(cudaEventCreate(&b));
+        for (Replica* r : v) CUDA_THROW(cudaStreamSynchronize(r->stream));
+        CUDA_THROW(cudaEventRecord(a, ctx->stream));
+        for (Replica* r : v) CUDA_THROW(cudaStreamWaitEvent(r->stream, a, 0));
+        for (uint64_t s = 0; s < steps; ++s) {
+            for (Replica* r : v) r->run_step(r->stream);
+            if ((s + 1) % avg_frequency == 0 || s + 1 == steps) avg.run();  // last event closes the window
+        }
+        CUDA_THROW(cudaEventRecord(b, ctx->stream));
+        CUDA_THROW(cudaEventSynchronize(b));
+        float t = 0.f;
+        CUDA_THROW(cudaEventElapsedTime(&t, a, b));
+        *ms = t;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    });
+}
+
+int parnn_dataset_write_f32(parnn_dataset* ds, const float* x, const int32_t* y, uint64_t row0, uint64_t n) {
+    return guarded([&] { ds->d->write_rows(x, y, static_cast<long>(row0), static_cast<long>(n), ds->d->ctx->stream); });
+}
+
 int parnn_comm_unique_id(unsigned char out[128]) {
     return guarded([&] { nccl_unique_id(out); });
 }

@@ -48,18 +48,19 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
     return m;
 }
 
-template <int BN>
+template <int BN, bool SPLIT>
 constexpr int stages_for() {
+    if (SPLIT) return BN == 256 ? 2 : (BN == 128 ? 3 : 4);
     return BN == 256 ? 4 : (BN == 128 ? 6 : 8);
 }
 
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, int, int, int, GemmEpi);
 
-template <typename T, int BN, bool AMN, bool BMN>
+template <typename T, int BN, bool AMN, bool BMN, bool SPLIT>
 KernelFn kernel_ptr(int* smem) {
-    constexpr int ST = stages_for<BN>();
-    *smem = GemmSmem<BN, ST, T>::kBytes;
-    auto k = &gemm_tc_kernel<T, BN, ST, AMN, BMN>;
+    constexpr int ST = stages_for<BN, SPLIT>();
+    *smem = GemmSmem<BN, ST, T, SPLIT>::kBytes;
+    auto k = &gemm_tc_kernel<T, BN, ST, AMN, BMN, SPLIT>;
     static bool configured = false;
     if (!configured) {
         CUDA_THROW(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem));
@@ -68,20 +69,20 @@ KernelFn kernel_ptr(int* smem) {
     return reinterpret_cast<KernelFn>(k);
 }
 
-template <typename T, int BN>
+template <typename T, int BN, bool SPLIT>
 KernelFn pick_major(bool amn, bool bmn, int* smem) {
-    if (!amn && !bmn) return kernel_ptr<T, BN, false, false>(smem);
-    if (amn && bmn) return kernel_ptr<T, BN, true, true>(smem);
-    if (!amn && bmn) return kernel_ptr<T, BN, false, true>(smem);
-    return kernel_ptr<T, BN, true, false>(smem);
+    if (!amn && !bmn) return kernel_ptr<T, BN, false, false, SPLIT>(smem);
+    if (amn && bmn) return kernel_ptr<T, BN, true, true, SPLIT>(smem);
+    if (!amn && bmn) return kernel_ptr<T, BN, false, true, SPLIT>(smem);
+    return kernel_ptr<T, BN, true, false, SPLIT>(smem);
 }
 
-template <typename T>
+template <typename T, bool SPLIT>
 KernelFn pick(int bn, bool amn, bool bmn, int* smem) {
     switch (bn) {
-        case 256: return pick_major<T, 256>(amn, bmn, smem);
-        case 128: return pick_major<T, 128>(amn, bmn, smem);
-        default: return pick_major<T, 64>(amn, bmn, smem);
+        case 256: return pick_major<T, 256, SPLIT>(amn, bmn, smem);
+        case 128: return pick_major<T, 128, SPLIT>(amn, bmn, smem);
+        default: return pick_major<T, 64, SPLIT>(amn, bmn, smem);
     }
 }
 
@@ -96,9 +97,10 @@ int choose_bn(int M, int N, int num_sms) {
     return 64;
 }
 
-void gemm_plan(GemmPlan& p, bool f32, bool a_mn, const void* A, long lda, bool b_mn, const void* B, long ldb,
+void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b_mn, const void* B, long ldb,
                int M, int N, int K, const GemmEpi& ep, int num_sms, int force_bn) {
     if (M <= 0 || N <= 0 || K <= 0) throw std::runtime_error("gemm: empty problem");
+    const bool f32 = prec != 0, split = prec == 2;
     const int bn = force_bn ? force_bn : choose_bn(M, N, num_sms);
     const uint32_t atom = f32 ? 32 : 64;  // elements per 128-B row
     const uint32_t bk = atom;
@@ -110,13 +112,19 @@ void gemm_plan(GemmPlan& p, bool f32, bool a_mn, const void* A, long lda, bool b
     p.K = K;
     p.ep = ep;
     p.grid = dim3((N + bn - 1) / bn, (M + 127) / 128, 1);
-    p.fn = reinterpret_cast<void*>(f32 ? pick<float>(bn, a_mn, b_mn, &p.smem) : pick<__nv_bfloat16>(bn, a_mn, b_mn, &p.smem));
+    if (split)
+        p.fn = reinterpret_cast<void*>(pick<float, true>(bn, a_mn, b_mn, &p.smem));
+    else if (f32)
+        p.fn = reinterpret_cast<void*>(pick<float, false>(bn, a_mn, b_mn, &p.smem));
+    else
+        p.fn = reinterpret_cast<void*>(pick<__nv_bfloat16, false>(bn, a_mn, b_mn, &p.smem));
     p.bn = bn;
+    p.threads = split ? 256 : 128;
 }
 
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {
     auto fn = reinterpret_cast<KernelFn>(p.fn);
-    fn<<<p.grid, 128, p.smem, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.ep);
+    fn<<<p.grid, p.threads, p.smem, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.ep);
     CUDA_THROW(cudaGetLastError());
 }
 

@@ -155,7 +155,7 @@ __device__ __forceinline__ void load_row32(const T* src, float (&v)[32], int val
     }
 }
 
-template <int BN, int STAGES, typename T>
+template <int BN, int STAGES, typename T, bool SPLIT = false>
 struct GemmSmem {
     static constexpr int kElem = sizeof(T);
     static constexpr int kBK = 128 / kElem;    // K per stage (one 128-B swizzle row)
@@ -163,23 +163,30 @@ struct GemmSmem {
     static constexpr int kAtom = 128 / kElem;  // MN elements per 128-B atom
     static constexpr int kABytes = 128 * 128;
     static constexpr int kBBytes = BN * 128;
-    static constexpr int kStage = kABytes + kBBytes;
-    static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kLoad = kABytes + kBBytes;          // bytes TMA brings per stage
+    static constexpr int kStage = kLoad * (SPLIT ? 2 : 1);   // + low-part copies for 3xTF32
+    static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 512 /*barriers*/;
 };
 
-template <typename T, int BN, int STAGES, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(128, 1)
+// SPLIT (fp32 mode, T = float): 3xTF32. Four extra warps split every staged
+// operand x into hi = x with the low 13 mantissa bits cleared (exact TF32,
+// written back in place) and lo = x - hi (exact in fp32), then the MMA warp
+// accumulates hi*hi + hi*lo + lo*hi: relative error ~2^-21 instead of 2^-11.
+template <typename T, int BN, int STAGES, bool A_MN, bool B_MN, bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, GemmEpi ep) {
-    using S = GemmSmem<BN, STAGES, T>;
+    using S = GemmSmem<BN, STAGES, T, SPLIT>;
     constexpr bool kTf32 = OpTraits<T>::kTf32;
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+    static_assert(!SPLIT || kTf32, "3xTF32 split needs fp32 operands");
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
     uint64_t* empty = full + STAGES;
-    uint64_t* done = empty + STAGES;
+    uint64_t* split_done = empty + STAGES;
+    uint64_t* done = split_done + STAGES;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
     const int warp = threadIdx.x >> 5;
@@ -192,6 +199,7 @@ __global__ void __launch_bounds__(128, 1)
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
+            mbar_init(&split_done[s], 128);
         }
         mbar_init(done, 1);
         fence_barrier_init();
@@ -211,7 +219,7 @@ __global__ void __launch_bounds__(128, 1)
             if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
             uint8_t* sa = smem + s * S::kStage;
             uint8_t* sb = sa + S::kABytes;
-            mbar_arrive_expect_tx(&full[s], S::kStage);
+            mbar_arrive_expect_tx(&full[s], S::kLoad);
             const int k0 = kb * S::kBK;
             if constexpr (!A_MN) {
                 tma_load_2d(sa, &tmA, &full[s], k0, m0);
@@ -231,27 +239,63 @@ __global__ void __launch_bounds__(128, 1)
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer ----------------
         constexpr uint32_t idesc = make_idesc(OpTraits<T>::kFmt, A_MN ? 1 : 0, B_MN ? 1 : 0, 128, BN);
+        constexpr uint32_t kMnLayout = kTf32 ? 1 : 2;  // BASE32B for TF32 MN-major
+        constexpr uint32_t kMnSbo = kTf32 ? 512 : 1024;
+        auto desc_a = [&](uint32_t base, int k) {
+            return A_MN ? smem_desc_sw128(base + k * S::kUK * 128, S::kBK * 128, kMnSbo, kMnLayout)
+                        : smem_desc_sw128(base + k * 32, 16, 1024);
+        };
+        auto desc_b = [&](uint32_t base, int k) {
+            return B_MN ? smem_desc_sw128(base + k * S::kUK * 128, S::kBK * 128, kMnSbo, kMnLayout)
+                        : smem_desc_sw128(base + k * 32, 16, 1024);
+        };
         for (int kb = 0; kb < nk; ++kb) {
             const int s = kb % STAGES;
-            mbar_wait(&full[s], (kb / STAGES) & 1);
+            mbar_wait(SPLIT ? &split_done[s] : &full[s], (kb / STAGES) & 1);
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + s * S::kStage);
             const uint32_t sb = sa + S::kABytes;
 #pragma unroll
             for (int k = 0; k < S::kBK / S::kUK; ++k) {
-                constexpr uint32_t kMnLayout = kTf32 ? 1 : 2;      // BASE32B for TF32 MN-major
-                constexpr uint32_t kMnSbo = kTf32 ? 512 : 1024;
-                const uint64_t ad = A_MN ? smem_desc_sw128(sa + k * S::kUK * 128, S::kBK * 128, kMnSbo, kMnLayout)
-                                         : smem_desc_sw128(sa + k * 32, 16, 1024);
-                const uint64_t bd = B_MN ? smem_desc_sw128(sb + k * S::kUK * 128, S::kBK * 128, kMnSbo, kMnLayout)
-                                         : smem_desc_sw128(sb + k * 32, 16, 1024);
-                umma<kTf32>(tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                umma<kTf32>(tmem, desc_a(sa, k), desc_b(sb, k), idesc, (kb | k) != 0 ? 1u : 0u);
+                if constexpr (SPLIT) {
+                    const uint32_t sal = sa + S::kLoad, sbl = sb + S::kLoad;
+                    umma<kTf32>(tmem, desc_a(sa, k), desc_b(sbl, k), idesc, 1u);
+                    umma<kTf32>(tmem, desc_a(sal, k), desc_b(sb, k), idesc, 1u);
+                }
             }
             umma_commit(&empty[s]);
         }
         umma_commit(done);
+    } else if (SPLIT && warp >= 4) {
+        // ---------------- 3xTF32 splitters (warps 4-7) ----------------
+        const int t = threadIdx.x - 128;
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % STAGES;
+            mbar_wait(&full[s], (kb / STAGES) & 1);
+            float4* hi = reinterpret_cast<float4*>(smem + s * S::kStage);
+            float4* lo = reinterpret_cast<float4*>(smem + s * S::kStage + S::kLoad);
+#pragma unroll 4
+            for (int i = t; i < S::kLoad / 16; i += 128) {
+                float4 x = hi[i], h, l;
+                h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+                h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+                h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+                h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+                l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+                hi[i] = h;
+                lo[i] = l;
+            }
+            fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+            mbar_arrive(&split_done[s]);
+        }
     }
     __syncwarp();
+    if (SPLIT && warp >= 4) {  // splitters take no part in the epilogue
+        tc_fence_before();
+        __syncthreads();
+        return;
+    }
 
     // ---------------- epilogue: TMEM -> registers -> global ----------------
     mbar_wait(done, 0);
@@ -346,7 +390,7 @@ __global__ void __launch_bounds__(128, 1)
     if (bad && ep.flag) atomicOr(ep.flag, 1u << ep.flag_bit);
 
     tc_fence_before();
-    __syncthreads();
+    __syncthreads();  // (SPLIT: matched by the splitters' barrier above)
     if (warp == 1) tmem_dealloc<(BN < 32 ? 32 : BN)>(tmem);
 }
 

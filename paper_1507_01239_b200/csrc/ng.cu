@@ -366,20 +366,29 @@ void ng_precondition_layer(Replica& r, int l, cudaStream_t s) {
     trace_lambda_kernel<<<1, 256, 0, s>>>(r.r_out[l], dout, ldo, r.ng_smoothing, sc + 5);
     shift_copy_kernel<<<grid_for(dout * ldo), 256, 0, s>>>(r.r_out[l], dout, ldo, sc + 5, r.chol_a);
     shift_copy_kernel<<<grid_for(din * ldi), 256, 0, s>>>(r.r_in[l], din, ldi, sc + 4, r.chol_b);
+    r.mark("ng_smooth", l, 0, s);
+    const double fo = static_cast<double>(dout), fi = static_cast<double>(din);
     cholesky(r.chol_a, dout, ldo, r.d_err, s);
+    r.mark("ng_potrf", l, fo * fo * fo / 3.0, s);
     cholesky(r.chol_b, din, ldi, r.d_err, s);
+    r.mark("ng_potrf", l, fi * fi * fi / 3.0, s);
 
     sumsq(g, r.ldw[l], dout, din, part, sc + 0, s);
     sumsq(gb, 1, dout, 1, part, sc + 1, s);
     pack_rhs_kernel<<<grid_for(dout * ldt), 256, 0, s>>>(g, r.ldw[l], gb, dout, din, t1, ldt);
+    r.mark("ng_norms", l, 0, s);
     chol_solve(r.chol_a, dout, ldo, t1, ldt, din + 1, s);  // S_out^-1 [G | g_b]
+    r.mark("ng_trsm", l, 2.0 * fo * fo * (fi + 1.0), s);
     {
         dim3 grid((din + 31) / 32, (dout + 31) / 32), block(32, 8);
         transpose_kernel<<<grid, block, 0, s>>>(t1, ldt, dout, din, t2, ldo);
     }
+    r.mark("ng_transpose", l, 0, s);
     chol_solve(r.chol_b, din, ldi, t2, ldo, dout, s);  // S_in^-1 (S_out^-1 G)^T
+    r.mark("ng_trsm", l, 2.0 * fi * fi * fo, s);
     sumsq(t2, ldo, din, dout, part, sc + 2, s);
     sumsq(t1 + din, ldt, dout, 1, part, sc + 3, s);
+    r.mark("ng_norms", l, 0, s);
 }
 
 void ng_apply_update(Replica& r, int l, cudaStream_t s) {
@@ -395,6 +404,7 @@ void ng_apply_update(Replica& r, int l, cudaStream_t s) {
     ng_update_kernel<<<grid_for(dout * din), 256, 0, s>>>(
         r.params + r.w_off[l], r.ldw[l], r.params + r.b_off[l], r.wshadow ? r.wshadow + r.w_off[l] : nullptr, t1,
         ldt, t1 + din, ldt, dout, din, r.scal + 16 * l, r.d_lr, r.d_step, r.d_flags, 2 * l);
+    r.mark("ng_update", l, 0, s);
 }
 
 }  // namespace pnb

@@ -212,25 +212,25 @@ void RbmDevice::plan(long b) {
     e.bias = hb;
     e.out = pn;
     e.ld_out = ldh;
-    gemm_plan(g_pos, F, false, xr, ldv, false, Wop, ldv, (int)b, (int)h, (int)v, e, sms);
+    gemm_plan(g_pos, prec, false, xr, ldv, false, Wop, ldv, (int)b, (int)h, (int)v, e, sms);
     GemmEpi r;
     r.mode = EPI_FWD_ACT;
     r.act = gaussian ? 2 : 0;  // reconstruct_mean: linear for gaussian visibles
     r.bias = vb;
     r.out = xr + b * ldv * es;
     r.ld_out = ldv;
-    gemm_plan(g_recon, F, false, HS, ldh, true, Wop, ldv, (int)b, (int)v, (int)h, r, sms);
+    gemm_plan(g_recon, prec, false, HS, ldh, true, Wop, ldv, (int)b, (int)v, (int)h, r, sms);
     GemmEpi n = e;
     n.out_scale = -1.f;
     n.out = pn + b * ldh * es;
-    gemm_plan(g_neg, F, false, xr + b * ldv * es, ldv, false, Wop, ldv, (int)b, (int)h, (int)v, n, sms);
+    gemm_plan(g_neg, prec, false, xr + b * ldv * es, ldv, false, Wop, ldv, (int)b, (int)h, (int)v, n, sms);
     GemmEpi u;
     u.mode = EPI_AXPY;
     u.out32 = W;
     u.ld_out32 = ldv;
     u.shadow = Ws;
     u.ld_shadow = ldv;
-    gemm_plan(g_upd, F, true, pn, ldh, true, xr, ldv, (int)h, (int)v, (int)(2 * b), u, sms);
+    gemm_plan(g_upd, prec, true, pn, ldh, true, xr, ldv, (int)h, (int)v, (int)(2 * b), u, sms);
     planned_b = b;
 }
 

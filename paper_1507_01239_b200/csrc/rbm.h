@@ -27,7 +27,7 @@ struct RbmDevice {
 
     RbmDevice(Context* c, long visible, long hidden, bool gaussian, long batch, Precision p);
     ~RbmDevice();
-    bool f32() const { return prec == PREC_TF32; }
+    bool f32() const { return prec != PREC_BF16; }
     void set_params(const double* p);  // [W, v_bias, h_bias]
     void get_params(double* p);
     void plan(long b);

@@ -83,13 +83,20 @@ DeviceDataset::~DeviceDataset() {
 }
 
 const void* DeviceDataset::features(Precision p) {
-    if (p == PREC_TF32) return x32;
+    if (p != PREC_BF16) return x32;
     if (!x16) {
         x16 = dalloc<bf16>(static_cast<size_t>(n * ld));
         launch_convert_dataset(x32, n, ld, x16, ctx->stream);
         CUDA_THROW(cudaStreamSynchronize(ctx->stream));
     }
     return x16;
+}
+
+void DeviceDataset::write_rows(const float* x, const int32_t* labels, long row0, long cnt, cudaStream_t s) {
+    if (row0 < 0 || row0 + cnt > n) throw std::runtime_error("dataset: write beyond the dataset");
+    CUDA_THROW(cudaMemcpy2DAsync(x32 + row0 * ld, ld * 4, x, d * 4, d * 4, cnt, cudaMemcpyHostToDevice, s));
+    if (labels) CUDA_THROW(cudaMemcpyAsync(y + row0, labels, cnt * 4, cudaMemcpyHostToDevice, s));
+    if (x16) launch_f32_to_bf16_rows(x32 + row0 * ld, ld, cnt, ld, x16 + row0 * ld, s);
 }
 
 Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision p, Optimizer o, long batch,
@@ -271,7 +278,7 @@ void Replica::bind(DeviceDataset* ds) {
             e.ld_out32 = ld_act[L];
         }
         e.bias = params + b_off[l];
-        gemm_plan(fwd[l], F, false, acts[l], ld_act[l], false, W, ldw[l], B, dout, din, e, sms);
+        gemm_plan(fwd[l], prec, false, acts[l], ld_act[l], false, W, ldw[l], B, dout, din, e, sms);
 
         // dW = dz^T A_prev / B  (M = dout, N = din, K = B)
         GemmEpi g;
@@ -291,7 +298,7 @@ void Replica::bind(DeviceDataset* ds) {
             g.out32 = grads + w_off[l];
             g.ld_out32 = ldw[l];
         }
-        gemm_plan(dw[l], F, true, dz[l], ld_act[l + 1], true, acts[l], ld_act[l], dout, din, B, g, sms);
+        gemm_plan(dw[l], prec, true, dz[l], ld_act[l + 1], true, acts[l], ld_act[l], dout, din, B, g, sms);
 
         if (l > 0) {
             // dz_{l-1} = (dz_l W_l) * act'(A_{l-1})   (M = B, N = din, K = dout)
@@ -302,7 +309,7 @@ void Replica::bind(DeviceDataset* ds) {
             a.ld_out = ld_act[l];
             a.aux = acts[l];
             a.ld_aux = ld_act[l];
-            gemm_plan(da[l], F, false, dz[l], ld_act[l + 1], true, W, ldw[l], B, din, dout, a, sms);
+            gemm_plan(da[l], prec, false, dz[l], ld_act[l + 1], true, W, ldw[l], B, din, dout, a, sms);
         }
         if (opt == OPT_NG_KRON) {
             GemmEpi m;
@@ -310,10 +317,10 @@ void Replica::bind(DeviceDataset* ds) {
             m.coef = coef;
             m.out32 = r_in[l];
             m.ld_out32 = pad32(din);
-            gemm_plan(mom_in[l], F, true, acts[l], ld_act[l], true, acts[l], ld_act[l], din, din, B, m, sms);
+            gemm_plan(mom_in[l], prec, true, acts[l], ld_act[l], true, acts[l], ld_act[l], din, din, B, m, sms);
             m.out32 = r_out[l];
             m.ld_out32 = pad32(dout);
-            gemm_plan(mom_out[l], F, true, dz[l], ld_act[l + 1], true, dz[l], ld_act[l + 1], dout, dout, B, m, sms);
+            gemm_plan(mom_out[l], prec, true, dz[l], ld_act[l + 1], true, dz[l], ld_act[l + 1], dout, dout, B, m, sms);
         }
     }
     if (graph) {
@@ -339,18 +346,40 @@ void Replica::bind(DeviceDataset* ds) {
     }
 }
 
+void Replica::mark(const char* kind, int layer, double flops, cudaStream_t s) {
+    if (!prof) return;
+    cudaEvent_t e;
+    CUDA_THROW(cudaEventCreate(&e));
+    CUDA_THROW(cudaEventRecord(e, s));
+    prof->events.push_back(e);
+    prof->names.push_back(std::string(kind) + ":" + std::to_string(layer));
+    prof->flops.push_back(flops);
+}
+
 void Replica::enqueue_step(cudaStream_t s) {
     const bool F = f32();
     DeviceDataset* ds = bound;
+    auto gf = [](const GemmPlan& p) { return 2.0 * p.M * p.N * p.K; };
+    mark("start", -1, 0, s);
     launch_gather(ds->features(prec), ds->ld, ds->y, d_rows, d_step, B, dims[0], acts[0], ld_act[0], d_ybatch, F, s);
-    for (int l = 0; l < L; ++l) gemm_launch(fwd[l], s);
+    mark("gather", 0, 0, s);
+    for (int l = 0; l < L; ++l) {
+        gemm_launch(fwd[l], s);
+        mark("gemm_fwd", l, gf(fwd[l]), s);
+    }
     launch_softmax_ce(zout, ld_act[L], B, dims[L], d_ybatch, dz[L - 1], ld_act[L], ce_rows, F, s);
+    mark("softmax_ce", L - 1, 0, s);
     const bool ng = opt == OPT_NG_KRON;
     for (int l = L - 1; l >= 0; --l) {
         launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
                          ng ? grads + b_off[l] : nullptr, d_lr, d_step, d_flags, 2 * l + 1, s);
-        if (l > 0) gemm_launch(da[l], s);  // reads W_l before its update below
+        mark("bias_grad", l, 0, s);
+        if (l > 0) {
+            gemm_launch(da[l], s);  // reads W_l before its update below
+            mark("gemm_da", l, gf(da[l]), s);
+        }
         gemm_launch(dw[l], s);
+        mark(ng ? "gemm_dw" : "gemm_dw_sgd", l, gf(dw[l]), s);
     }
     if (ng) {
         float* coef = reinterpret_cast<float*>(scal + 16 * (L + 1) + 480);
@@ -359,6 +388,7 @@ void Replica::enqueue_step(cudaStream_t s) {
         for (int l = 0; l < L; ++l) {
             gemm_launch(mom_in[l], s);
             gemm_launch(mom_out[l], s);
+            mark("gemm_ng_moments", l, gf(mom_in[l]) + gf(mom_out[l]), s);
         }
         for (int l = 0; l < L; ++l) {
             ng_precondition_layer(*this, l, s);
@@ -367,6 +397,53 @@ void Replica::enqueue_step(cudaStream_t s) {
     }
     flags_latch_kernel<<<1, 1, 0, s>>>(d_flags, d_step);
     launch_ce_reduce(ce_rows, B, d_ce, d_step, 1, s);
+    mark("ce_reduce", 0, 0, s);
+}
+
+void Replica::profile_steps(long steps, std::vector<std::string>& names, std::vector<double>& ms,
+                            std::vector<double>& flops) {
+    if (!bound) throw std::runtime_error("replica: no dataset bound");
+    names.clear();
+    ms.clear();
+    flops.clear();
+    for (long it = 0; it < steps; ++it) {
+        Profile p;
+        prof = &p;
+        try {
+            enqueue_step(stream);
+        } catch (...) {
+            prof = nullptr;
+            throw;
+        }
+        prof = nullptr;
+        CUDA_THROW(cudaStreamSynchronize(stream));
+        for (size_t i = 1; i < p.events.size(); ++i) {
+            float t = 0.f;
+            CUDA_THROW(cudaEventElapsedTime(&t, p.events[i - 1], p.events[i]));
+            if (it == 0) {
+                names.push_back(p.names[i]);
+                ms.push_back(0.0);
+                flops.push_back(p.flops[i]);
+            }
+            ms[i - 1] += t / static_cast<double>(steps);
+        }
+        for (auto e : p.events) cudaEventDestroy(e);
+    }
+}
+
+double Replica::time_steps(long steps) {
+    cudaEvent_t a, b;
+    CUDA_THROW(cudaEventCreate(&a));
+    CUDA_THROW(cudaEventCreate(&b));
+    CUDA_THROW(cudaEventRecord(a, stream));
+    for (long i = 0; i < steps; ++i) run_step(stream);
+    CUDA_THROW(cudaEventRecord(b, stream));
+    CUDA_THROW(cudaEventSynchronize(b));
+    float t = 0.f;
+    CUDA_THROW(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return t;
 }
 
 void Replica::upload_epoch(const uint32_t* rows, const float* lrs, long steps) {

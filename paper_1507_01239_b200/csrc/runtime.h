@@ -28,17 +28,18 @@ using bf16 = __nv_bfloat16;
 struct GemmPlan {
     CUtensorMap ta, tb;
     dim3 grid;
-    int smem = 0, M = 0, N = 0, K = 0, bn = 0;
+    int smem = 0, M = 0, N = 0, K = 0, bn = 0, threads = 128;
     GemmEpi ep;
     void* fn = nullptr;
 };
 
 int choose_bn(int M, int N, int num_sms);
-void gemm_plan(GemmPlan& p, bool f32, bool a_mn, const void* A, long lda, bool b_mn, const void* B, long ldb,
+// prec: 0 = BF16 operands, 1 = TF32, 2 = fp32 via 3xTF32 split
+void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b_mn, const void* B, long ldb,
                int M, int N, int K, const GemmEpi& ep, int num_sms, int force_bn = 0);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);
 
-enum Precision : int { PREC_BF16 = 0, PREC_TF32 = 1 };
+enum Precision : int { PREC_BF16 = 0, PREC_TF32 = 1, PREC_FP32 = 2 };
 enum Optimizer : int { OPT_SGD = 0, OPT_NG_KRON = 1 };
 
 inline long pad32(long v) { return (v + 31) / 32 * 32; }
@@ -60,6 +61,8 @@ struct DeviceDataset {
     DeviceDataset(Context* c, const double* x, const int32_t* labels, long n, long d, long classes);
     ~DeviceDataset();
     const void* features(Precision p);
+    // overwrite rows [row0, row0+n) from host fp32 (+ labels); refreshes the bf16 copy
+    void write_rows(const float* x, const int32_t* y, long row0, long n, cudaStream_t s);
 };
 
 // Host-visible error record written by device kernels (pivot failures).
@@ -68,6 +71,12 @@ struct DevErr {
     int chol_index;
     float chol_value;
     int pad;
+};
+
+struct Profile {
+    std::vector<cudaEvent_t> events;
+    std::vector<std::string> names;
+    std::vector<double> flops;
 };
 
 struct Replica {
@@ -121,7 +130,7 @@ struct Replica {
             long max_steps, double decay, double smoothing);
     ~Replica();
 
-    bool f32() const { return prec == PREC_TF32; }
+    bool f32() const { return prec != PREC_BF16; }  // fp32 storage of operands
     size_t esz() const { return f32() ? 4 : 2; }
     void set_params(const double* flat);  // canonical flatten order (network.cpp:238-248)
     void get_params(double* flat) const;
@@ -134,6 +143,13 @@ struct Replica {
     void enqueue_step(cudaStream_t s);
     void sync_shadow(cudaStream_t s);  // recompute bf16 copy after external param writes
     void check_errors();               // throws the reference's messages
+
+    // live per-region timing with CUDA events on the replica stream (bench)
+    Profile* prof = nullptr;
+    void mark(const char* kind, int layer, double flops, cudaStream_t s);
+    void profile_steps(long steps, std::vector<std::string>& names, std::vector<double>& ms,
+                       std::vector<double>& flops);
+    double time_steps(long steps);  // ms for `steps` graph launches (CUDA events)
 
     // debug/test hooks
     void forward_only(DeviceDataset* ds, const uint32_t* rows, long b, float* zout_host);

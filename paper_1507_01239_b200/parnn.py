@@ -54,6 +54,7 @@ class LrVariant(enum.IntEnum):
 class Precision(enum.IntEnum):
     bf16 = 0
     tf32 = 1
+    fp32 = 2  # 3xTF32 split on tcgen05: fp32-accurate (parity mode)
 
 
 # ------------------------------------------------------------ value types
@@ -291,6 +292,12 @@ class DeviceDataset:
         check(lib().parnn_dataset_create(ctx.h, ptr(x), ptr(y), x.shape[0], x.shape[1], classes, C.byref(h)))
         self.h, self.ctx, self.n = h, ctx, x.shape[0]
 
+    def write_rows(self, x, y, row0: int = 0):
+        """Host fp32 rows -> device (the per-step H2D of the end-to-end path)."""
+        x = np.ascontiguousarray(x, np.float32)
+        y = np.ascontiguousarray(y, np.int32)
+        check(lib().parnn_dataset_write_f32(self.h, ptr(x), ptr(y), row0, x.shape[0]))
+
     def close(self):
         if self.h:
             lib().parnn_dataset_destroy(self.h)
@@ -373,6 +380,22 @@ class Replica:
         check(lib().parnn_replica_accuracy(self.h, ds.h, C.byref(out)))
         return out.value
 
+    def time_steps(self, steps: int) -> float:
+        """Device ms (CUDA events on the replica stream) for `steps` graph launches."""
+        out = C.c_double()
+        check(lib().parnn_replica_time_steps(self.h, steps, C.byref(out)))
+        return out.value
+
+    def profile(self, steps: int = 1):
+        """Eager profiled steps -> list of (region, avg ms, algorithmic flops)."""
+        names = C.create_string_buffer(1 << 16)
+        cap = 4096
+        ms, fl = np.zeros(cap), np.zeros(cap)
+        n = C.c_uint64()
+        check(lib().parnn_replica_profile(self.h, steps, names, len(names), ptr(ms), ptr(fl), cap, C.byref(n)))
+        labels = names.value.decode().split("\n")[:n.value]
+        return [(labels[i], float(ms[i]), float(fl[i])) for i in range(n.value)]
+
     def kernels_per_step(self) -> int:
         out = C.c_uint64()
         check(lib().parnn_replica_kernels_per_step(self.h, C.byref(out)))
@@ -395,6 +418,16 @@ def average(replicas, comm=None, m_total: int | None = None) -> None:
     arr = (C.c_void_p * len(replicas))(*[r.h for r in replicas])
     check(lib().parnn_average(arr, len(replicas), comm.h if comm else None,
                               m_total if m_total is not None else len(replicas)))
+
+
+def run_steps(replicas, steps: int, avg_frequency: int, comm=None, m_total: int | None = None) -> float:
+    """Device-timed inner loop of worker_epoch over local replicas (+ comm)."""
+    arr = (C.c_void_p * len(replicas))(*[r.h for r in replicas])
+    out = C.c_double()
+    check(lib().parnn_run_steps(arr, len(replicas), comm.h if comm else None,
+                                m_total if m_total is not None else len(replicas), steps, avg_frequency,
+                                C.byref(out)))
+    return out.value
 
 
 class Comm:
