@@ -34,6 +34,7 @@ enum EpiMode : int {
     EPI_ACTGRAD = 4,     // out(T)   = acc * act'(aux[m, n])
     EPI_EMA = 5,         // out32    = beta * out32 + alpha * acc
     EPI_AXPY = 6,        // out32   += alpha * acc; shadow = bf16(out32)   (CD-1 update)
+    EPI_SUB = 7,         // out32   -= acc      (blocked Cholesky / TRSM updates)
 };
 
 struct GemmEpi {
@@ -56,6 +57,7 @@ struct GemmEpi {
     const int* step = nullptr;
     unsigned* flag = nullptr;  // bit `flag_bit` set on a non-finite gradient
     unsigned flag_bit = 0;
+    int lower = 0;  // skip tiles strictly above the diagonal (SYRK-style updates)
 };
 
 template <typename T>
@@ -194,6 +196,7 @@ __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
     const int m0 = blockIdx.y * 128;
     const int n0 = blockIdx.x * BN;
     const int nk = (K + S::kBK - 1) / S::kBK;
+    if (ep.lower && n0 > m0 + 127) return;  // whole tile above the diagonal: nothing to do
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -370,6 +373,15 @@ __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
                 if (beta != 0.f) load_row32<float>(op, o, valid);
 #pragma unroll
                 for (int j = 0; j < 32; ++j) o[j] = (beta != 0.f ? beta * o[j] : 0.f) + alpha * v[j];
+                store_row32<float>(op, o, valid);
+                break;
+            }
+            case EPI_SUB: {
+                float o[32];
+                float* op = ep.out32 + row * ep.ld_out32 + n;
+                load_row32<float>(op, o, valid);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) o[j] -= v[j];
                 store_row32<float>(op, o, valid);
                 break;
             }

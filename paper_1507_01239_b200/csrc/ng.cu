@@ -1,13 +1,21 @@
-// NG-SGD, full Kronecker-factored variant (optimizer.cpp:108-157), on device
-// in fp32 (SIMT FMA, fp32-accurate: SURVEY §7 "NG-SGD kron-full cost" rules
-// out TF32-operand solves at kappa(S) ~ 1e2).
+// NG-SGD, full Kronecker-factored variant (optimizer.cpp:108-157), on device.
 //
 // Per layer: S = R + lambda I with lambda = max(alpha tr(R)/n, 1e-8)
-// (smoothed_factor), blocked right-looking Cholesky of S_out and S_in
-// (S_out factored ONCE; the reference re-factors it for the bias solve),
-// Ghat = S_out^-1 [G | g_b] by blocked forward/back substitution, transpose,
-// S_in^-1 on the weight part, transpose back, Frobenius rescale gamma and the
-// fused SGD update (sgd_step_in_place) with the non-finite check.
+// (smoothed_factor), Cholesky of S_out and S_in (S_out factored ONCE; the
+// reference re-factors it for the bias solve), Ghat = S_out^-1 [G | g_b],
+// transpose, S_in^-1 on the weight part, transpose back, Frobenius rescale
+// gamma and the fused SGD update (sgd_step_in_place) with the finite check.
+//
+// Blocked algorithms, 128-row blocks (NG_NB):
+//   Cholesky (right-looking): per block j
+//     chol_diag_kernel  — SIMT fp32, one CTA: L_jj = chol(A_jj) and L_jj^-1
+//     panel  A_{>j,j} <- A_{>j,j} L_jj^-T           tcgen05 GEMM (in place)
+//     trail  A_{>j,>j} -= A_{>j,j} A_{>j,j}^T       tcgen05 GEMM, lower tiles only
+//   S^-1 X (X with c columns, in place):
+//     forward  X_i <- L_ii^-1 X_i ; X_{>i} -= L_{>i,i} X_i
+//     backward X_i <- L_ii^-T X_i ; X_{<i} -= L_{i,<i}^T X_i
+// Every GEMM runs in fp32 mode (3xTF32 split, see gemm.cuh): the solves need
+// fp32 accuracy at kappa(S) ~ 1e2, which TF32 alone does not give.
 #include <cfloat>
 
 #include "runtime.h"
@@ -16,7 +24,21 @@ namespace pnb {
 
 namespace {
 
-constexpr int NB = 64;  // Cholesky / TRSM block
+#ifndef PNB_CLK
+#define PNB_CLK(i) \
+    do {           \
+    } while (0)
+#endif
+
+constexpr int NB = NG_NB;
+constexpr int LDS = NB + 1;  // padded shared-memory row
+
+float* dalloc_f(size_t n) {
+    void* p = nullptr;
+    CUDA_THROW(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(float)));
+    CUDA_THROW(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(float)));
+    return static_cast<float*>(p);
+}
 
 __global__ void trace_lambda_kernel(const float* __restrict__ r, long n, long ld, double alpha,
                                     double* __restrict__ lam) {
@@ -35,7 +57,7 @@ __global__ void trace_lambda_kernel(const float* __restrict__ r, long n, long ld
     }
 }
 
-// S = R + lambda I (lower triangle incl. diagonal is all Cholesky reads).
+// S = R + lambda I (Cholesky reads the lower triangle incl. the diagonal).
 __global__ void shift_copy_kernel(const float* __restrict__ r, long n, long ld, const double* __restrict__ lam,
                                   float* __restrict__ s) {
     const long total = n * ld;
@@ -48,167 +70,255 @@ __global__ void shift_copy_kernel(const float* __restrict__ r, long n, long ld, 
     }
 }
 
-// Unblocked Cholesky of the b x b diagonal block at (j, j), in shared memory.
-__global__ void potrf_diag_kernel(float* __restrict__ a, long ld, long j, int b, DevErr* err) {
-    __shared__ float t[NB][NB + 1];
-    for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
-        const int r = idx / b, c = idx % b;
-        t[r][c] = a[(j + r) * ld + j + c];
+// Per-thread micro-tile product for the in-CTA block algebra of the diagonal
+// kernel (256 threads as a 16 x 16 grid, thread tile TM x TN):
+//   acc[i][q] = sum_{k<K} A(m0 + ty*TM + i, k) * B(n0 + tx*TN + q, k)
+// A(m, k) = A[m*LDS + k]; B(n, k) = Bm[n*LDS + k] if BT, else Bm[k*LDS + n].
+template <int TM, int TN, bool BT>
+__device__ __forceinline__ void micro_mma(const float* A, const float* Bm, int K, int m0, int n0,
+                                          float (&acc)[TM][TN]) {
+    const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int q = 0; q < TN; ++q) acc[i][q] = 0.f;
+    const float* ap = A + (m0 + ty * TM) * LDS;
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {
+        float av[TM], bv[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) av[i] = ap[i * LDS + k];
+#pragma unroll
+        for (int q = 0; q < TN; ++q)
+            bv[q] = BT ? Bm[(n0 + tx * TN + q) * LDS + k] : Bm[k * LDS + n0 + tx * TN + q];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int q = 0; q < TN; ++q) acc[i][q] = fmaf(av[i], bv[q], acc[i][q]);
+    }
+}
+
+// Rows [r0, r0 + 16*TM) of the panel columns [c0, c0+32): P <- P * D^-T.
+template <int TM>
+__device__ __forceinline__ void panel_solve(float* S, const float* V, int c0) {
+    const int r0 = c0 + 32;
+    float acc[TM][2];
+    micro_mma<TM, 2, true>(S + c0, V + c0 * LDS + c0, 32, r0, 0, acc);
+    __syncthreads();
+    const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) S[(r0 + ty * TM + i) * LDS + c0 + tx * 2 + q] = acc[i][q];
+}
+
+// Lower part of S[r0:, r0:] -= P P^T with P = S[r0:, c0:c0+32], r0 = c0 + 32.
+template <int TM>
+__device__ __forceinline__ void trailing_update(float* S, int c0) {
+    const int r0 = c0 + 32;
+    const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+    if (tx * TM > ty * TM + TM - 1) return;  // micro tile strictly above the diagonal
+    float acc[TM][TM];
+    micro_mma<TM, TM, true>(S + c0, S + c0, 32, r0, r0, acc);  // A(m,k) = B(m,k) = S[m][c0+k]
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int q = 0; q < TM; ++q) {
+            const int r = r0 + ty * TM + i, c = r0 + tx * TM + q;
+            if (c <= r) S[r * LDS + c] -= acc[i][q];
+        }
+}
+
+// Diagonal block j: L = chol(A_jj) in place (zero upper part) and V = L^-1
+// into linv (NB x NB, zero padded). Pivot failures are recorded with the
+// reference's semantics (first non-positive / non-finite pivot, matrix.cpp:110-113).
+//
+// 256 threads; 4 panels of 32 columns. Per panel:
+//   A. warp 0 factors the 32x32 diagonal sub-block D: lane i keeps row i in
+//      registers; each step broadcasts column k through shared memory
+//      (one store, eight 16-byte broadcast loads) — the serial chain is short;
+//   B. rows below solve x D^T = a by forward substitution (one thread per row,
+//      D broadcast from shared memory);
+//   C. all 8 warps apply the rank-32 trailing update with register-tiled
+//      micro products (6x6/4x4/2x2 per thread).
+// Then 4 warps invert the 4 diagonal sub-blocks concurrently and the
+// off-diagonal blocks of V follow by block forward substitution.
+// Padding rows/columns (b < NB) hold the identity so every step is
+// branch-free; only the b x b block is written back.
+__global__ void __launch_bounds__(256) chol_diag_kernel(float* __restrict__ a, long ld, long j, int b,
+                                                        float* __restrict__ linv, DevErr* err) {
+    extern __shared__ float sm[];
+    float* S = sm;                 // [NB][LDS]  A -> L
+    float* V = sm + NB * LDS;      // [NB][LDS]  L^-1
+    float* col = V + NB * LDS;     // [32] column broadcast (16-byte aligned)
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    PNB_CLK(0);
+    {
+        // 16 rows of 128 per pass: all loads issued before the shared stores
+        float v[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+            const int idx = t + 256 * i, r = idx >> 7, c = idx & (NB - 1);
+            v[i] = (r < b && c <= r) ? a[(j + r) * ld + j + c] : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+            const int idx = t + 256 * i, r = idx >> 7, c = idx & (NB - 1);
+            S[r * LDS + c] = (r >= b && r == c) ? 1.f : v[i];
+            V[r * LDS + c] = 0.f;
+        }
     }
     __syncthreads();
-    for (int k = 0; k < b; ++k) {
-        if (threadIdx.x == 0) {
-            const float piv = t[k][k];
-            if (!(piv > 0.f) || !isfinite(piv)) {
-                if (atomicCAS(&err->chol_failed, 0, 1) == 0) {
-                    err->chol_index = static_cast<int>(j + k);
-                    err->chol_value = piv;
+    PNB_CLK(1);
+#pragma unroll 1
+    for (int p = 0; p < NB / 32; ++p) {
+        const int c0 = 32 * p;
+        if (warp == 0) {
+            float d[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) d[c] = S[(c0 + lane) * LDS + c0 + c];
+#pragma unroll 1
+            for (int k = 0; k < 32; ++k) {
+                // dk = d[k] for a runtime k: 5-level select tree (depth 5, not a 32-long chain)
+                float s16[16], s8[8], s4[4], s2[2];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) s16[i] = (k & 16) ? d[i + 16] : d[i];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s8[i] = (k & 8) ? s16[i + 8] : s16[i];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) s4[i] = (k & 4) ? s8[i + 4] : s8[i];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) s2[i] = (k & 2) ? s4[i + 2] : s4[i];
+                const float dk = (k & 1) ? s2[1] : s2[0];
+                if (lane == k) col[32] = dk;
+                __syncwarp();
+                const float piv = col[32];
+                if (lane == 0 && c0 + k < b && (!(piv > 0.f) || !isfinite(piv))) {
+                    if (atomicCAS(&err->chol_failed, 0, 1) == 0) {
+                        err->chol_index = static_cast<int>(j + c0 + k);
+                        err->chol_value = piv;
+                    }
                 }
+                const float rs = rsqrtf(piv);  // 1/L_kk
+                const float lkk = piv * rs;
+                const float lik = lane > k ? dk * rs : (lane == k ? lkk : 0.f);
+                col[lane] = lik;
+                __syncwarp();
+                float cv[32];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 f = reinterpret_cast<const float4*>(col)[q];
+                    cv[4 * q] = f.x; cv[4 * q + 1] = f.y; cv[4 * q + 2] = f.z; cv[4 * q + 3] = f.w;
+                }
+                // branch-free (select) updates: divergent predicated branches
+                // here cost ~30 cycles of reconvergence each
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const float w = (c > k && c <= lane) ? lik : 0.f;
+                    d[c] = (c == k) ? lik : fmaf(-w, cv[c], d[c]);
+                }
+                __syncwarp();
             }
-            t[k][k] = sqrtf(piv);
+#pragma unroll
+            for (int c = 0; c < 32; ++c) S[(c0 + lane) * LDS + c0 + c] = c <= lane ? d[c] : 0.f;
         }
         __syncthreads();
-        const float inv = 1.f / t[k][k];
-        for (int r = k + 1 + threadIdx.x; r < b; r += blockDim.x) t[r][k] *= inv;
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < (b - k - 1) * (b - k - 1); idx += blockDim.x) {
-            const int r = k + 1 + idx / (b - k - 1), c = k + 1 + idx % (b - k - 1);
-            if (c <= r) t[r][c] -= t[r][k] * t[c][k];
+        // B. rows below: x D^T = a (forward substitution, D rows broadcast)
+        if (t < NB - c0 - 32) {
+            const int r = c0 + 32 + t;
+            float x[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) x[c] = S[r * LDS + c0 + c];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const float* dr = S + (c0 + c) * LDS + c0;
+                float acc = x[c];
+#pragma unroll
+                for (int k = 0; k < c; ++k) acc -= x[k] * dr[k];
+                x[c] = acc / dr[c];
+            }
+#pragma unroll
+            for (int c = 0; c < 32; ++c) S[r * LDS + c0 + c] = x[c];
         }
         __syncthreads();
+        PNB_CLK(2 + 2 * p);
+        if (p == 0) trailing_update<6>(S, c0);
+        else if (p == 1) trailing_update<4>(S, c0);
+        else if (p == 2) trailing_update<2>(S, c0);
+        __syncthreads();
+        PNB_CLK(3 + 2 * p);
     }
-    for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
-        const int r = idx / b, c = idx % b;
-        a[(j + r) * ld + j + c] = c <= r ? t[r][c] : 0.f;
-    }
-}
-
-// Panel: rows [j+b, n) of columns [j, j+b): x L11^T = a  (forward substitution per row).
-__global__ void trsm_panel_kernel(float* __restrict__ a, long ld, long j, int b, long n) {
-    __shared__ float l11[NB][NB + 1];
-    for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
-        const int r = idx / b, c = idx % b;
-        l11[r][c] = a[(j + r) * ld + j + c];
+    // D. inverses of the four 32x32 diagonal sub-blocks, one warp each:
+    //    lane owns column `lane`; x_i = (e - sum_{q<i} D[i][q] x_q) / D[i][i]
+    if (warp < NB / 32) {
+        const int c0 = 32 * warp;
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const float* dr = S + (c0 + i) * LDS + c0;
+            float acc = (i == lane) ? 1.f : 0.f;
+#pragma unroll
+            for (int q = 0; q < i; ++q) acc -= dr[q] * x[q];
+            x[i] = acc / dr[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) V[(c0 + i) * LDS + c0 + lane] = x[i];
     }
     __syncthreads();
-    const long row = j + b + blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (row >= n) return;
-    float x[NB];
-    float* ar = a + row * ld + j;
-#pragma unroll
-    for (int c = 0; c < NB; ++c) x[c] = c < b ? ar[c] : 0.f;
-#pragma unroll
-    for (int c = 0; c < NB; ++c) {
-        if (c < b) {
-            float acc = x[c];
-#pragma unroll
-            for (int k = 0; k < NB; ++k)
-                if (k < c) acc -= x[k] * l11[c][k];
-            x[c] = acc / l11[c][c];
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < NB; ++c)
-        if (c < b) ar[c] = x[c];
-}
-
-// C[m, n] -= sum_k opA(m, k) * opB(k, n); opA = A[m*lda+k] (TA=0) or A[k*lda+m] (TA=1);
-// opB = B[k*ldb+n] (TB=0) or B[n*ldb+k] (TB=1). LOWER: only tiles touching n <= m.
-template <int TA, int TB, int LOWER>
-__global__ void __launch_bounds__(256) gemm_sub_kernel(float* __restrict__ c, long ldc, const float* __restrict__ a,
-                                                       long lda, const float* __restrict__ b, long ldb, long M, long N,
-                                                       long K) {
-    const long m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
-    if (LOWER && n0 > m0 + 63) return;
-    __shared__ float As[16][64 + 4];
-    __shared__ float Bs[16][64 + 4];
-    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    float acc[4][4] = {};
-    for (long k0 = 0; k0 < K; k0 += 16) {
-        for (int idx = threadIdx.x; idx < 16 * 64; idx += 256) {
-            int kk, mm;
-            if (TA == 0) { kk = idx % 16; mm = idx / 16; } else { mm = idx % 64; kk = idx / 64; }
-            const long gm = m0 + mm, gk = k0 + kk;
-            float v = 0.f;
-            if (gm < M && gk < K) v = TA == 0 ? a[gm * lda + gk] : a[gk * lda + gm];
-            As[kk][mm] = v;
-        }
-        for (int idx = threadIdx.x; idx < 16 * 64; idx += 256) {
-            int kk, nn;
-            if (TB == 0) { nn = idx % 64; kk = idx / 64; } else { kk = idx % 16; nn = idx / 16; }
-            const long gn = n0 + nn, gk = k0 + kk;
-            float v = 0.f;
-            if (gn < N && gk < K) v = TB == 0 ? b[gk * ldb + gn] : b[gn * ldb + gk];
-            Bs[kk][nn] = v;
+    PNB_CLK(10);
+    // E. off-diagonal blocks of V = L^-1: V_{bi,q} = -D_bi^-1 sum_{k=q}^{bi-1} L_{bi,k} V_{k,q}
+#pragma unroll 1
+    for (int bi = 1; bi < NB / 32; ++bi) {
+        const int r0 = 32 * bi;
+        const int ty = t >> 4, tx = t & 15;
+        // T = L[r0:r0+32, 0:r0] V[0:r0, 0:r0] -> staged in V[r0:r0+32, 0:r0] (still zero)
+        if (bi == 1) {
+            float acc[2][2];
+            micro_mma<2, 2, false>(S, V, r0, r0, 0, acc);
+            for (int i = 0; i < 2; ++i)
+                for (int q = 0; q < 2; ++q) V[(r0 + ty * 2 + i) * LDS + tx * 2 + q] = acc[i][q];
+        } else if (bi == 2) {
+            float acc[2][4];
+            micro_mma<2, 4, false>(S, V, r0, r0, 0, acc);
+            for (int i = 0; i < 2; ++i)
+                for (int q = 0; q < 4; ++q) V[(r0 + ty * 2 + i) * LDS + tx * 4 + q] = acc[i][q];
+        } else {
+            float acc[2][6];
+            micro_mma<2, 6, false>(S, V, r0, r0, 0, acc);
+            for (int i = 0; i < 2; ++i)
+                for (int q = 0; q < 6; ++q) V[(r0 + ty * 2 + i) * LDS + tx * 6 + q] = acc[i][q];
         }
         __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-            float av[4], bv[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) bv[i] = Bs[kk][tx * 4 + i];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) acc[i][q] = fmaf(av[i], bv[q], acc[i][q]);
+        // V[r0:r0+32, 0:r0] = -D_bi^-1 T  (D_bi^-1 = V[r0:, r0:r0+32])
+        if (bi == 1) {
+            float acc[2][2];
+            micro_mma<2, 2, false>(V + r0, V + r0 * LDS, 32, r0, 0, acc);
+            __syncthreads();
+            for (int i = 0; i < 2; ++i)
+                for (int q = 0; q < 2; ++q) V[(r0 + ty * 2 + i) * LDS + tx * 2 + q] = -acc[i][q];
+        } else if (bi == 2) {
+            float acc[2][4];
+            micro_mma<2, 4, false>(V + r0, V + r0 * LDS, 32, r0, 0, acc);
+            __syncthreads();
+            for (int i = 0; i < 2; ++i)
+                for (int q = 0; q < 4; ++q) V[(r0 + ty * 2 + i) * LDS + tx * 4 + q] = -acc[i][q];
+        } else {
+            float acc[2][6];
+            micro_mma<2, 6, false>(V + r0, V + r0 * LDS, 32, r0, 0, acc);
+            __syncthreads();
+            for (int i = 0; i < 2; ++i)
+                for (int q = 0; q < 6; ++q) V[(r0 + ty * 2 + i) * LDS + tx * 6 + q] = -acc[i][q];
         }
         __syncthreads();
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const long gm = m0 + ty * 4 + i;
-        if (gm >= M) continue;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const long gn = n0 + tx * 4 + q;
-            if (gn < N && (!LOWER || gn <= gm)) c[gm * ldc + gn] -= acc[i][q];
-        }
+    PNB_CLK(14);
+#pragma unroll 8
+    for (int i = 0; i < 64; ++i) {
+        const int idx = t + 256 * i, r = idx >> 7, c = idx & (NB - 1);
+        if (r < b && c < b) a[(j + r) * ld + j + c] = c <= r ? S[r * LDS + c] : 0.f;
+        linv[idx] = (r < b && c < b && c <= r) ? V[r * LDS + c] : 0.f;
     }
-}
-
-// X_i = L_ii^-1 X_i (FWD) or L_ii^-T X_i (!FWD) for rows [i0, i0+b) of X, one thread per column.
-template <int FWD>
-__global__ void trsv_block_kernel(const float* __restrict__ l, long ld, long i0, int b, float* __restrict__ x,
-                                  long ldx, long ncols) {
-    __shared__ float t[NB][NB + 1];
-    for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
-        const int r = idx / b, c = idx % b;
-        t[r][c] = l[(i0 + r) * ld + i0 + c];
-    }
-    __syncthreads();
-    const long col = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (col >= ncols) return;
-    float v[NB];
-#pragma unroll
-    for (int r = 0; r < NB; ++r) v[r] = r < b ? x[(i0 + r) * ldx + col] : 0.f;
-    if (FWD) {
-#pragma unroll
-        for (int r = 0; r < NB; ++r) {
-            if (r < b) {
-                float acc = v[r];
-#pragma unroll
-                for (int k = 0; k < NB; ++k)
-                    if (k < r) acc -= t[r][k] * v[k];
-                v[r] = acc / t[r][r];
-            }
-        }
-    } else {
-#pragma unroll
-        for (int r = NB - 1; r >= 0; --r) {
-            if (r < b) {
-                float acc = v[r];
-#pragma unroll
-                for (int k = 0; k < NB; ++k)
-                    if (k > r && k < b) acc -= t[k][r] * v[k];
-                v[r] = acc / t[r][r];
-            }
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < NB; ++r)
-        if (r < b) x[(i0 + r) * ldx + col] = v[r];
+    PNB_CLK(15);
 }
 
 __global__ void transpose_kernel(const float* __restrict__ src, long lds, long rows, long cols,
@@ -268,8 +378,8 @@ __global__ void sum_final_kernel(const double* __restrict__ part, int n, double*
     if (threadIdx.x == 0) *out = sh[0];
 }
 
-// W -= lr * gamma * Ghat (transposed back from th [d_in x ldth]); b -= lr * gamma_b * bhat.
-// scal: [0] |G|^2, [1] |g_b|^2, [2] |Ghat|^2, [3] |bhat|^2 (optimizer.cpp:142-154).
+// W -= lr * gamma * Ghat ; b -= lr * gamma_b * bhat (optimizer.cpp:142-154 + 29-34).
+// scal: [0] |G|^2, [1] |g_b|^2, [2] |Ghat|^2, [3] |bhat|^2.
 __global__ void ng_update_kernel(float* __restrict__ w, long ldw, float* __restrict__ bias, bf16* __restrict__ shadow,
                                  const float* __restrict__ gh, long ldgh, const float* __restrict__ bh, long ldbh,
                                  long dout, long din, const double* __restrict__ scal, const float* __restrict__ lr,
@@ -300,42 +410,108 @@ __global__ void ng_update_kernel(float* __restrict__ w, long ldw, float* __restr
 
 int grid_for(long total) { return (int)std::max<long>(1, std::min<long>((total + 255) / 256, 148L * 8)); }
 
-void cholesky(float* a, long n, long ld, DevErr* err, cudaStream_t s) {
-    for (long j = 0; j < n; j += NB) {
-        const int b = (int)std::min<long>(NB, n - j);
-        potrf_diag_kernel<<<1, 256, 0, s>>>(a, ld, j, b, err);
-        const long rest = n - j - b;
-        if (rest <= 0) break;
-        trsm_panel_kernel<<<(rest + 127) / 128, 128, 0, s>>>(a, ld, j, b, n);
-        dim3 grid((rest + 63) / 64, (rest + 63) / 64);
-        gemm_sub_kernel<0, 1, 1><<<grid, 256, 0, s>>>(a + (j + b) * ld + (j + b), ld, a + (j + b) * ld + j, ld,
-                                                        a + (j + b) * ld + j, ld, rest, rest, b);
+constexpr int kDiagSmem = 2 * NB * LDS * 4 + 48 * 4;
+
+void ensure_diag_attr() {
+    static bool done = false;
+    if (!done) {
+        CUDA_THROW(cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem));
+        done = true;
     }
 }
 
-// X <- L^-1 X then X <- L^-T X  (X is n x ncols, ld ldx): S^-1 X via the factor.
-void chol_solve(const float* l, long n, long ld, float* x, long ldx, long ncols, cudaStream_t s) {
-    const int tb = 128;
-    const int gcols = (int)((ncols + tb - 1) / tb);
-    for (long i0 = 0; i0 < n; i0 += NB) {
-        const int b = (int)std::min<long>(NB, n - i0);
-        trsv_block_kernel<1><<<gcols, tb, 0, s>>>(l, ld, i0, b, x, ldx, ncols);
-        const long rest = n - i0 - b;
+float* linv_blk(NgFactor& f, long j) { return f.linv + (j / NB) * NB * NB; }
+
+void build_factor(NgFactor& f, int sms) {
+    f.panel.clear();
+    f.trail.clear();
+    for (long j = 0; j < f.n; j += NB) {
+        const long b = std::min<long>(NB, f.n - j), rest = f.n - j - b;
+        GemmPlan pp, tp;
         if (rest > 0) {
-            dim3 grid((ncols + 63) / 64, (rest + 63) / 64);
-            gemm_sub_kernel<0, 0, 0><<<grid, 256, 0, s>>>(x + (i0 + b) * ldx, ldx, l + (i0 + b) * ld + i0, ld,
-                                                            x + i0 * ldx, ldx, rest, ncols, b);
+            float* a21 = f.a + (j + b) * f.ld + j;
+            GemmEpi e;  // A21 <- A21 L_jj^-T, in place (one N tile: BN = 128 >= b)
+            e.mode = EPI_GRAD;
+            e.alpha = 1.f;
+            e.out32 = a21;
+            e.ld_out32 = f.ld;
+            gemm_plan(pp, PREC_FP32, false, a21, f.ld, false, linv_blk(f, j), NB, (int)rest, (int)b, (int)b, e, sms,
+                      128);
+            GemmEpi u;  // A22 -= A21 A21^T (lower tiles)
+            u.mode = EPI_SUB;
+            u.lower = 1;
+            u.out32 = f.a + (j + b) * f.ld + (j + b);
+            u.ld_out32 = f.ld;
+            gemm_plan(tp, PREC_FP32, false, a21, f.ld, false, a21, f.ld, (int)rest, (int)rest, (int)b, u, sms);
+        }
+        f.panel.push_back(pp);
+        f.trail.push_back(tp);
+    }
+}
+
+void build_solve(NgFactor& f, NgSolve& sv, float* x, long ldx, long c, int sms) {
+    sv.fdiag.clear();
+    sv.fupd.clear();
+    sv.bdiag.clear();
+    sv.bupd.clear();
+    for (long i0 = 0; i0 < f.n; i0 += NB) {
+        const long b = std::min<long>(NB, f.n - i0), rest = f.n - i0 - b;
+        float* xi = x + i0 * ldx;
+        GemmEpi d;  // X_i <- Linv_ii X_i  (in place; single M tile)
+        d.mode = EPI_GRAD;
+        d.alpha = 1.f;
+        d.out32 = xi;
+        d.ld_out32 = ldx;
+        GemmPlan fd, fu, bd, bu;
+        gemm_plan(fd, PREC_FP32, false, linv_blk(f, i0), NB, true, xi, ldx, (int)b, (int)c, (int)b, d, sms);
+        gemm_plan(bd, PREC_FP32, true, linv_blk(f, i0), NB, true, xi, ldx, (int)b, (int)c, (int)b, d, sms);
+        if (rest > 0) {
+            GemmEpi u;  // X_{>i} -= L_{>i,i} X_i
+            u.mode = EPI_SUB;
+            u.out32 = x + (i0 + b) * ldx;
+            u.ld_out32 = ldx;
+            gemm_plan(fu, PREC_FP32, false, f.a + (i0 + b) * f.ld + i0, f.ld, true, xi, ldx, (int)rest, (int)c,
+                      (int)b, u, sms);
+        }
+        if (i0 > 0) {
+            GemmEpi u;  // X_{<i} -= L_{i,<i}^T X_i
+            u.mode = EPI_SUB;
+            u.out32 = x;
+            u.ld_out32 = ldx;
+            gemm_plan(bu, PREC_FP32, true, f.a + i0 * f.ld, f.ld, true, xi, ldx, (int)i0, (int)c, (int)b, u, sms);
+        }
+        sv.fdiag.push_back(fd);
+        sv.fupd.push_back(fu);
+        sv.bdiag.push_back(bd);
+        sv.bupd.push_back(bu);
+    }
+}
+
+void cholesky(Replica& r, int l, NgFactor& f, DevErr* err, cudaStream_t s) {
+    size_t blk = 0;
+    for (long j = 0; j < f.n; j += NB, ++blk) {
+        const int b = (int)std::min<long>(NB, f.n - j);
+        chol_diag_kernel<<<1, 256, kDiagSmem, s>>>(f.a, f.ld, j, b, linv_blk(f, j), err);
+        CUDA_THROW(cudaGetLastError());
+        r.mark("ng_potrf_diag", l, static_cast<double>(b) * b * b / 3.0 * 2.0, s);
+        if (f.panel[blk].M > 0) {
+            gemm_launch(f.panel[blk], s);
+            r.mark("ng_potrf_panel", l, 2.0 * f.panel[blk].M * f.panel[blk].N * f.panel[blk].K, s);
+            gemm_launch(f.trail[blk], s);
+            r.mark("ng_potrf_trail", l, 1.0 * f.trail[blk].M * f.trail[blk].N * f.trail[blk].K, s);
         }
     }
-    const long last = ((n - 1) / NB) * NB;
-    for (long i0 = last; i0 >= 0; i0 -= NB) {
-        const int b = (int)std::min<long>(NB, n - i0);
-        trsv_block_kernel<0><<<gcols, tb, 0, s>>>(l, ld, i0, b, x, ldx, ncols);
-        if (i0 > 0) {
-            dim3 grid((ncols + 63) / 64, (i0 + 63) / 64);
-            // X[0:i0] -= L[i0:i0+b, 0:i0]^T X[i0:i0+b]
-            gemm_sub_kernel<1, 0, 0><<<grid, 256, 0, s>>>(x, ldx, l + i0 * ld, ld, x + i0 * ldx, ldx, i0, ncols, b);
-        }
+}
+
+void solve(NgSolve& sv, cudaStream_t s) {
+    const size_t nb = sv.fdiag.size();
+    for (size_t i = 0; i < nb; ++i) {
+        gemm_launch(sv.fdiag[i], s);
+        if (sv.fupd[i].M > 0) gemm_launch(sv.fupd[i], s);
+    }
+    for (size_t i = nb; i-- > 0;) {
+        gemm_launch(sv.bdiag[i], s);
+        if (sv.bupd[i].M > 0) gemm_launch(sv.bupd[i], s);
     }
 }
 
@@ -347,63 +523,102 @@ void sumsq(const float* x, long ld, long rows, long cols, double* part, double* 
 
 }  // namespace
 
-// ng_precondition (optimizer.cpp:123-157) for layer l of replica r; the
-// gradient is in r.grads (W part [dout x ldw], bias part at b_off); writes the
-// preconditioned direction into r.tbuf (transposed back) and scalars in r.scal.
+void ng_alloc(Replica& r) {
+    r.ngl.assign(r.L, NgLayer());
+    for (int l = 0; l < r.L; ++l) {
+        NgLayer& g = r.ngl[l];
+        const long din = r.dims[l], dout = r.dims[l + 1];
+        for (auto [f, n] : {std::pair<NgFactor*, long>{&g.out, dout}, {&g.in, din}}) {
+            f->n = n;
+            f->ld = pad32(n);
+            f->a = dalloc_f(n * f->ld);
+            f->linv = dalloc_f(((n + NB - 1) / NB) * NB * NB);
+        }
+        g.ldt = pad32(din + 1);
+        g.ld2 = pad32(dout);
+        g.t1 = dalloc_f(dout * g.ldt);
+        g.t2 = dalloc_f(din * g.ld2);
+        CUDA_THROW(cudaMalloc(&g.part, 512 * sizeof(double)));
+        CUDA_THROW(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+        CUDA_THROW(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
+    }
+    CUDA_THROW(cudaEventCreateWithFlags(&r.ng_fork, cudaEventDisableTiming));
+}
+
+void ng_free(Replica& r) {
+    for (NgLayer& g : r.ngl) {
+        for (float* p : {g.out.a, g.out.linv, g.in.a, g.in.linv, g.t1, g.t2})
+            if (p) cudaFree(p);
+        if (g.part) cudaFree(g.part);
+        if (g.stream) cudaStreamDestroy(g.stream);
+        if (g.done) cudaEventDestroy(g.done);
+    }
+    if (r.ng_fork) cudaEventDestroy(r.ng_fork);
+    r.ng_fork = nullptr;
+    r.ngl.clear();
+}
+
+void ng_build_plans(Replica& r) {
+    const int sms = r.ctx->num_sms;
+    ensure_diag_attr();  // function attributes may not be set while a graph is being captured
+    for (int l = 0; l < r.L; ++l) {
+        NgLayer& g = r.ngl[l];
+        build_factor(g.out, sms);
+        build_factor(g.in, sms);
+        build_solve(g.out, g.solve_out, g.t1, g.ldt, r.dims[l] + 1, sms);
+        build_solve(g.in, g.solve_in, g.t2, g.ld2, r.dims[l + 1], sms);
+    }
+}
+
+// ng_precondition (optimizer.cpp:123-157) for layer l: G is in r.grads (W part
+// [dout x ldw], bias at b_off); leaves Ghat^T in t2, bhat in t1[:, din] and
+// the four norms in r.scal.
 void ng_precondition_layer(Replica& r, int l, cudaStream_t s) {
+    NgLayer& g = r.ngl[l];
     const long din = r.dims[l], dout = r.dims[l + 1];
-    const long ldi = pad32(din), ldo = pad32(dout);
     double* sc = r.scal + 16 * l;  // [0..3] norms, [4] lambda_in, [5] lambda_out
-    double* part = r.scal + 16 * r.L;
-    float* g = r.grads + r.w_off[l];
+    double* part = g.part;
+    float* gw = r.grads + r.w_off[l];
     float* gb = r.grads + r.b_off[l];
-    const long ldt = pad32(din + 1);
-    float* t1 = r.tbuf;                      // [dout x ldt] = [G | g_b]
-    float* t2 = r.tbuf + dout * ldt;         // [din x ldo]  = transposed weight part
-
-    // smoothed_factor: lambda = max(alpha tr(R)/n, 1e-8)
-    trace_lambda_kernel<<<1, 256, 0, s>>>(r.r_in[l], din, ldi, r.ng_smoothing, sc + 4);
-    trace_lambda_kernel<<<1, 256, 0, s>>>(r.r_out[l], dout, ldo, r.ng_smoothing, sc + 5);
-    shift_copy_kernel<<<grid_for(dout * ldo), 256, 0, s>>>(r.r_out[l], dout, ldo, sc + 5, r.chol_a);
-    shift_copy_kernel<<<grid_for(din * ldi), 256, 0, s>>>(r.r_in[l], din, ldi, sc + 4, r.chol_b);
-    r.mark("ng_smooth", l, 0, s);
     const double fo = static_cast<double>(dout), fi = static_cast<double>(din);
-    cholesky(r.chol_a, dout, ldo, r.d_err, s);
-    r.mark("ng_potrf", l, fo * fo * fo / 3.0, s);
-    cholesky(r.chol_b, din, ldi, r.d_err, s);
-    r.mark("ng_potrf", l, fi * fi * fi / 3.0, s);
 
-    sumsq(g, r.ldw[l], dout, din, part, sc + 0, s);
+    trace_lambda_kernel<<<1, 256, 0, s>>>(r.r_in[l], din, g.in.ld, r.ng_smoothing, sc + 4);
+    trace_lambda_kernel<<<1, 256, 0, s>>>(r.r_out[l], dout, g.out.ld, r.ng_smoothing, sc + 5);
+    shift_copy_kernel<<<grid_for(dout * g.out.ld), 256, 0, s>>>(r.r_out[l], dout, g.out.ld, sc + 5, g.out.a);
+    shift_copy_kernel<<<grid_for(din * g.in.ld), 256, 0, s>>>(r.r_in[l], din, g.in.ld, sc + 4, g.in.a);
+    r.mark("ng_smooth", l, 0, s);
+    cholesky(r, l, g.out, r.d_err, s);
+    cholesky(r, l, g.in, r.d_err, s);
+    (void)fi;
+
+    sumsq(gw, r.ldw[l], dout, din, part, sc + 0, s);
     sumsq(gb, 1, dout, 1, part, sc + 1, s);
-    pack_rhs_kernel<<<grid_for(dout * ldt), 256, 0, s>>>(g, r.ldw[l], gb, dout, din, t1, ldt);
+    pack_rhs_kernel<<<grid_for(dout * g.ldt), 256, 0, s>>>(gw, r.ldw[l], gb, dout, din, g.t1, g.ldt);
     r.mark("ng_norms", l, 0, s);
-    chol_solve(r.chol_a, dout, ldo, t1, ldt, din + 1, s);  // S_out^-1 [G | g_b]
+    solve(g.solve_out, s);  // S_out^-1 [G | g_b]
     r.mark("ng_trsm", l, 2.0 * fo * fo * (fi + 1.0), s);
     {
         dim3 grid((din + 31) / 32, (dout + 31) / 32), block(32, 8);
-        transpose_kernel<<<grid, block, 0, s>>>(t1, ldt, dout, din, t2, ldo);
+        transpose_kernel<<<grid, block, 0, s>>>(g.t1, g.ldt, dout, din, g.t2, g.ld2);
     }
     r.mark("ng_transpose", l, 0, s);
-    chol_solve(r.chol_b, din, ldi, t2, ldo, dout, s);  // S_in^-1 (S_out^-1 G)^T
+    solve(g.solve_in, s);  // S_in^-1 (S_out^-1 G)^T
     r.mark("ng_trsm", l, 2.0 * fi * fi * fo, s);
-    sumsq(t2, ldo, din, dout, part, sc + 2, s);
-    sumsq(t1 + din, ldt, dout, 1, part, sc + 3, s);
+    sumsq(g.t2, g.ld2, din, dout, part, sc + 2, s);
+    sumsq(g.t1 + din, g.ldt, dout, 1, part, sc + 3, s);
     r.mark("ng_norms", l, 0, s);
 }
 
 void ng_apply_update(Replica& r, int l, cudaStream_t s) {
+    NgLayer& g = r.ngl[l];
     const long din = r.dims[l], dout = r.dims[l + 1];
-    const long ldt = pad32(din + 1);
-    float* t1 = r.tbuf;
-    float* t2 = r.tbuf + dout * ldt;
-    // Ghat^T is t2 [din x ldo]; transpose back into t1's weight columns.
     {
         dim3 grid((dout + 31) / 32, (din + 31) / 32), block(32, 8);
-        transpose_kernel<<<grid, block, 0, s>>>(t2, pad32(dout), din, dout, t1, ldt);
+        transpose_kernel<<<grid, block, 0, s>>>(g.t2, g.ld2, din, dout, g.t1, g.ldt);
     }
     ng_update_kernel<<<grid_for(dout * din), 256, 0, s>>>(
-        r.params + r.w_off[l], r.ldw[l], r.params + r.b_off[l], r.wshadow ? r.wshadow + r.w_off[l] : nullptr, t1,
-        ldt, t1 + din, ldt, dout, din, r.scal + 16 * l, r.d_lr, r.d_step, r.d_flags, 2 * l);
+        r.params + r.w_off[l], r.ldw[l], r.params + r.b_off[l], r.wshadow ? r.wshadow + r.w_off[l] : nullptr, g.t1,
+        g.ldt, g.t1 + din, g.ldt, dout, din, r.scal + 16 * l, r.d_lr, r.d_step, r.d_flags, 2 * l);
     r.mark("ng_update", l, 0, s);
 }
 

@@ -1,6 +1,7 @@
 // Contexts, device-resident datasets and replicas; the fused minibatch step
 // (worker_epoch's body, parallel.cpp:117-130) as one CUDA graph.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -129,17 +130,11 @@ Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision
     for (int l = 0; l < L; ++l)
         dz.push_back(f32() ? (void*)dalloc<float>(B * ld_act[l + 1]) : (void*)dalloc<bf16>(B * ld_act[l + 1]));
     if (opt == OPT_NG_KRON) {
-        long max_out = 0, max_in = 0, max_t = 0;
         for (int l = 0; l < L; ++l) {
             r_in.push_back(dalloc<float>(dims[l] * pad32(dims[l])));
             r_out.push_back(dalloc<float>(dims[l + 1] * pad32(dims[l + 1])));
-            max_out = std::max(max_out, dims[l + 1] * pad32(dims[l + 1]));
-            max_in = std::max(max_in, dims[l] * pad32(dims[l]));
-            max_t = std::max(max_t, dims[l + 1] * pad32(dims[l] + 1) + dims[l] * pad32(dims[l + 1]));
         }
-        chol_a = dalloc<float>(max_out);
-        chol_b = dalloc<float>(max_in);
-        tbuf = dalloc<float>(max_t);
+        ng_alloc(*this);
     }
     scal = dalloc<double>(16 * (L + 1) + 512);
     d_step = dalloc<int>(4);
@@ -163,9 +158,7 @@ Replica::~Replica() {
     for (void* p : dz) dfree(p);
     for (float* p : r_in) dfree(p);
     for (float* p : r_out) dfree(p);
-    dfree(chol_a);
-    dfree(chol_b);
-    dfree(tbuf);
+    ng_free(*this);
     dfree(scal);
     dfree(d_step);
     dfree(d_lr);
@@ -323,10 +316,12 @@ void Replica::bind(DeviceDataset* ds) {
             gemm_plan(mom_out[l], prec, true, dz[l], ld_act[l + 1], true, dz[l], ld_act[l + 1], dout, dout, B, m, sms);
         }
     }
+    if (opt == OPT_NG_KRON) ng_build_plans(*this);
     if (graph) {
         cudaGraphExecDestroy(graph);
         graph = nullptr;
     }
+    if (std::getenv("PARNN_NO_GRAPH")) use_graph = false;  // debugging: eager launches
     if (use_graph) {
         cudaStream_t s = stream;
         cudaGraph_t g;
@@ -385,14 +380,29 @@ void Replica::enqueue_step(cudaStream_t s) {
         float* coef = reinterpret_cast<float*>(scal + 16 * (L + 1) + 480);
         long* tdev = reinterpret_cast<long*>(scal + 16 * (L + 1) + 500);
         ng_coeff_kernel<<<1, 1, 0, s>>>(tdev, ng_decay, 1.0 / static_cast<double>(B), coef);
-        for (int l = 0; l < L; ++l) {
-            gemm_launch(mom_in[l], s);
-            gemm_launch(mom_out[l], s);
-            mark("gemm_ng_moments", l, gf(mom_in[l]) + gf(mom_out[l]), s);
-        }
-        for (int l = 0; l < L; ++l) {
-            ng_precondition_layer(*this, l, s);
-            ng_apply_update(*this, l, s);
+        if (prof) {  // profiled: serial on one stream so event regions are well defined
+            for (int l = 0; l < L; ++l) {
+                gemm_launch(mom_in[l], s);
+                gemm_launch(mom_out[l], s);
+                mark("gemm_ng_moments", l, gf(mom_in[l]) + gf(mom_out[l]), s);
+            }
+            for (int l = 0; l < L; ++l) {
+                ng_precondition_layer(*this, l, s);
+                ng_apply_update(*this, l, s);
+            }
+        } else {
+            // the layers' NG chains are independent: fork one stream per layer, join
+            CUDA_THROW(cudaEventRecord(ng_fork, s));
+            for (int l = L - 1; l >= 0; --l) {  // largest (output) layer first
+                cudaStream_t ls = ngl[l].stream;
+                CUDA_THROW(cudaStreamWaitEvent(ls, ng_fork, 0));
+                gemm_launch(mom_in[l], ls);
+                gemm_launch(mom_out[l], ls);
+                ng_precondition_layer(*this, l, ls);
+                ng_apply_update(*this, l, ls);
+                CUDA_THROW(cudaEventRecord(ngl[l].done, ls));
+            }
+            for (int l = 0; l < L; ++l) CUDA_THROW(cudaStreamWaitEvent(s, ngl[l].done, 0));
         }
     }
     flags_latch_kernel<<<1, 1, 0, s>>>(d_flags, d_step);

@@ -73,6 +73,30 @@ struct DevErr {
     int pad;
 };
 
+// Smoothed Kronecker factor S = R + lambda I, factored in place by the blocked
+// Cholesky of ng.cu (128-row blocks; diagonal blocks on SIMT, panel and
+// trailing updates as 3xTF32 tcgen05 GEMMs).
+constexpr int NG_NB = 128;
+struct NgFactor {
+    long n = 0, ld = 0;
+    float* a = nullptr;     // [n x ld]: S, overwritten by L (lower triangle)
+    float* linv = nullptr;  // [nblk x NB x NB]: inverses of the diagonal blocks of L
+    std::vector<GemmPlan> panel, trail;  // per block
+};
+struct NgSolve {  // X <- S^-1 X for one fixed right-hand-side buffer
+    std::vector<GemmPlan> fdiag, fupd, bdiag, bupd;  // per block
+};
+struct NgLayer {
+    NgFactor out, in;
+    NgSolve solve_out, solve_in;
+    float* t1 = nullptr;  // [dout x ldt]: [G | g_b], solved in place by S_out
+    float* t2 = nullptr;  // [din x ld2]: (S_out^-1 G)^T, solved in place by S_in
+    long ldt = 0, ld2 = 0;
+    double* part = nullptr;         // norm-reduction scratch
+    cudaStream_t stream = nullptr;  // the layer's NG chain runs concurrently with the others
+    cudaEvent_t done = nullptr;
+};
+
 struct Profile {
     std::vector<cudaEvent_t> events;
     std::vector<std::string> names;
@@ -105,9 +129,8 @@ struct Replica {
     float* zout = nullptr;  // last layer pre-activation [B x ld_act[L]]
     std::vector<void*> dz;  // per layer [B x ld_act[l+1]] (op dtype)
     std::vector<float*> r_in, r_out;  // NG factors [n x pad32(n)]
-    float* chol_a = nullptr;  // Cholesky workspace (largest factor)
-    float* chol_b = nullptr;
-    float* tbuf = nullptr;    // transpose / solve workspace (largest W)
+    std::vector<NgLayer> ngl;         // per-layer Cholesky/TRSM workspaces and GEMM plans
+    cudaEvent_t ng_fork = nullptr;
     double* scal = nullptr;   // per-layer scalars: traces, norms (device)
 
     // per-epoch device state
@@ -169,7 +192,10 @@ void launch_convert_dataset(const float* x32, long n, long ld, bf16* x16, cudaSt
 void launch_argmax_correct(const float* z, long ldz, long B, long C, const int32_t* y, unsigned long long* correct,
                            cudaStream_t s);
 
-// NG kron-full (SIMT fp32, ng.cu)
+// NG kron-full (ng.cu)
+void ng_alloc(Replica& r);
+void ng_free(Replica& r);
+void ng_build_plans(Replica& r);
 void ng_precondition_layer(Replica& r, int l, cudaStream_t s);
 void ng_apply_update(Replica& r, int l, cudaStream_t s);
 

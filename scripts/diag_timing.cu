@@ -1,0 +1,37 @@
+// Microbenchmark of the NG diagonal-block kernel phases (clock64 probes).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DPNB_DIAG_TIMING \
+//      -I paper_1507_01239_b200/csrc scripts/diag_timing.cu -o /tmp/diag_timing
+#include <cstdio>
+#include <vector>
+__device__ long long g_clk[64];
+#define PNB_CLK(i) do { if (threadIdx.x == 0) g_clk[i] = clock64(); } while (0)
+#include "ng.cu"
+int main() {
+    const int n = 128, ld = 128;
+    std::vector<float> h(n * ld);
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c < n; ++c) h[r * ld + c] = (r == c ? n : 0.f) + 1.0f / (1 + r + c);
+    float *a, *linv;
+    pnb::DevErr* err;
+    cudaMalloc(&a, n * ld * 4);
+    cudaMalloc(&linv, 128 * 128 * 4);
+    cudaMalloc(&err, sizeof(pnb::DevErr));
+    cudaMemset(err, 0, sizeof(pnb::DevErr));
+    cudaFuncSetAttribute(pnb::chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pnb::kDiagSmem);
+    for (int it = 0; it < 3; ++it) {
+        cudaMemcpy(a, h.data(), n * ld * 4, cudaMemcpyHostToDevice);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        pnb::chol_diag_kernel<<<1, 256, pnb::kDiagSmem>>>(a, ld, 0, 128, linv, err);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        long long c[64];
+        cudaMemcpyFromSymbol(c, g_clk, sizeof(c));
+        printf("iter %d: %.1f us | phases (cycles):", it, ms * 1e3);
+        for (int i = 1; i < 16 && c[i]; ++i) printf(" %lld", c[i] - c[i - 1]);
+        printf(" | err %s\n", cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
