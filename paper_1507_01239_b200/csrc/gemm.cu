@@ -111,7 +111,8 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     p.N = N;
     p.K = K;
     p.ep = ep;
-    p.grid = dim3((N + bn - 1) / bn, (M + 127) / 128, 1);
+    const long tiles = static_cast<long>((N + bn - 1) / bn) * ((M + 127) / 128);
+    p.grid = dim3(static_cast<unsigned>(std::min<long>(tiles, num_sms)), 1, 1);  // persistent
     if (split)
         p.fn = reinterpret_cast<void*>(pick<float, true>(bn, a_mn, b_mn, &p.smem));
     else if (f32)
@@ -119,7 +120,7 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     else
         p.fn = reinterpret_cast<void*>(pick<__nv_bfloat16, false>(bn, a_mn, b_mn, &p.smem));
     p.bn = bn;
-    p.threads = split ? 256 : 128;
+    p.threads = split ? 320 : 192;  // GemmSmem::kThreads
 }
 
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {

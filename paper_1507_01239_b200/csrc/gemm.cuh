@@ -101,7 +101,8 @@ __device__ __forceinline__ void st_from_float<__nv_bfloat16>(__nv_bfloat16* p, f
     *p = __float2bfloat16_rn(v);
 }
 
-// 32 consecutive values of one row -> memory, vectorised when aligned.
+// 32 consecutive values of one row -> memory, vectorised when aligned. The
+// ragged path is fully unrolled with predication so v[] stays in registers.
 template <typename T>
 __device__ __forceinline__ void store_row32(T* dst, const float (&v)[32], int valid) {
     if (valid == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -123,7 +124,9 @@ __device__ __forceinline__ void store_row32(T* dst, const float (&v)[32], int va
             }
         }
     } else {
-        for (int j = 0; j < valid; ++j) st_from_float<T>(dst + j, v[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < valid) st_from_float<T>(dst + j, v[j]);
     }
 }
 
@@ -153,6 +156,7 @@ __device__ __forceinline__ void load_row32(const T* src, float (&v)[32], int val
             }
         }
     } else {
+#pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = j < valid ? ld_as_float<T>(src + j) : 0.f;
     }
 }
@@ -168,14 +172,111 @@ struct GemmSmem {
     static constexpr int kLoad = kABytes + kBBytes;          // bytes TMA brings per stage
     static constexpr int kStage = kLoad * (SPLIT ? 2 : 1);   // + low-part copies for 3xTF32
     static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 512 /*barriers*/;
+    static constexpr int kThreads = SPLIT ? 320 : 192;       // + 4 splitter warps
+    static constexpr uint32_t kTmemCols = 2 * BN;            // double-buffered accumulator
 };
 
-// SPLIT (fp32 mode, T = float): 3xTF32. Four extra warps split every staged
-// operand x into hi = x with the low 13 mantissa bits cleared (exact TF32,
-// written back in place) and lo = x - hi (exact in fp32), then the MMA warp
+// Epilogue of one 32-column chunk of one accumulator row.
+template <typename T>
+__device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, float (&v)[32], int row, int n, int valid,
+                                               float lr) {
+    bool bad = false;
+    switch (ep.mode) {
+        case EPI_FWD_ACT: {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                v[j] = ep.out_scale * act_fwd(ep.act, v[j] + (j < valid ? ep.bias[n + j] : 0.f));
+            store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
+            break;
+        }
+        case EPI_FWD_LINEAR: {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += (j < valid ? ep.bias[n + j] : 0.f);
+            store_row32<float>(ep.out32 + row * ep.ld_out32 + n, v, valid);
+            break;
+        }
+        case EPI_GRAD: {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                v[j] *= ep.alpha;
+                bad |= (j < valid) && !isfinite(v[j]);
+            }
+            store_row32<float>(ep.out32 + row * ep.ld_out32 + n, v, valid);
+            break;
+        }
+        case EPI_GRAD_SGD: {
+            float w[32];
+            float* wp = ep.out32 + row * ep.ld_out32 + n;
+            load_row32<float>(wp, w, valid);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float g = v[j] * ep.alpha;
+                bad |= (j < valid) && !isfinite(g);
+                w[j] -= lr * g;
+            }
+            store_row32<float>(wp, w, valid);
+            if (ep.shadow) store_row32<__nv_bfloat16>(ep.shadow + row * ep.ld_shadow + n, w, valid);
+            break;
+        }
+        case EPI_ACTGRAD: {
+            float a[32];
+            load_row32<T>(static_cast<const T*>(ep.aux) + row * ep.ld_aux + n, a, valid);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= act_grad(ep.act, a[j]);
+            store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
+            break;
+        }
+        case EPI_EMA: {
+            float o[32];
+            float* op = ep.out32 + row * ep.ld_out32 + n;
+            const float beta = ep.coef ? ep.coef[0] : ep.beta;
+            const float alpha = ep.coef ? ep.coef[1] : ep.alpha;
+            if (beta != 0.f) load_row32<float>(op, o, valid);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] = (beta != 0.f ? beta * o[j] : 0.f) + alpha * v[j];
+            store_row32<float>(op, o, valid);
+            break;
+        }
+        case EPI_SUB: {
+            float o[32];
+            float* op = ep.out32 + row * ep.ld_out32 + n;
+            load_row32<float>(op, o, valid);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] -= v[j];
+            store_row32<float>(op, o, valid);
+            break;
+        }
+        case EPI_AXPY: {
+            float w[32];
+            float* wp = ep.out32 + row * ep.ld_out32 + n;
+            load_row32<float>(wp, w, valid);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w[j] += ep.alpha * v[j];
+            store_row32<float>(wp, w, valid);
+            if (ep.shadow) store_row32<__nv_bfloat16>(ep.shadow + row * ep.ld_shadow + n, w, valid);
+            break;
+        }
+        default:
+            break;
+    }
+    return bad;
+}
+
+// Persistent, warp-specialised tcgen05 GEMM. grid <= #tiles; CTA c handles
+// tiles c, c + grid, ... (m fastest). Roles:
+//   warp 0      TMA producer (one elected lane), STAGES-deep smem ring
+//   warp 1      MMA issuer (one elected lane); owns the TMEM allocation
+//   warps 2-5   epilogue: TMEM lane quadrant (warp % 4) -> registers -> global
+//   warps 6-9   (SPLIT only) 3xTF32 splitters
+// The accumulator is double buffered in TMEM (2 x BN columns), so the
+// epilogue of tile i overlaps the mainloop of tile i+1.
+//
+// SPLIT (fp32 mode, T = float): 3xTF32. The splitters rewrite every staged
+// operand x as hi = x with the low 13 mantissa bits cleared (exact TF32, in
+// place) and lo = x - hi (exact in fp32) next to it; the MMA warp then
 // accumulates hi*hi + hi*lo + lo*hi: relative error ~2^-21 instead of 2^-11.
 template <typename T, int BN, int STAGES, bool A_MN, bool B_MN, bool SPLIT>
-__global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
+__global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, GemmEpi ep) {
     using S = GemmSmem<BN, STAGES, T, SPLIT>;
@@ -188,15 +289,16 @@ __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
     uint64_t* empty = full + STAGES;
     uint64_t* split_done = empty + STAGES;
-    uint64_t* done = split_done + STAGES;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* tfull = split_done + STAGES;  // [2] accumulator ready for the epilogue
+    uint64_t* tempty = tfull + 2;           // [2] accumulator drained by the epilogue
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * 128;
-    const int n0 = blockIdx.x * BN;
+    const int tiles_m = (M + 127) / 128;
+    const int tiles = tiles_m * ((N + BN - 1) / BN);
     const int nk = (K + S::kBK - 1) / S::kBK;
-    if (ep.lower && n0 > m0 + 127) return;  // whole tile above the diagonal: nothing to do
+    auto tile_skipped = [&](int m0, int n0) { return ep.lower && n0 > m0 + 127; };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -204,206 +306,158 @@ __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
             mbar_init(&empty[s], 1);
             mbar_init(&split_done[s], 128);
         }
-        mbar_init(done, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 128);
+        }
         fence_barrier_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
     }
-    if (warp == 1) tmem_alloc<(BN < 32 ? 32 : BN)>(tslot);
+    if (warp == 1) tmem_alloc<S::kTmemCols>(tslot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
 
-    if (warp == 0 && lane == 0) {
+    if (warp == 0) {
         // ---------------- TMA producer ----------------
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % STAGES;
-            if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
-            uint8_t* sa = smem + s * S::kStage;
-            uint8_t* sb = sa + S::kABytes;
-            mbar_arrive_expect_tx(&full[s], S::kLoad);
-            const int k0 = kb * S::kBK;
-            if constexpr (!A_MN) {
-                tma_load_2d(sa, &tmA, &full[s], k0, m0);
-            } else {
+        if (lane == 0) {
+            int it = 0;  // global k-block counter (ring position)
+            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+                const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
+                if (tile_skipped(m0, n0)) continue;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+                    uint8_t* sa = smem + s * S::kStage;
+                    uint8_t* sb = sa + S::kABytes;
+                    mbar_arrive_expect_tx(&full[s], S::kLoad);
+                    const int k0 = kb * S::kBK;
+                    if constexpr (!A_MN) {
+                        tma_load_2d(sa, &tmA, &full[s], k0, m0);
+                    } else {
 #pragma unroll
-                for (int a = 0; a < 128 / S::kAtom; ++a)
-                    tma_load_2d(sa + a * (S::kBK * 128), &tmA, &full[s], m0 + a * S::kAtom, k0);
-            }
-            if constexpr (!B_MN) {
-                tma_load_2d(sb, &tmB, &full[s], k0, n0);
-            } else {
+                        for (int a = 0; a < 128 / S::kAtom; ++a)
+                            tma_load_2d(sa + a * (S::kBK * 128), &tmA, &full[s], m0 + a * S::kAtom, k0);
+                    }
+                    if constexpr (!B_MN) {
+                        tma_load_2d(sb, &tmB, &full[s], k0, n0);
+                    } else {
 #pragma unroll
-                for (int a = 0; a < BN / S::kAtom; ++a)
-                    tma_load_2d(sb + a * (S::kBK * 128), &tmB, &full[s], n0 + a * S::kAtom, k0);
+                        for (int a = 0; a < BN / S::kAtom; ++a)
+                            tma_load_2d(sb + a * (S::kBK * 128), &tmB, &full[s], n0 + a * S::kAtom, k0);
+                    }
+                }
             }
         }
-    } else if (warp == 1 && lane == 0) {
+    } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
-        constexpr uint32_t idesc = make_idesc(OpTraits<T>::kFmt, A_MN ? 1 : 0, B_MN ? 1 : 0, 128, BN);
-        constexpr uint32_t kMnLayout = kTf32 ? 1 : 2;  // BASE32B for TF32 MN-major
-        constexpr uint32_t kMnSbo = kTf32 ? 512 : 1024;
-        auto desc_a = [&](uint32_t base, int k) {
-            return A_MN ? smem_desc_sw128(base + k * S::kUK * 128, S::kBK * 128, kMnSbo, kMnLayout)
-                        : smem_desc_sw128(base + k * 32, 16, 1024);
-        };
-        auto desc_b = [&](uint32_t base, int k) {
-            return B_MN ? smem_desc_sw128(base + k * S::kUK * 128, S::kBK * 128, kMnSbo, kMnLayout)
-                        : smem_desc_sw128(base + k * 32, 16, 1024);
-        };
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % STAGES;
-            mbar_wait(SPLIT ? &split_done[s] : &full[s], (kb / STAGES) & 1);
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc(OpTraits<T>::kFmt, A_MN ? 1 : 0, B_MN ? 1 : 0, 128, BN);
+            constexpr uint32_t kMnLayout = kTf32 ? 1 : 2;  // BASE32B for TF32 MN-major
+            constexpr uint32_t kMnSbo = kTf32 ? 512 : 1024;
+            auto desc_a = [&](uint32_t base, int k) {
+                return A_MN ? smem_desc_sw128(base + k * S::kUK * 128, S::kBK * 128, kMnSbo, kMnLayout)
+                            : smem_desc_sw128(base + k * 32, 16, 1024);
+            };
+            auto desc_b = [&](uint32_t base, int k) {
+                return B_MN ? smem_desc_sw128(base + k * S::kUK * 128, S::kBK * 128, kMnSbo, kMnLayout)
+                            : smem_desc_sw128(base + k * 32, 16, 1024);
+            };
+            int it = 0, local = 0;
+            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+                const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
+                if (tile_skipped(m0, n0)) continue;
+                const int acc = local & 1;
+                if (local >= 2) mbar_wait(&tempty[acc], ((local >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(SPLIT ? &split_done[s] : &full[s], (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + s * S::kStage);
+                    const uint32_t sb = sa + S::kABytes;
+#pragma unroll
+                    for (int k = 0; k < S::kBK / S::kUK; ++k) {
+                        umma<kTf32>(d, desc_a(sa, k), desc_b(sb, k), idesc, (kb | k) != 0 ? 1u : 0u);
+                        if constexpr (SPLIT) {
+                            const uint32_t sal = sa + S::kLoad, sbl = sb + S::kLoad;
+                            umma<kTf32>(d, desc_a(sa, k), desc_b(sbl, k), idesc, 1u);
+                            umma<kTf32>(d, desc_a(sal, k), desc_b(sb, k), idesc, 1u);
+                        }
+                    }
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[acc]);
+                ++local;
+            }
+        }
+    } else if (warp < 6) {
+        // ---------------- epilogue (4 warps = 128 TMEM lanes) ----------------
+        const int quad = warp & 3;
+        float lr = 0.f;
+        if (ep.mode == EPI_GRAD_SGD) lr = ep.lr[ep.step ? *ep.step : 0];
+        bool bad = false;
+        int local = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
+            if (tile_skipped(m0, n0)) continue;
+            const int acc = local & 1;
+            mbar_wait(&tfull[acc], (local >> 1) & 1);
             tc_fence_after();
-            const uint32_t sa = smem_u32(smem + s * S::kStage);
-            const uint32_t sb = sa + S::kABytes;
-#pragma unroll
-            for (int k = 0; k < S::kBK / S::kUK; ++k) {
-                umma<kTf32>(tmem, desc_a(sa, k), desc_b(sb, k), idesc, (kb | k) != 0 ? 1u : 0u);
-                if constexpr (SPLIT) {
-                    const uint32_t sal = sa + S::kLoad, sbl = sb + S::kLoad;
-                    umma<kTf32>(tmem, desc_a(sa, k), desc_b(sbl, k), idesc, 1u);
-                    umma<kTf32>(tmem, desc_a(sal, k), desc_b(sb, k), idesc, 1u);
-                }
-            }
-            umma_commit(&empty[s]);
-        }
-        umma_commit(done);
-    } else if (SPLIT && warp >= 4) {
-        // ---------------- 3xTF32 splitters (warps 4-7) ----------------
-        const int t = threadIdx.x - 128;
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % STAGES;
-            mbar_wait(&full[s], (kb / STAGES) & 1);
-            float4* hi = reinterpret_cast<float4*>(smem + s * S::kStage);
-            float4* lo = reinterpret_cast<float4*>(smem + s * S::kStage + S::kLoad);
-#pragma unroll 4
-            for (int i = t; i < S::kLoad / 16; i += 128) {
-                float4 x = hi[i], h, l;
-                h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-                h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-                h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-                h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-                l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
-                hi[i] = h;
-                lo[i] = l;
-            }
-            fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
-            mbar_arrive(&split_done[s]);
-        }
-    }
-    __syncwarp();
-    if (SPLIT && warp >= 4) {  // splitters take no part in the epilogue
-        tc_fence_before();
-        __syncthreads();
-        return;
-    }
-
-    // ---------------- epilogue: TMEM -> registers -> global ----------------
-    mbar_wait(done, 0);
-    tc_fence_after();
-    const int row = m0 + warp * 32 + lane;
-    const bool row_ok = row < M;
-    float lr = 0.f;
-    if (ep.mode == EPI_GRAD_SGD) lr = ep.lr[ep.step ? *ep.step : 0];
-    bool bad = false;
+            const int row = m0 + quad * 32 + lane;
+            const bool row_ok = row < M;
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-        const int n = n0 + c * 32;
-        if (n >= N) break;  // warp-uniform
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 32, r);
-        tmem_ld_wait();
-        if (!row_ok) continue;
-        const int valid = min(32, N - n);
-        float v[32];
+            for (int c = 0; c < BN / 32; ++c) {
+                const int n = n0 + c * 32;
+                if (n >= N) break;  // warp-uniform
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c * 32, r);
+                tmem_ld_wait();
+                if (!row_ok) continue;
+                float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        switch (ep.mode) {
-            case EPI_FWD_ACT: {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    v[j] = ep.out_scale * act_fwd(ep.act, v[j] + (j < valid ? ep.bias[n + j] : 0.f));
-                store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
-                break;
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                bad |= epilogue_chunk<T>(ep, v, row, n, min(32, N - n), lr);
             }
-            case EPI_FWD_LINEAR: {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] += (j < valid ? ep.bias[n + j] : 0.f);
-                store_row32<float>(ep.out32 + row * ep.ld_out32 + n, v, valid);
-                break;
-            }
-            case EPI_GRAD: {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    v[j] *= ep.alpha;
-                    bad |= !isfinite(v[j]);
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+            ++local;
+        }
+        if (bad && ep.flag) atomicOr(ep.flag, 1u << ep.flag_bit);
+    } else if (SPLIT) {
+        // ---------------- 3xTF32 splitters (warps 6-9) ----------------
+        const int t = threadIdx.x - 192;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
+            if (tile_skipped(m0, n0)) continue;
+            for (int kb = 0; kb < nk; ++kb, ++it) {
+                const int s = it % STAGES;
+                mbar_wait(&full[s], (it / STAGES) & 1);
+                float4* hi = reinterpret_cast<float4*>(smem + s * S::kStage);
+                float4* lo = reinterpret_cast<float4*>(smem + s * S::kStage + S::kLoad);
+#pragma unroll 4
+                for (int i = t; i < S::kLoad / 16; i += 128) {
+                    float4 x = hi[i], h, l;
+                    h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+                    h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+                    h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+                    h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+                    l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+                    hi[i] = h;
+                    lo[i] = l;
                 }
-                store_row32<float>(ep.out32 + row * ep.ld_out32 + n, v, valid);
-                break;
+                fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+                mbar_arrive(&split_done[s]);
             }
-            case EPI_GRAD_SGD: {
-                float w[32];
-                float* wp = ep.out32 + row * ep.ld_out32 + n;
-                load_row32<float>(wp, w, valid);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float g = v[j] * ep.alpha;
-                    bad |= (j < valid) && !isfinite(g);
-                    w[j] -= lr * g;
-                }
-                store_row32<float>(wp, w, valid);
-                if (ep.shadow) store_row32<__nv_bfloat16>(ep.shadow + row * ep.ld_shadow + n, w, valid);
-                break;
-            }
-            case EPI_ACTGRAD: {
-                float a[32];
-                load_row32<T>(static_cast<const T*>(ep.aux) + row * ep.ld_aux + n, a, valid);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] *= act_grad(ep.act, a[j]);
-                store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
-                break;
-            }
-            case EPI_EMA: {
-                float o[32];
-                float* op = ep.out32 + row * ep.ld_out32 + n;
-                const float beta = ep.coef ? ep.coef[0] : ep.beta;
-                const float alpha = ep.coef ? ep.coef[1] : ep.alpha;
-                if (beta != 0.f) load_row32<float>(op, o, valid);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) o[j] = (beta != 0.f ? beta * o[j] : 0.f) + alpha * v[j];
-                store_row32<float>(op, o, valid);
-                break;
-            }
-            case EPI_SUB: {
-                float o[32];
-                float* op = ep.out32 + row * ep.ld_out32 + n;
-                load_row32<float>(op, o, valid);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) o[j] -= v[j];
-                store_row32<float>(op, o, valid);
-                break;
-            }
-            case EPI_AXPY: {
-                float w[32];
-                float* wp = ep.out32 + row * ep.ld_out32 + n;
-                load_row32<float>(wp, w, valid);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) w[j] += ep.alpha * v[j];
-                store_row32<float>(wp, w, valid);
-                if (ep.shadow) store_row32<__nv_bfloat16>(ep.shadow + row * ep.ld_shadow + n, w, valid);
-                break;
-            }
-            default:
-                break;
         }
     }
-    if (bad && ep.flag) atomicOr(ep.flag, 1u << ep.flag_bit);
-
     tc_fence_before();
-    __syncthreads();  // (SPLIT: matched by the splitters' barrier above)
-    if (warp == 1) tmem_dealloc<(BN < 32 ? 32 : BN)>(tmem);
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<S::kTmemCols>(tmem);
 }
 
 }  // namespace pnb
