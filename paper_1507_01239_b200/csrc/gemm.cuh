@@ -405,10 +405,25 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
             const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
             if (tile_skipped(m0, n0)) continue;
             const int acc = local & 1;
-            mbar_wait(&tfull[acc], (local >> 1) & 1);
-            tc_fence_after();
             const int row = m0 + quad * 32 + lane;
             const bool row_ok = row < M;
+            // Pull this tile's epilogue source rows (weights / activations /
+            // factors being read-modify-written) into L2 while the MMAs run:
+            // otherwise each 32-column chunk pays a full DRAM round trip.
+            if (row_ok) {
+                const char* src = nullptr;
+                long bytes = 0;
+                if (ep.mode == EPI_GRAD_SGD || ep.mode == EPI_EMA || ep.mode == EPI_SUB || ep.mode == EPI_AXPY) {
+                    src = reinterpret_cast<const char*>(ep.out32 + row * ep.ld_out32 + n0);
+                    bytes = static_cast<long>(min(BN, N - n0)) * 4;
+                } else if (ep.mode == EPI_ACTGRAD) {
+                    src = static_cast<const char*>(ep.aux) + (row * ep.ld_aux + n0) * static_cast<long>(sizeof(T));
+                    bytes = static_cast<long>(min(BN, N - n0)) * static_cast<long>(sizeof(T));
+                }
+                for (long o = 0; o < bytes; o += 128) prefetch_l2(src + o);
+            }
+            mbar_wait(&tfull[acc], (local >> 1) & 1);
+            tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 const int n = n0 + c * 32;

@@ -68,6 +68,57 @@ __device__ __forceinline__ float block_reduce_sum(float v, float* sh) {
 
 // softmax_rows + cross_entropy + dz init (network.cpp:76-92, 145-160, 194-197):
 // per row, max-subtracted softmax, CE_i = lse_i - z_{i,y}, dz = p - onehot.
+// Register-resident variant (C <= 4 * 256 * kVec): one read of the row, float4
+// loads, exp computed once.
+constexpr int kVec = 12;
+template <typename T>
+__global__ void __launch_bounds__(256) softmax_ce_reg_kernel(const float* __restrict__ z, long ldz, long C,
+                                                             const int32_t* __restrict__ y, T* __restrict__ dz,
+                                                             long lddz, float* __restrict__ ce_rows) {
+    __shared__ float sh[33];
+    const long i = blockIdx.x;
+    const float4* zr = reinterpret_cast<const float4*>(z + i * ldz);
+    float4 v[kVec];
+    float m = -FLT_MAX;
+#pragma unroll
+    for (int k = 0; k < kVec; ++k) {
+        const long q = threadIdx.x + 256L * k, j = 4 * q;
+        if (j + 3 < C) {
+            v[k] = zr[q];
+        } else {
+            const float* s = z + i * ldz + j;
+            v[k].x = j < C ? s[0] : -FLT_MAX;
+            v[k].y = j + 1 < C ? s[1] : -FLT_MAX;
+            v[k].z = j + 2 < C ? s[2] : -FLT_MAX;
+            v[k].w = -FLT_MAX;
+        }
+        m = fmaxf(m, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
+    }
+    m = block_reduce_max(m, sh);
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < kVec; ++k) {
+        v[k].x = expf(v[k].x - m);
+        v[k].y = expf(v[k].y - m);
+        v[k].z = expf(v[k].z - m);
+        v[k].w = expf(v[k].w - m);
+        s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+    }
+    s = block_reduce_sum(s, sh);
+    const float inv = 1.f / s;
+    const int lab = y[i];
+    T* dr = dz + i * lddz;
+#pragma unroll
+    for (int k = 0; k < kVec; ++k) {
+        const long j = 4 * (threadIdx.x + 256L * k);
+        const float p[4] = {v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (j + e < C) dr[j + e] = static_cast<T>(j + e == lab ? p[e] - 1.f : p[e]);
+    }
+    if (threadIdx.x == 0) ce_rows[i] = logf(s) + m - z[i * ldz + lab];
+}
+
 template <typename T>
 __global__ void softmax_ce_kernel(const float* __restrict__ z, long ldz, long C, const int32_t* __restrict__ y,
                                   T* __restrict__ dz, long lddz, float* __restrict__ ce_rows) {
@@ -116,16 +167,18 @@ template <typename T>
 __global__ void bias_grad_kernel(const T* __restrict__ dz, long lddz, long B, long C, float* __restrict__ bias,
                                  float* __restrict__ gb, const float* __restrict__ lr, const int* __restrict__ step,
                                  unsigned* __restrict__ flags, unsigned bit) {
-    __shared__ float sh[8][33];
+    __shared__ float sh[32][33];
     const long j = blockIdx.x * 32 + threadIdx.x;
     float acc = 0.f;
-    if (j < C)
-        for (long b = threadIdx.y; b < B; b += 8) acc += to_f<T>(dz[b * lddz + j]);
+    if (j < C) {
+#pragma unroll 8
+        for (long b = threadIdx.y; b < B; b += 32) acc += to_f<T>(dz[b * lddz + j]);
+    }
     sh[threadIdx.y][threadIdx.x] = acc;
     __syncthreads();
     if (threadIdx.y == 0 && j < C) {
         float s = 0.f;
-        for (int r = 0; r < 8; ++r) s += sh[r][threadIdx.x];
+        for (int r = 0; r < 32; ++r) s += sh[r][threadIdx.x];
         const float g = s * (1.f / static_cast<float>(B));
         if (!isfinite(g) && flags) atomicOr(flags, 1u << bit);
         if (gb) gb[j] = g;
@@ -185,9 +238,15 @@ void launch_gather(const void* x, long ldx, const int32_t* y, const uint32_t* ro
 void launch_softmax_ce(const float* z, long ldz, long B, long C, const int32_t* y, void* dz, long lddz,
                        float* ce_rows, bool f32, cudaStream_t s) {
     if (f32)
-        softmax_ce_kernel<float><<<B, 256, 0, s>>>(z, ldz, C, y, static_cast<float*>(dz), lddz, ce_rows);
+        if (C <= 4 * 256 * kVec)
+            softmax_ce_reg_kernel<float><<<B, 256, 0, s>>>(z, ldz, C, y, static_cast<float*>(dz), lddz, ce_rows);
+        else
+            softmax_ce_kernel<float><<<B, 256, 0, s>>>(z, ldz, C, y, static_cast<float*>(dz), lddz, ce_rows);
     else
-        softmax_ce_kernel<bf16><<<B, 256, 0, s>>>(z, ldz, C, y, static_cast<bf16*>(dz), lddz, ce_rows);
+        if (C <= 4 * 256 * kVec)
+            softmax_ce_reg_kernel<bf16><<<B, 256, 0, s>>>(z, ldz, C, y, static_cast<bf16*>(dz), lddz, ce_rows);
+        else
+            softmax_ce_kernel<bf16><<<B, 256, 0, s>>>(z, ldz, C, y, static_cast<bf16*>(dz), lddz, ce_rows);
 }
 
 void launch_ce_reduce(const float* ce_rows, long B, double* d_ce, int* step, int advance, cudaStream_t s) {
@@ -196,7 +255,7 @@ void launch_ce_reduce(const float* ce_rows, long B, double* d_ce, int* step, int
 
 void launch_bias_grad(const void* dz, long lddz, long B, long C, bool f32, float* bias, float* gb, const float* lr,
                       const int* step, unsigned* flags, unsigned bit, cudaStream_t s) {
-    dim3 grid((C + 31) / 32), block(32, 8);
+    dim3 grid((C + 31) / 32), block(32, 32);
     if (f32)
         bias_grad_kernel<float><<<grid, block, 0, s>>>(static_cast<const float*>(dz), lddz, B, C, bias, gb, lr, step,
                                                        flags, bit);

@@ -110,7 +110,15 @@ Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision
     if (B <= 0) throw std::runtime_error("replica: minibatch must be >= 1");
     CUDA_THROW(cudaSetDevice(c->device));
     CUDA_THROW(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CUDA_THROW(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    CUDA_THROW(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
     L = static_cast<int>(dims.size()) - 1;
+    ev_bwd.resize(L);
+    ev_dw.resize(L);
+    for (int l = 0; l < L; ++l) {
+        CUDA_THROW(cudaEventCreateWithFlags(&ev_bwd[l], cudaEventDisableTiming));
+        CUDA_THROW(cudaEventCreateWithFlags(&ev_dw[l], cudaEventDisableTiming));
+    }
     long off = 0;
     for (int l = 0; l < L; ++l) {
         ldw.push_back(pad32(dims[l]));
@@ -168,6 +176,10 @@ Replica::~Replica() {
     dfree(d_ce);
     dfree(d_flags);
     dfree(d_err);
+    for (auto e : ev_bwd) cudaEventDestroy(e);
+    for (auto e : ev_dw) cudaEventDestroy(e);
+    if (ev_side) cudaEventDestroy(ev_side);
+    if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -365,6 +377,41 @@ void Replica::enqueue_step(cudaStream_t s) {
     launch_softmax_ce(zout, ld_act[L], B, dims[L], d_ybatch, dz[L - 1], ld_act[L], ce_rows, F, s);
     mark("softmax_ce", L - 1, 0, s);
     const bool ng = opt == OPT_NG_KRON;
+    float* coef = reinterpret_cast<float*>(scal + 16 * (L + 1) + 480);
+    long* tdev = reinterpret_cast<long*>(scal + 16 * (L + 1) + 500);
+    if (!prof) {
+        // Concurrent backward: dA_l stays on the main stream (it carries the
+        // dz chain), dW_l goes to the side stream as soon as dA_l has read W_l
+        // (SGD) / dz_l exists (NG); layer l's NG chain starts right after dW_l,
+        // so the output layer's long Cholesky/TRSM chain overlaps the rest of
+        // the backward pass.
+        if (ng) ng_coeff_kernel<<<1, 1, 0, s>>>(tdev, ng_decay, 1.0 / static_cast<double>(B), coef);
+        for (int l = L - 1; l >= 0; --l) {
+            launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
+                             ng ? grads + b_off[l] : nullptr, d_lr, d_step, d_flags, 2 * l + 1, s);
+            if (l > 0) gemm_launch(da[l], s);
+            CUDA_THROW(cudaEventRecord(ev_bwd[l], s));
+            CUDA_THROW(cudaStreamWaitEvent(side, ev_bwd[l], 0));
+            gemm_launch(dw[l], side);
+            if (ng) {
+                CUDA_THROW(cudaEventRecord(ev_dw[l], side));
+                cudaStream_t ls = ngl[l].stream;
+                CUDA_THROW(cudaStreamWaitEvent(ls, ev_dw[l], 0));
+                gemm_launch(mom_in[l], ls);
+                gemm_launch(mom_out[l], ls);
+                ng_precondition_layer(*this, l, ls);
+                ng_apply_update(*this, l, ls);
+                CUDA_THROW(cudaEventRecord(ngl[l].done, ls));
+            }
+        }
+        CUDA_THROW(cudaEventRecord(ev_side, side));
+        CUDA_THROW(cudaStreamWaitEvent(s, ev_side, 0));
+        if (ng)
+            for (int l = 0; l < L; ++l) CUDA_THROW(cudaStreamWaitEvent(s, ngl[l].done, 0));
+        flags_latch_kernel<<<1, 1, 0, s>>>(d_flags, d_step);
+        launch_ce_reduce(ce_rows, B, d_ce, d_step, 1, s);
+        return;
+    }
     for (int l = L - 1; l >= 0; --l) {
         launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
                          ng ? grads + b_off[l] : nullptr, d_lr, d_step, d_flags, 2 * l + 1, s);
@@ -377,8 +424,6 @@ void Replica::enqueue_step(cudaStream_t s) {
         mark(ng ? "gemm_dw" : "gemm_dw_sgd", l, gf(dw[l]), s);
     }
     if (ng) {
-        float* coef = reinterpret_cast<float*>(scal + 16 * (L + 1) + 480);
-        long* tdev = reinterpret_cast<long*>(scal + 16 * (L + 1) + 500);
         ng_coeff_kernel<<<1, 1, 0, s>>>(tdev, ng_decay, 1.0 / static_cast<double>(B), coef);
         if (prof) {  // profiled: serial on one stream so event regions are well defined
             for (int l = 0; l < L; ++l) {

@@ -106,6 +106,9 @@ struct Profile {
 struct Replica {
     Context* ctx;
     cudaStream_t stream = nullptr;  // private stream: local replicas step concurrently
+    cudaStream_t side = nullptr;    // dW GEMMs, concurrent with the dA chain
+    std::vector<cudaEvent_t> ev_bwd, ev_dw;
+    cudaEvent_t ev_side = nullptr;
     std::vector<long> dims;  // input, hidden..., output
     int L = 0;
     int act = 0;

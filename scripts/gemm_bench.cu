@@ -1,0 +1,60 @@
+// GEMM microbenchmark (warm L2, CUDA events, 20 reps) over the trainer's shapes.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1507_01239_b200/csrc -I include \
+//   scripts/gemm_bench.cu -o scripts/gemm_bench.bin -Lpaper_1507_01239_b200 -lparnn_b200 -Xlinker -rpath ...
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include "runtime.h"
+using namespace pnb;
+int main(int argc, char** argv) {
+    int bnf = argc > 1 ? atoi(argv[1]) : 0;
+    struct Case { const char* name; int prec; bool amn, bmn; int M, N, K; };
+    std::vector<Case> cases = {
+        {"fwd hidden 1024x2048x2048", 0, false, false, 1024, 2048, 2048},
+        {"fwd out    1024x8806x2048", 0, false, false, 1024, 8806, 2048},
+        {"dW hidden  2048x2048x1024", 0, true, true, 2048, 2048, 1024},
+        {"dW out     8806x2048x1024", 0, true, true, 8806, 2048, 1024},
+        {"dA hidden  1024x2048x2048", 0, false, true, 1024, 2048, 2048},
+        {"dA out     1024x2048x8806", 0, false, true, 1024, 2048, 8806},
+        {"big        8192x8192x8192", 0, false, false, 8192, 8192, 8192},
+        {"f32 trsm   8678x2049x128 ", 2, false, true, 8678, 2049, 128},
+        {"f32 trail  8678x8678x128 ", 2, false, false, 8678, 8678, 128},
+    };
+    void *A, *B;
+    float* C;
+    size_t maxe = 8192L * 8192;
+    cudaMalloc(&A, maxe * 4);
+    cudaMalloc(&B, maxe * 4);
+    cudaMalloc(&C, maxe * 4);
+    cudaMemset(A, 0, maxe * 4);
+    cudaMemset(B, 0, maxe * 4);
+    int sms = 148;
+    for (auto& c : cases) {
+        GemmPlan p;
+        GemmEpi e;
+        e.mode = EPI_GRAD;
+        e.out32 = C;
+        e.ld_out32 = (c.N + 31) / 32 * 32;
+        long lda = c.amn ? (c.M + 31) / 32 * 32 : (c.K + 31) / 32 * 32;
+        long ldb = c.bmn ? (c.N + 31) / 32 * 32 : (c.K + 31) / 32 * 32;
+        gemm_plan(p, c.prec, c.amn, A, lda, c.bmn, B, ldb, c.M, c.N, c.K, e, sms, bnf);
+        cudaStream_t s;
+        cudaStreamCreate(&s);
+        for (int i = 0; i < 3; ++i) gemm_launch(p, s);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, s);
+        const int reps = 20;
+        for (int i = 0; i < reps; ++i) gemm_launch(p, s);
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        double us = ms * 1e3 / reps;
+        double fl = 2.0 * c.M * c.N * c.K * (c.prec == 2 ? 3 : 1);
+        printf("%-28s bn=%3d grid=%3d  %8.2f us  %7.1f TFLOP/s%s  %s\n", c.name, p.bn, p.grid.x, us, fl / us / 1e6,
+               c.prec == 2 ? " (tf32 MMA rate, 3x)" : "", cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
