@@ -424,28 +424,42 @@ float* linv_blk(NgFactor& f, long j) { return f.linv + (j / NB) * NB * NB; }
 
 void build_factor(NgFactor& f, int sms) {
     f.panel.clear();
-    f.trail.clear();
+    f.col.clear();
+    f.rest.clear();
     for (long j = 0; j < f.n; j += NB) {
-        const long b = std::min<long>(NB, f.n - j), rest = f.n - j - b;
-        GemmPlan pp, tp;
-        if (rest > 0) {
+        const long b = std::min<long>(NB, f.n - j), below = f.n - j - b;
+        GemmPlan pp, cp, rp;
+        if (below > 0) {
             float* a21 = f.a + (j + b) * f.ld + j;
             GemmEpi e;  // A21 <- A21 L_jj^-T, in place (one N tile: BN = 128 >= b)
             e.mode = EPI_GRAD;
             e.alpha = 1.f;
             e.out32 = a21;
             e.ld_out32 = f.ld;
-            gemm_plan(pp, PREC_FP32, false, a21, f.ld, false, linv_blk(f, j), NB, (int)rest, (int)b, (int)b, e, sms,
+            gemm_plan(pp, PREC_FP32, false, a21, f.ld, false, linv_blk(f, j), NB, (int)below, (int)b, (int)b, e, sms,
                       128);
-            GemmEpi u;  // A22 -= A21 A21^T (lower tiles)
-            u.mode = EPI_SUB;
-            u.lower = 1;
-            u.out32 = f.a + (j + b) * f.ld + (j + b);
-            u.ld_out32 = f.ld;
-            gemm_plan(tp, PREC_FP32, false, a21, f.ld, false, a21, f.ld, (int)rest, (int)rest, (int)b, u, sms);
+            // look-ahead: block column j+1 first (rows >= j+1) ...
+            const long bn1 = std::min<long>(NB, below);
+            GemmEpi c;
+            c.mode = EPI_SUB;
+            c.out32 = f.a + (j + b) * f.ld + (j + b);
+            c.ld_out32 = f.ld;
+            gemm_plan(cp, PREC_FP32, false, a21, f.ld, false, a21, f.ld, (int)below, (int)bn1, (int)b, c, sms);
+            // ... then the rest of the trailing matrix (rows/cols >= j+2), lower tiles only
+            const long rest = below - bn1;
+            if (rest > 0) {
+                float* a31 = a21 + bn1 * f.ld;
+                GemmEpi u;
+                u.mode = EPI_SUB;
+                u.lower = 1;
+                u.out32 = f.a + (j + b + bn1) * f.ld + (j + b + bn1);
+                u.ld_out32 = f.ld;
+                gemm_plan(rp, PREC_FP32, false, a31, f.ld, false, a31, f.ld, (int)rest, (int)rest, (int)b, u, sms);
+            }
         }
         f.panel.push_back(pp);
-        f.trail.push_back(tp);
+        f.col.push_back(cp);
+        f.rest.push_back(rp);
     }
 }
 
@@ -487,29 +501,53 @@ void build_solve(NgFactor& f, NgSolve& sv, float* x, long ldx, long c, int sms) 
     }
 }
 
-void cholesky(Replica& r, int l, NgFactor& f, DevErr* err, cudaStream_t s) {
+// Blocked Cholesky with look-ahead. fs carries the critical path
+// diag(j) -> panel(j) -> col(j) [-> diag(j+1)]; the bulk rest(j) runs on ts
+// concurrently with diag(j+1)/panel(j+1). col(j) must see rest(j-1) (both
+// update block column j+1), so fs waits for it first. ev_panel[j] tells the
+// forward solve that block column j of L is final.
+void cholesky(Replica& r, int l, NgFactor& f, DevErr* err, cudaStream_t fs, cudaStream_t ts, bool conc) {
     size_t blk = 0;
     for (long j = 0; j < f.n; j += NB, ++blk) {
         const int b = (int)std::min<long>(NB, f.n - j);
-        chol_diag_kernel<<<1, 256, kDiagSmem, s>>>(f.a, f.ld, j, b, linv_blk(f, j), err);
+        chol_diag_kernel<<<1, 256, kDiagSmem, fs>>>(f.a, f.ld, j, b, linv_blk(f, j), err);
         CUDA_THROW(cudaGetLastError());
-        r.mark("ng_potrf_diag", l, static_cast<double>(b) * b * b / 3.0 * 2.0, s);
+        r.mark("ng_potrf_diag", l, static_cast<double>(b) * b * b / 3.0 * 2.0, fs);
         if (f.panel[blk].M > 0) {
-            gemm_launch(f.panel[blk], s);
-            r.mark("ng_potrf_panel", l, 2.0 * f.panel[blk].M * f.panel[blk].N * f.panel[blk].K, s);
-            gemm_launch(f.trail[blk], s);
-            r.mark("ng_potrf_trail", l, 1.0 * f.trail[blk].M * f.trail[blk].N * f.trail[blk].K, s);
+            gemm_launch(f.panel[blk], fs);
+            r.mark("ng_potrf_panel", l, 2.0 * f.panel[blk].M * f.panel[blk].N * f.panel[blk].K, fs);
         }
+        if (conc) CUDA_THROW(cudaEventRecord(f.ev_panel[blk], fs));
+        if (f.col[blk].M > 0) {
+            if (conc && blk >= 1 && f.rest[blk - 1].M > 0) CUDA_THROW(cudaStreamWaitEvent(fs, f.ev_trail[blk - 1], 0));
+            gemm_launch(f.col[blk], fs);
+            r.mark("ng_potrf_trail", l, 2.0 * f.col[blk].M * f.col[blk].N * f.col[blk].K, fs);
+        }
+        if (f.rest[blk].M > 0) {
+            if (conc) CUDA_THROW(cudaStreamWaitEvent(ts, f.ev_panel[blk], 0));
+            gemm_launch(f.rest[blk], ts);
+            r.mark("ng_potrf_trail", l, 1.0 * f.rest[blk].M * f.rest[blk].N * f.rest[blk].K, ts);
+            if (conc) CUDA_THROW(cudaEventRecord(f.ev_trail[blk], ts));
+        }
+    }
+    if (conc) {  // rejoin ts (graph capture requires every forked stream to join back)
+        cudaEvent_t last = f.ev_trail.back();  // the last block never has a rest update
+        CUDA_THROW(cudaEventRecord(last, ts));
+        CUDA_THROW(cudaStreamWaitEvent(fs, last, 0));
     }
 }
 
-void solve(NgSolve& sv, cudaStream_t s) {
-    const size_t nb = sv.fdiag.size();
-    for (size_t i = 0; i < nb; ++i) {
+// Forward solve block by block, each block as soon as its column of L is final.
+void solve_forward(NgFactor& f, NgSolve& sv, cudaStream_t s, bool conc) {
+    for (size_t i = 0; i < sv.fdiag.size(); ++i) {
+        if (conc) CUDA_THROW(cudaStreamWaitEvent(s, f.ev_panel[i], 0));
         gemm_launch(sv.fdiag[i], s);
         if (sv.fupd[i].M > 0) gemm_launch(sv.fupd[i], s);
     }
-    for (size_t i = nb; i-- > 0;) {
+}
+
+void solve_backward(NgSolve& sv, cudaStream_t s) {
+    for (size_t i = sv.bdiag.size(); i-- > 0;) {
         gemm_launch(sv.bdiag[i], s);
         if (sv.bupd[i].M > 0) gemm_launch(sv.bupd[i], s);
     }
@@ -541,6 +579,19 @@ void ng_alloc(Replica& r) {
         CUDA_THROW(cudaMalloc(&g.part, 512 * sizeof(double)));
         CUDA_THROW(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
         CUDA_THROW(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
+        CUDA_THROW(cudaEventCreateWithFlags(&g.ev_ready, cudaEventDisableTiming));
+        CUDA_THROW(cudaEventCreateWithFlags(&g.ev_in_done, cudaEventDisableTiming));
+        for (NgFactor* f : {&g.out, &g.in}) {
+            CUDA_THROW(cudaStreamCreateWithFlags(&f->fs, cudaStreamNonBlocking));
+            CUDA_THROW(cudaStreamCreateWithFlags(&f->ts, cudaStreamNonBlocking));
+            const long nb = (f->n + NB - 1) / NB;
+            f->ev_panel.resize(nb);
+            f->ev_trail.resize(nb);
+            for (long i = 0; i < nb; ++i) {
+                CUDA_THROW(cudaEventCreateWithFlags(&f->ev_panel[i], cudaEventDisableTiming));
+                CUDA_THROW(cudaEventCreateWithFlags(&f->ev_trail[i], cudaEventDisableTiming));
+            }
+        }
     }
     CUDA_THROW(cudaEventCreateWithFlags(&r.ng_fork, cudaEventDisableTiming));
 }
@@ -551,7 +602,14 @@ void ng_free(Replica& r) {
             if (p) cudaFree(p);
         if (g.part) cudaFree(g.part);
         if (g.stream) cudaStreamDestroy(g.stream);
-        if (g.done) cudaEventDestroy(g.done);
+        for (cudaEvent_t e : {g.done, g.ev_ready, g.ev_in_done})
+            if (e) cudaEventDestroy(e);
+        for (NgFactor* f : {&g.out, &g.in}) {
+            for (cudaEvent_t e : f->ev_panel) cudaEventDestroy(e);
+            for (cudaEvent_t e : f->ev_trail) cudaEventDestroy(e);
+            if (f->fs) cudaStreamDestroy(f->fs);
+            if (f->ts) cudaStreamDestroy(f->ts);
+        }
     }
     if (r.ng_fork) cudaEventDestroy(r.ng_fork);
     r.ng_fork = nullptr;
@@ -572,9 +630,12 @@ void ng_build_plans(Replica& r) {
 
 // ng_precondition (optimizer.cpp:123-157) for layer l: G is in r.grads (W part
 // [dout x ldw], bias at b_off); leaves Ghat^T in t2, bhat in t1[:, din] and
-// the four norms in r.scal.
+// the four norms in r.scal. Runs on stream s; unless a profile is being taken
+// the two factorizations fork onto their own streams and the forward S_out
+// solve trails the S_out factorization block by block.
 void ng_precondition_layer(Replica& r, int l, cudaStream_t s) {
     NgLayer& g = r.ngl[l];
+    const bool conc = r.prof == nullptr;
     const long din = r.dims[l], dout = r.dims[l + 1];
     double* sc = r.scal + 16 * l;  // [0..3] norms, [4] lambda_in, [5] lambda_out
     double* part = g.part;
@@ -587,22 +648,35 @@ void ng_precondition_layer(Replica& r, int l, cudaStream_t s) {
     shift_copy_kernel<<<grid_for(dout * g.out.ld), 256, 0, s>>>(r.r_out[l], dout, g.out.ld, sc + 5, g.out.a);
     shift_copy_kernel<<<grid_for(din * g.in.ld), 256, 0, s>>>(r.r_in[l], din, g.in.ld, sc + 4, g.in.a);
     r.mark("ng_smooth", l, 0, s);
-    cholesky(r, l, g.out, r.d_err, s);
-    cholesky(r, l, g.in, r.d_err, s);
-    (void)fi;
+    if (conc) {
+        CUDA_THROW(cudaEventRecord(g.ev_ready, s));
+        for (NgFactor* f : {&g.out, &g.in}) {
+            CUDA_THROW(cudaStreamWaitEvent(f->fs, g.ev_ready, 0));
+            CUDA_THROW(cudaStreamWaitEvent(f->ts, g.ev_ready, 0));
+        }
+        cholesky(r, l, g.out, r.d_err, g.out.fs, g.out.ts, true);
+        cholesky(r, l, g.in, r.d_err, g.in.fs, g.in.ts, true);
+        CUDA_THROW(cudaEventRecord(g.ev_in_done, g.in.fs));
+    } else {
+        cholesky(r, l, g.out, r.d_err, s, s, false);
+        cholesky(r, l, g.in, r.d_err, s, s, false);
+    }
 
     sumsq(gw, r.ldw[l], dout, din, part, sc + 0, s);
     sumsq(gb, 1, dout, 1, part, sc + 1, s);
     pack_rhs_kernel<<<grid_for(dout * g.ldt), 256, 0, s>>>(gw, r.ldw[l], gb, dout, din, g.t1, g.ldt);
     r.mark("ng_norms", l, 0, s);
-    solve(g.solve_out, s);  // S_out^-1 [G | g_b]
+    solve_forward(g.out, g.solve_out, s, conc);  // S_out^-1 [G | g_b], pipelined behind the factor
+    solve_backward(g.solve_out, s);
     r.mark("ng_trsm", l, 2.0 * fo * fo * (fi + 1.0), s);
     {
         dim3 grid((din + 31) / 32, (dout + 31) / 32), block(32, 8);
         transpose_kernel<<<grid, block, 0, s>>>(g.t1, g.ldt, dout, din, g.t2, g.ld2);
     }
     r.mark("ng_transpose", l, 0, s);
-    solve(g.solve_in, s);  // S_in^-1 (S_out^-1 G)^T
+    if (conc) CUDA_THROW(cudaStreamWaitEvent(s, g.ev_in_done, 0));
+    solve_forward(g.in, g.solve_in, s, false);  // S_in^-1 (S_out^-1 G)^T
+    solve_backward(g.solve_in, s);
     r.mark("ng_trsm", l, 2.0 * fi * fi * fo, s);
     sumsq(g.t2, g.ld2, din, dout, part, sc + 2, s);
     sumsq(g.t1 + din, g.ldt, dout, 1, part, sc + 3, s);

@@ -81,7 +81,9 @@ struct NgFactor {
     long n = 0, ld = 0;
     float* a = nullptr;     // [n x ld]: S, overwritten by L (lower triangle)
     float* linv = nullptr;  // [nblk x NB x NB]: inverses of the diagonal blocks of L
-    std::vector<GemmPlan> panel, trail;  // per block
+    std::vector<GemmPlan> panel, col, rest;  // per block: panel solve, look-ahead column, rest of trailing
+    cudaStream_t fs = nullptr, ts = nullptr;  // critical-path / bulk-trailing streams
+    std::vector<cudaEvent_t> ev_panel, ev_trail;
 };
 struct NgSolve {  // X <- S^-1 X for one fixed right-hand-side buffer
     std::vector<GemmPlan> fdiag, fupd, bdiag, bupd;  // per block
@@ -94,7 +96,7 @@ struct NgLayer {
     long ldt = 0, ld2 = 0;
     double* part = nullptr;         // norm-reduction scratch
     cudaStream_t stream = nullptr;  // the layer's NG chain runs concurrently with the others
-    cudaEvent_t done = nullptr;
+    cudaEvent_t done = nullptr, ev_ready = nullptr, ev_in_done = nullptr;
 };
 
 struct Profile {
