@@ -654,8 +654,11 @@ void ng_precondition_layer(Replica& r, int l, cudaStream_t s) {
             CUDA_THROW(cudaStreamWaitEvent(f->fs, g.ev_ready, 0));
             CUDA_THROW(cudaStreamWaitEvent(f->ts, g.ev_ready, 0));
         }
+        r.tmark("ready" + std::to_string(l), s);
         cholesky(r, l, g.out, r.d_err, g.out.fs, g.out.ts, true);
+        r.tmark("fact_out" + std::to_string(l), g.out.fs);
         cholesky(r, l, g.in, r.d_err, g.in.fs, g.in.ts, true);
+        r.tmark("fact_in" + std::to_string(l), g.in.fs);
         CUDA_THROW(cudaEventRecord(g.ev_in_done, g.in.fs));
     } else {
         cholesky(r, l, g.out, r.d_err, s, s, false);
@@ -667,7 +670,9 @@ void ng_precondition_layer(Replica& r, int l, cudaStream_t s) {
     pack_rhs_kernel<<<grid_for(dout * g.ldt), 256, 0, s>>>(gw, r.ldw[l], gb, dout, din, g.t1, g.ldt);
     r.mark("ng_norms", l, 0, s);
     solve_forward(g.out, g.solve_out, s, conc);  // S_out^-1 [G | g_b], pipelined behind the factor
+    if (conc) r.tmark("fsolve" + std::to_string(l), s);
     solve_backward(g.solve_out, s);
+    if (conc) r.tmark("bsolve" + std::to_string(l), s);
     r.mark("ng_trsm", l, 2.0 * fo * fo * (fi + 1.0), s);
     {
         dim3 grid((din + 31) / 32, (dout + 31) / 32), block(32, 8);
@@ -677,6 +682,7 @@ void ng_precondition_layer(Replica& r, int l, cudaStream_t s) {
     if (conc) CUDA_THROW(cudaStreamWaitEvent(s, g.ev_in_done, 0));
     solve_forward(g.in, g.solve_in, s, false);  // S_in^-1 (S_out^-1 G)^T
     solve_backward(g.solve_in, s);
+    if (conc) r.tmark("insolve" + std::to_string(l), s);
     r.mark("ng_trsm", l, 2.0 * fi * fi * fo, s);
     sumsq(g.t2, g.ld2, din, dout, part, sc + 2, s);
     sumsq(g.t1 + din, g.ldt, dout, 1, part, sc + 3, s);

@@ -334,6 +334,11 @@ void Replica::bind(DeviceDataset* ds) {
         graph = nullptr;
     }
     if (std::getenv("PARNN_NO_GRAPH")) use_graph = false;  // debugging: eager launches
+    tl.clear();
+    if (std::getenv("PARNN_TIMELINE") && tl_pool.empty()) {
+        tl_pool.resize(128);
+        for (auto& e : tl_pool) CUDA_THROW(cudaEventCreate(&e));
+    }
     if (use_graph) {
         cudaStream_t s = stream;
         cudaGraph_t g;
@@ -353,6 +358,31 @@ void Replica::bind(DeviceDataset* ds) {
     }
 }
 
+void Replica::tmark(const std::string& name, cudaStream_t s) {
+    if (tl.size() >= tl_pool.size()) return;
+    cudaEvent_t e = tl_pool[tl.size()];
+    // External: becomes an event-record node of the captured graph (a plain
+    // record inside a capture is only a fork/join marker)
+    cudaStreamCaptureStatus cs;
+    CUDA_THROW(cudaStreamIsCapturing(s, &cs));
+    if (cs == cudaStreamCaptureStatusActive)
+        CUDA_THROW(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+    else
+        CUDA_THROW(cudaEventRecord(e, s));
+    tl.emplace_back(name, e);
+}
+
+void Replica::dump_timeline() {
+    if (tl.empty()) return;
+    std::ostringstream os;
+    os << "[parnn timeline ms]";
+    for (auto& [name, e] : tl) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, tl[0].second, e) == cudaSuccess) os << " " << name << "=" << t;
+    }
+    fprintf(stderr, "%s\n", os.str().c_str());
+}
+
 void Replica::mark(const char* kind, int layer, double flops, cudaStream_t s) {
     if (!prof) return;
     cudaEvent_t e;
@@ -368,6 +398,7 @@ void Replica::enqueue_step(cudaStream_t s) {
     DeviceDataset* ds = bound;
     auto gf = [](const GemmPlan& p) { return 2.0 * p.M * p.N * p.K; };
     mark("start", -1, 0, s);
+    if (!prof) tmark("t0", s);
     launch_gather(ds->features(prec), ds->ld, ds->y, d_rows, d_step, B, dims[0], acts[0], ld_act[0], d_ybatch, F, s);
     mark("gather", 0, 0, s);
     for (int l = 0; l < L; ++l) {
@@ -385,6 +416,7 @@ void Replica::enqueue_step(cudaStream_t s) {
         // (SGD) / dz_l exists (NG); layer l's NG chain starts right after dW_l,
         // so the output layer's long Cholesky/TRSM chain overlaps the rest of
         // the backward pass.
+        tmark("fwd", s);
         if (ng) ng_coeff_kernel<<<1, 1, 0, s>>>(tdev, ng_decay, 1.0 / static_cast<double>(B), coef);
         for (int l = L - 1; l >= 0; --l) {
             launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
@@ -393,6 +425,7 @@ void Replica::enqueue_step(cudaStream_t s) {
             CUDA_THROW(cudaEventRecord(ev_bwd[l], s));
             CUDA_THROW(cudaStreamWaitEvent(side, ev_bwd[l], 0));
             gemm_launch(dw[l], side);
+            tmark("dw" + std::to_string(l), side);
             if (ng) {
                 CUDA_THROW(cudaEventRecord(ev_dw[l], side));
                 cudaStream_t ls = ngl[l].stream;
@@ -401,6 +434,7 @@ void Replica::enqueue_step(cudaStream_t s) {
                 gemm_launch(mom_out[l], ls);
                 ng_precondition_layer(*this, l, ls);
                 ng_apply_update(*this, l, ls);
+                tmark("done" + std::to_string(l), ls);
                 CUDA_THROW(cudaEventRecord(ngl[l].done, ls));
             }
         }
@@ -410,6 +444,7 @@ void Replica::enqueue_step(cudaStream_t s) {
             for (int l = 0; l < L; ++l) CUDA_THROW(cudaStreamWaitEvent(s, ngl[l].done, 0));
         flags_latch_kernel<<<1, 1, 0, s>>>(d_flags, d_step);
         launch_ce_reduce(ce_rows, B, d_ce, d_step, 1, s);
+        tmark("end", s);
         return;
     }
     for (int l = L - 1; l >= 0; --l) {
@@ -518,6 +553,10 @@ void Replica::run_step(cudaStream_t s) {
 }
 
 void Replica::check_errors() {
+    if (!tl.empty()) {
+        CUDA_THROW(cudaStreamSynchronize(stream));
+        dump_timeline();
+    }
     DevErr e;
     unsigned f[4];
     CUDA_THROW(cudaStreamSynchronize(stream));

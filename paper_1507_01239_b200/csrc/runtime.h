@@ -172,6 +172,13 @@ struct Replica {
     void sync_shadow(cudaStream_t s);  // recompute bf16 copy after external param writes
     void check_errors();               // throws the reference's messages
 
+    // optional timeline of the concurrent step (PARNN_TIMELINE=1): timing events
+    // captured into the graph, dumped to stderr by check_errors()
+    std::vector<std::pair<std::string, cudaEvent_t>> tl;
+    std::vector<cudaEvent_t> tl_pool;
+    void tmark(const std::string& name, cudaStream_t s);
+    void dump_timeline();
+
     // live per-region timing with CUDA events on the replica stream (bench)
     Profile* prof = nullptr;
     void mark(const char* kind, int layer, double flops, cudaStream_t s);

@@ -259,3 +259,22 @@ def test_config2_shape_step(ctx, prec, opt):
     ce = r.ce(2)
     assert np.all(np.isfinite(ce)) and abs(ce[0] - np.log(8806)) < 0.2
     assert r.kernels_per_step() > 20
+
+
+def test_reference_adapter_dropin():
+    # The reference's own C++ types + train_parallel (from its unmodified
+    # sources) next to the C-ABI adapter (integration/), same inputs.
+    import json
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration", "_build",
+                       "adapter_demo")
+    if not os.path.exists(exe):
+        pytest.skip("integration/_build/adapter_demo not built (needs the reference headers at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    res, err = [json.loads(l) for l in out.stdout.strip().splitlines()]
+    assert res["epochs"][0] == res["epochs"][1] and res["avg_events"][0] == res["avg_events"][1]
+    assert abs(res["ce_ref"] - res["ce_b200"]) <= 0.01 * res["ce_ref"]
+    assert res["theta_rel_l2"] < 2e-3
+    assert "train_parallel: avg_frequency must be >= 1" in err["error"]
