@@ -2,14 +2,16 @@
 """Benchmark of the model-averaging DNN trainer path (BASELINE.json).
 
 Workload (N=1): config 2 of BASELINE.json — Switchboard-shaped DNN
-440-2048x6-8806 sigmoid, NG-SGD (the reference's full Kronecker-factored
-preconditioner), minibatch 1024, synthetic frames from the reference's own
-generate_synthetic recipe. N>1 (torchrun): config 3 — one replica per GPU,
+440-2048x6-8806 sigmoid, NG-SGD, minibatch 1024, synthetic frames from the
+reference's own generate_synthetic recipe. NG-SGD is the north star's online
+low-rank preconditioner by default (--optimizer ngsgd_lowrank); the
+reference's kron-full NG-SGD is timed on the same data in the same run
+("ngsgd_kron_full") and is selectable with --optimizer ngsgd. N>1 (torchrun): config 3 — one replica per GPU,
 model averaging every 4 minibatches over NCCL (weak scaling: each GPU does
 the same per-step work).
 
 One "step" = one minibatch update on every replica (gather -> forward ->
-softmax-CE -> backward -> NG moments -> NG precondition -> SGD), plus the
+softmax-CE -> backward -> NG precondition (+ subspace update) -> SGD), plus the
 averaging event every --avg-frequency steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -30,6 +32,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 DIMS = [440] + [2048] * 6 + [8806]
+OPT_DESC = {"ngsgd_lowrank": "NG-SGD (online low-rank Fisher, rank 20/80, update every 4)",
+            "ngsgd": "NG-SGD (the reference's kron-full Fisher)", "sgd": "plain SGD"}
 METRIC = "training frames/sec (440-2048x6-8806 NG-SGD, minibatch 1024)"
 UNIT = "frames/s"
 
@@ -140,7 +144,7 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     prec = P.Precision.bf16 if args.precision == "bf16" else P.Precision.tf32
-    opt = P.OptimizerKind.ngsgd if args.optimizer == "ngsgd" else P.OptimizerKind.sgd
+    opt = P.OptimizerKind[args.optimizer]
     B, K, W = args.minibatch, args.steps, args.warmup
     ctx = P.Context(local_rank)
     comm = None
@@ -260,12 +264,27 @@ def run_ours(args, rank, world, local_rank):
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
 
+    # ---- the reference's own NG variant (kron-full) on the same data, same clock
+    kron = None
+    if world == 1 and not args.no_kron and args.optimizer != "ngsgd":
+        rk = P.Replica(ctx, DIMS, precision=prec, optimizer=P.OptimizerKind.ngsgd, minibatch=B, max_steps=8)
+        rk.set_params(m0.params)
+        rk.bind(ds)
+        rk.upload_epoch(rows[:8 * B], lrs[:8])
+        rk.step(2)
+        rk.sync()
+        kms = rk.time_steps(4) / 4
+        kron = {"optimizer": "ngsgd (kron-full, the reference's NG-SGD)", "value": B / (kms / 1e3), "unit": UNIT,
+                "ms_per_step": kms, "kernels_per_step": rk.kernels_per_step(), "steps": 4,
+                "timing": "CUDA events on the replica stream, graph launches"}
+        rk.close()
+
     kps = rep.kernels_per_step()
     out.update({
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": args.precision, "data": f"synthetic (generate_synthetic 8806x{args.per_class}, 440-dim, s=8)",
-        "config": {"workload": f"config 2: 440-2048x6-8806 sigmoid {args.optimizer} (kron-full NG), "
+        "config": {"workload": f"config 2: 440-2048x6-8806 sigmoid {OPT_DESC[args.optimizer]}, "
                                f"minibatch {B}, {'1 replica' if world == 1 else f'{world} replicas, averaging every {args.avg_frequency}'}",
                    "global_batch": B * world, "parallelism": f"dp{world} model-averaging",
                    "precision": f"{args.precision} operands, fp32 accumulate, fp32 NG solves",
@@ -280,6 +299,7 @@ def run_ours(args, rank, world, local_rank):
         "model_flops_per_frame": flops_per_frame(DIMS),
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "ngsgd_kron_full": kron,
         "final_ce": float(ce[-1]),
         "regions_ms": {k: round(v[0], 4) for k, v in sorted(by_kind.items(), key=lambda kv: -kv[1][0])},
     })
@@ -319,7 +339,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--precision", choices=["bf16", "tf32"], default="bf16")
-    ap.add_argument("--optimizer", choices=["ngsgd", "sgd"], default="ngsgd")
+    ap.add_argument("--optimizer", choices=["ngsgd_lowrank", "ngsgd", "sgd"], default="ngsgd_lowrank",
+                    help="ngsgd_lowrank: the north star's online low-rank NG-SGD (default); ngsgd: the "
+                         "reference's kron-full NG-SGD; sgd: plain SGD")
+    ap.add_argument("--no-kron", action="store_true", help="skip the kron-full NG-SGD side measurement")
     ap.add_argument("--minibatch", type=int, default=1024)
     ap.add_argument("--avg-frequency", type=int, default=4)
     ap.add_argument("--per-class", type=int, default=24)

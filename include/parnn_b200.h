@@ -28,7 +28,10 @@ extern "C" {
 /* GEMM operand precision (fp32 accumulation always): BF16, TF32, or FP32 =
  * fp32-accurate 3xTF32 split on the tensor cores (the parity mode). */
 enum parnn_precision { PARNN_BF16 = 0, PARNN_TF32 = 1, PARNN_FP32 = 2 };
-enum parnn_optimizer { PARNN_SGD = 0, PARNN_NGSGD = 1 };    /* parallel.hpp:14-18 */
+/* parallel.hpp:14-18. PARNN_NGSGD is the reference's kron-full NG-SGD
+ * (optimizer.cpp:44-157); PARNN_NGSGD_LOWRANK is the north star's online
+ * low-rank NG-SGD (not in the reference, oracle/ng_lowrank.py). */
+enum parnn_optimizer { PARNN_SGD = 0, PARNN_NGSGD = 1, PARNN_NGSGD_LOWRANK = 2 };
 enum parnn_lr_variant { PARNN_NEWBOB = 0, PARNN_EXPONENTIAL = 1 }; /* optimizer.hpp:57 */
 enum parnn_activation { PARNN_SIGMOID = 0, PARNN_TANH = 1 };   /* network.hpp:16 */
 
@@ -73,6 +76,10 @@ int parnn_scale_lr_for_workers(double lr_init, uint64_t workers, double* lr);
 int parnn_save_model(const char* path, const uint64_t* dims, int ndims, int activation, const double* params);
 int parnn_load_model(const char* path, uint64_t* dims, int* ndims, int* activation, double* params,
                      uint64_t capacity);
+/* Low-rank NG initial basis: rank x dim, orthonormal rows (Rng(seed) gaussians,
+ * modified Gram-Schmidt). Seeds per (layer, side): parnn_lowrank_seed. */
+int parnn_lowrank_basis(uint64_t dim, uint64_t rank, uint64_t seed, double* out);
+uint64_t parnn_lowrank_seed(int layer, int side);
 /* allreduce_average on host vectors (parallel.cpp:40-59), fixed midpoint tree */
 int parnn_allreduce_average_host(const double* contributions, uint64_t m, uint64_t len, double* out);
 
@@ -97,6 +104,19 @@ int parnn_replica_get_params(parnn_replica* r, double* params, uint64_t n);
 /* NgState factors: per layer r_in (din^2) then r_out (dout^2) (optimizer.hpp:22-34) */
 int parnn_replica_get_ng_state(parnn_replica* r, double* factors, uint64_t n);
 int parnn_replica_set_ng_state(parnn_replica* r, const double* factors, uint64_t n, uint64_t update_count);
+/* Low-rank NG-SGD knobs (optimizer PARNN_NGSGD_LOWRANK; alpha = ng_smoothing):
+ * ranks of the input / output-derivative Fisher factors (<= 96), subspace
+ * update period P, initial updates on the first minibatch, and the history
+ * length S (eta = 1 - exp(-B P / S)). Resets the NG state. */
+int parnn_replica_set_lowrank(parnn_replica* r, int rank_in, int rank_out, int update_period, int init_iters,
+                              double num_samples_history);
+/* Low-rank NG state of (layer, side 0 = in [A_prev | 1], 1 = out dz):
+ * W = E^1/2 R (rank x dim, row-major), d (rank), rho. */
+int parnn_replica_lowrank_state(parnn_replica* r, int layer, int side, double* w, double* d, double* rho,
+                                uint64_t* rank, uint64_t* dim);
+/* Diagnostics of (layer, side): {tr(X X^T), gamma, Jacobi sweeps, Jacobi SM
+ * cycles} of the last preconditioning / subspace update. */
+int parnn_replica_lowrank_diag(parnn_replica* r, int layer, int side, double out[4]);
 /* Build the step's GEMM plans + CUDA graph against a training dataset. */
 int parnn_replica_bind(parnn_replica* r, parnn_dataset* train);
 /* Upload one epoch: steps*minibatch dataset row ids (Dataset::select order) and per-step lr. */
@@ -157,6 +177,11 @@ typedef struct {
     uint64_t rank0;          /* first global rank hosted by this process */
     uint64_t local_workers;  /* ranks hosted here (0 = all m) */
     int serial;              /* serial_train semantics (parallel.cpp:285-294) */
+    /* low-rank NG-SGD knobs (PARNN_NGSGD_LOWRANK); 0 = default (20, 80, 4, 2000) */
+    int ng_rank_in;
+    int ng_rank_out;
+    int ng_update_period;
+    double ng_history;
 } parnn_train_config;
 
 /* train_parallel / serial_train (parallel.cpp:163-294). metrics_out holds up

@@ -29,7 +29,8 @@ class TrainConfig(C.Structure):
     _fields_ = [("workers", c_u64), ("avg_frequency", c_u64), ("minibatch", c_u64), ("base_seed", c_u64),
                 ("optimizer", c_int), ("lr_schedule", c_int), ("lr_init", c_f64), ("epochs", c_u64),
                 ("ng_decay", c_f64), ("ng_smoothing", c_f64), ("precision", c_int), ("activation", c_int),
-                ("rank0", c_u64), ("local_workers", c_u64), ("serial", c_int)]
+                ("rank0", c_u64), ("local_workers", c_u64), ("serial", c_int),
+                ("ng_rank_in", c_int), ("ng_rank_out", c_int), ("ng_update_period", c_int), ("ng_history", c_f64)]
 
 
 # (name, restype, argtypes) for every symbol declared in include/parnn_b200.h
@@ -50,6 +51,8 @@ SIGNATURES = [
     ("parnn_scale_lr_for_workers", c_int, [c_f64, c_u64, vp]),
     ("parnn_save_model", c_int, [C.c_char_p, vp, c_int, c_int, vp]),
     ("parnn_load_model", c_int, [C.c_char_p, vp, vp, vp, vp, c_u64]),
+    ("parnn_lowrank_basis", c_int, [c_u64, c_u64, c_u64, vp]),
+    ("parnn_lowrank_seed", c_u64, [c_int, c_int]),
     ("parnn_allreduce_average_host", c_int, [vp, c_u64, c_u64, vp]),
     ("parnn_ctx_create", c_int, [c_int, vp]),
     ("parnn_ctx_destroy", c_int, [vp]),
@@ -62,6 +65,9 @@ SIGNATURES = [
     ("parnn_replica_get_params", c_int, [vp, vp, c_u64]),
     ("parnn_replica_get_ng_state", c_int, [vp, vp, c_u64]),
     ("parnn_replica_set_ng_state", c_int, [vp, vp, c_u64, c_u64]),
+    ("parnn_replica_set_lowrank", c_int, [vp, c_int, c_int, c_int, c_int, c_f64]),
+    ("parnn_replica_lowrank_state", c_int, [vp, c_int, c_int, vp, vp, vp, vp, vp]),
+    ("parnn_replica_lowrank_diag", c_int, [vp, c_int, c_int, vp]),
     ("parnn_replica_bind", c_int, [vp, vp]),
     ("parnn_replica_upload_epoch", c_int, [vp, vp, vp, c_u64]),
     ("parnn_replica_step", c_int, [vp, c_u64]),

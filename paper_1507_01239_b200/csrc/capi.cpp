@@ -233,13 +233,63 @@ int parnn_replica_create(parnn_ctx* ctx, const uint64_t* dims, int nd, int act, 
         if (decay <= 0.0 || decay >= 1.0)
             throw std::runtime_error("ng_init: decay must be in (0,1), got " + std::to_string(decay));
         if (smoothing <= 0.0) throw std::runtime_error("ng_init: smoothing must be positive, got " + std::to_string(smoothing));
+        if (opt < 0 || opt > 2) throw std::runtime_error("replica: unknown optimizer " + std::to_string(opt));
         auto* p = new parnn_replica;
         p->r.reset(new Replica(ctx->c.get(), to_dims(dims, nd), act, static_cast<Precision>(prec),
-                               opt ? OPT_NG_KRON : OPT_SGD, static_cast<long>(minibatch), static_cast<long>(max_steps),
+                               static_cast<Optimizer>(opt), static_cast<long>(minibatch), static_cast<long>(max_steps),
                                decay, smoothing));
         *out = p;
     });
 }
+
+int parnn_replica_set_lowrank(parnn_replica* r, int rank_in, int rank_out, int update_period, int init_iters,
+                              double history) {
+    return guarded([&] {
+        need(r, "replica");
+        LrConfig c = r->r->lrc;
+        c.rank_in = rank_in;
+        c.rank_out = rank_out;
+        c.update_period = update_period;
+        c.init_iters = init_iters;
+        c.history = history;
+        r->r->set_lowrank(c);
+    });
+}
+
+int parnn_replica_lowrank_state(parnn_replica* r, int layer, int side, double* w, double* d, double* rho,
+                                uint64_t* rank, uint64_t* dim) {
+    return guarded([&] {
+        need(r, "replica");
+        Replica& rp = *r->r;
+        if (rp.opt != OPT_NG_LOWRANK) throw std::runtime_error("replica: not a low-rank NG-SGD replica");
+        if (layer < 0 || layer >= rp.L || side < 0 || side > 1) throw std::runtime_error("ng lowrank: bad layer/side");
+        const LrSide& sd = side == 0 ? rp.lrl[layer].in : rp.lrl[layer].out;
+        if (rank) *rank = static_cast<uint64_t>(sd.R);
+        if (dim) *dim = static_cast<uint64_t>(sd.D);
+        rp.get_lowrank_state(layer, side, w, d, rho);
+    });
+}
+
+int parnn_replica_lowrank_diag(parnn_replica* r, int layer, int side, double out[4]) {
+    return guarded([&] {
+        need(r, "replica");
+        Replica& rp = *r->r;
+        if (rp.opt != OPT_NG_LOWRANK) throw std::runtime_error("replica: not a low-rank NG-SGD replica");
+        if (layer < 0 || layer >= rp.L || side < 0 || side > 1) throw std::runtime_error("ng lowrank: bad layer/side");
+        const LrSide& sd = side == 0 ? rp.lrl[layer].in : rp.lrl[layer].out;
+        CUDA_THROW(cudaDeviceSynchronize());
+        CUDA_THROW(cudaMemcpy(out, sd.st + 2 * sd.R + 1, 4 * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+int parnn_lowrank_basis(uint64_t dim, uint64_t rank, uint64_t seed, double* out) {
+    return guarded([&] {
+        const std::vector<double> b = host::lowrank_basis(dim, rank, seed);
+        std::copy(b.begin(), b.end(), out);
+    });
+}
+
+uint64_t parnn_lowrank_seed(int layer, int side) { return host::lowrank_seed(layer, side); }
 
 int parnn_replica_destroy(parnn_replica* r) {
     return guarded([&] { delete r; });
@@ -324,7 +374,7 @@ int parnn_replica_accuracy(parnn_replica* r, parnn_dataset* ds, double* acc) {
 int parnn_replica_kernels_per_step(parnn_replica* r, uint64_t* n) {
     return guarded([&] {
         Replica& R = *r->r;
-        if (!R.graph) throw std::runtime_error("replica: no step graph");
+        if (!R.graph && R.kernels_per_step == 0) throw std::runtime_error("replica: no step graph");
         *n = static_cast<uint64_t>(R.kernels_per_step);
     });
 }
@@ -434,6 +484,12 @@ int parnn_train(parnn_ctx* ctx, parnn_comm* comm, const parnn_train_config* c, c
         t.rank0 = c->rank0;
         t.local = c->local_workers;
         t.serial = c->serial;
+        if (c->optimizer < 0 || c->optimizer > 2)
+            throw std::runtime_error("train_parallel: unknown optimizer " + std::to_string(c->optimizer));
+        if (c->ng_rank_in) t.lr.rank_in = c->ng_rank_in;
+        if (c->ng_rank_out) t.lr.rank_out = c->ng_rank_out;
+        if (c->ng_update_period) t.lr.update_period = c->ng_update_period;
+        if (c->ng_history > 0.0) t.lr.history = c->ng_history;
         std::vector<EpochRec> met;
         pnb::train(ctx->c.get(), comm ? comm->c.get() : nullptr, t, to_dims(dims, nd), params0, train_set->d.get(),
               cv ? cv->d.get() : nullptr, params_out, met);

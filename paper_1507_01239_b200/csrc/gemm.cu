@@ -111,7 +111,12 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     p.N = N;
     p.K = K;
     p.ep = ep;
-    const long tiles = static_cast<long>((N + bn - 1) / bn) * ((M + 127) / 128);
+    // split-K: round the factor so that every split owns >= 1 k-block
+    const int nk = static_cast<int>((K + bk - 1) / bk);
+    const int per = (nk + std::max(ep.ksplit, 1) - 1) / std::max(ep.ksplit, 1);
+    p.ep.ksplit = (nk + per - 1) / per;
+    if (p.ep.ksplit > 1 && ep.mode != EPI_PARTIAL) throw std::runtime_error("gemm: split-K needs EPI_PARTIAL");
+    const long tiles = static_cast<long>((N + bn - 1) / bn) * ((M + 127) / 128) * p.ep.ksplit;
     p.grid = dim3(static_cast<unsigned>(std::min<long>(tiles, num_sms)), 1, 1);  // persistent
     if (split)
         p.fn = reinterpret_cast<void*>(pick<float, true>(bn, a_mn, b_mn, &p.smem));

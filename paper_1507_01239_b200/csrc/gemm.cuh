@@ -35,6 +35,8 @@ enum EpiMode : int {
     EPI_EMA = 5,         // out32    = beta * out32 + alpha * acc
     EPI_AXPY = 6,        // out32   += alpha * acc; shadow = bf16(out32)   (CD-1 update)
     EPI_SUB = 7,         // out32   -= acc      (blocked Cholesky / TRSM updates)
+    EPI_PARTIAL = 8,     // out32[ks * split_stride + ...] = acc   (split-K partial products)
+    EPI_RESID = 9,       // out(T)   = aux(T) - acc; per-CTA sums of aux^2, out^2 -> part
 };
 
 struct GemmEpi {
@@ -58,6 +60,9 @@ struct GemmEpi {
     unsigned* flag = nullptr;  // bit `flag_bit` set on a non-finite gradient
     unsigned flag_bit = 0;
     int lower = 0;  // skip tiles strictly above the diagonal (SYRK-style updates)
+    int ksplit = 1;         // split-K factor (set by gemm_plan; every split non-empty)
+    long split_stride = 0;  // PARTIAL: floats between the per-split outputs
+    double* part = nullptr; // RESID: [gridDim.x][2] per-CTA {sum aux^2, sum out^2}
 };
 
 template <typename T>
@@ -179,9 +184,26 @@ struct GemmSmem {
 // Epilogue of one 32-column chunk of one accumulator row.
 template <typename T>
 __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, float (&v)[32], int row, int n, int valid,
-                                               float lr) {
+                                               float lr, int ks, float& s_aux, float& s_out) {
     bool bad = false;
     switch (ep.mode) {
+        case EPI_PARTIAL: {
+            store_row32<float>(ep.out32 + ks * ep.split_stride + row * ep.ld_out32 + n, v, valid);
+            break;
+        }
+        case EPI_RESID: {
+            float a[32];
+            load_row32<T>(static_cast<const T*>(ep.aux) + row * ep.ld_aux + n, a, valid);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                v[j] = a[j] - v[j];
+                if constexpr (sizeof(T) == 2) v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));  // as stored
+                s_aux = fmaf(a[j], a[j], s_aux);
+                s_out = fmaf(v[j], v[j], s_out);  // padding columns: a = acc = 0
+            }
+            store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
+            break;
+        }
         case EPI_FWD_ACT: {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
@@ -208,9 +230,10 @@ __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, float (&v)[32]
             float w[32];
             float* wp = ep.out32 + row * ep.ld_out32 + n;
             load_row32<float>(wp, w, valid);
+            const float alpha = ep.coef ? ep.alpha * ep.coef[0] : ep.alpha;  // NG low-rank scale
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const float g = v[j] * ep.alpha;
+                const float g = v[j] * alpha;
                 bad |= (j < valid) && !isfinite(g);
                 w[j] -= lr * g;
             }
@@ -296,9 +319,18 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int tiles_m = (M + 127) / 128;
-    const int tiles = tiles_m * ((N + BN - 1) / BN);
-    const int nk = (K + S::kBK - 1) / S::kBK;
+    const int tiles_mn = tiles_m * ((N + BN - 1) / BN);
+    const int tiles = tiles_mn * ep.ksplit;  // split-K: tile = mn + tiles_mn * ks
+    const int nk_all = (K + S::kBK - 1) / S::kBK;
+    const int nk_per = (nk_all + ep.ksplit - 1) / ep.ksplit;
     auto tile_skipped = [&](int m0, int n0) { return ep.lower && n0 > m0 + 127; };
+    // k-block range [kb0, kb1) of split ks (gemm_plan guarantees it is non-empty)
+    auto krange = [&](int tile, int& kb0, int& kb1) {
+        const int ks = tile / tiles_mn;
+        kb0 = ks * nk_per;
+        kb1 = min(nk_all, kb0 + nk_per);
+        return ks;
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -325,9 +357,11 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
         if (lane == 0) {
             int it = 0;  // global k-block counter (ring position)
             for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-                const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
+                const int m0 = (tile % tiles_m) * 128, n0 = ((tile % tiles_mn) / tiles_m) * BN;
                 if (tile_skipped(m0, n0)) continue;
-                for (int kb = 0; kb < nk; ++kb, ++it) {
+                int kb0, kb1;
+                krange(tile, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
                     if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
                     uint8_t* sa = smem + s * S::kStage;
@@ -367,13 +401,15 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
             };
             int it = 0, local = 0;
             for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-                const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
+                const int m0 = (tile % tiles_m) * 128, n0 = ((tile % tiles_mn) / tiles_m) * BN;
                 if (tile_skipped(m0, n0)) continue;
                 const int acc = local & 1;
                 if (local >= 2) mbar_wait(&tempty[acc], ((local >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t d = tmem + acc * BN;
-                for (int kb = 0; kb < nk; ++kb, ++it) {
+                int kb0, kb1;
+                krange(tile, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(SPLIT ? &split_done[s] : &full[s], (it / STAGES) & 1);
                     tc_fence_after();
@@ -381,7 +417,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
                     const uint32_t sb = sa + S::kABytes;
 #pragma unroll
                     for (int k = 0; k < S::kBK / S::kUK; ++k) {
-                        umma<kTf32>(d, desc_a(sa, k), desc_b(sb, k), idesc, (kb | k) != 0 ? 1u : 0u);
+                        umma<kTf32>(d, desc_a(sa, k), desc_b(sb, k), idesc, (kb != kb0 || k != 0) ? 1u : 0u);
                         if constexpr (SPLIT) {
                             const uint32_t sal = sa + S::kLoad, sbl = sb + S::kLoad;
                             umma<kTf32>(d, desc_a(sa, k), desc_b(sbl, k), idesc, 1u);
@@ -400,10 +436,12 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
         float lr = 0.f;
         if (ep.mode == EPI_GRAD_SGD) lr = ep.lr[ep.step ? *ep.step : 0];
         bool bad = false;
+        float s_aux = 0.f, s_out = 0.f;  // RESID sums (per thread, this CTA's tiles)
         int local = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-            const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
+            const int m0 = (tile % tiles_m) * 128, n0 = ((tile % tiles_mn) / tiles_m) * BN;
             if (tile_skipped(m0, n0)) continue;
+            const int ks = tile / tiles_mn;
             const int acc = local & 1;
             const int row = m0 + quad * 32 + lane;
             const bool row_ok = row < M;
@@ -416,7 +454,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
                 if (ep.mode == EPI_GRAD_SGD || ep.mode == EPI_EMA || ep.mode == EPI_SUB || ep.mode == EPI_AXPY) {
                     src = reinterpret_cast<const char*>(ep.out32 + row * ep.ld_out32 + n0);
                     bytes = static_cast<long>(min(BN, N - n0)) * 4;
-                } else if (ep.mode == EPI_ACTGRAD) {
+                } else if (ep.mode == EPI_ACTGRAD || ep.mode == EPI_RESID) {
                     src = static_cast<const char*>(ep.aux) + (row * ep.ld_aux + n0) * static_cast<long>(sizeof(T));
                     bytes = static_cast<long>(min(BN, N - n0)) * static_cast<long>(sizeof(T));
                 }
@@ -435,21 +473,41 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
                 float v[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                bad |= epilogue_chunk<T>(ep, v, row, n, min(32, N - n), lr);
+                bad |= epilogue_chunk<T>(ep, v, row, n, min(32, N - n), lr, ks, s_aux, s_out);
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
             ++local;
         }
         if (bad && ep.flag) atomicOr(ep.flag, 1u << ep.flag_bit);
+        if (ep.mode == EPI_RESID) {
+            // deterministic per-CTA sums: fixed tile order, fixed reduction tree
+            __shared__ float red[2][4];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                s_aux += __shfl_xor_sync(0xffffffffu, s_aux, o);
+                s_out += __shfl_xor_sync(0xffffffffu, s_out, o);
+            }
+            if (lane == 0) {
+                red[0][quad] = s_aux;
+                red[1][quad] = s_out;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+            if (warp == 2 && lane == 0) {
+                ep.part[2 * blockIdx.x] = (double)red[0][0] + red[0][1] + red[0][2] + red[0][3];
+                ep.part[2 * blockIdx.x + 1] = (double)red[1][0] + red[1][1] + red[1][2] + red[1][3];
+            }
+        }
     } else if (SPLIT) {
         // ---------------- 3xTF32 splitters (warps 6-9) ----------------
         const int t = threadIdx.x - 192;
         int it = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-            const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
+            const int m0 = (tile % tiles_m) * 128, n0 = ((tile % tiles_mn) / tiles_m) * BN;
             if (tile_skipped(m0, n0)) continue;
-            for (int kb = 0; kb < nk; ++kb, ++it) {
+            int kb0, kb1;
+            krange(tile, kb0, kb1);
+            for (int kb = kb0; kb < kb1; ++kb, ++it) {
                 const int s = it % STAGES;
                 mbar_wait(&full[s], (it / STAGES) & 1);
                 float4* hi = reinterpret_cast<float4*>(smem + s * S::kStage);

@@ -356,5 +356,29 @@ std::vector<double> allreduce_average(const std::vector<const double*>& contrib,
     return out;
 }
 
+std::vector<double> lowrank_basis(uint64_t dim, uint64_t rank, uint64_t seed) {
+    if (rank == 0 || rank >= dim) fail("lowrank_basis: need 0 < rank < dim, got rank " + std::to_string(rank) +
+                                       ", dim " + std::to_string(dim));
+    Rng rng(seed);
+    std::vector<double> m(rank * dim);
+    for (uint64_t i = 0; i < rank * dim; ++i) m[i] = rng.gaussian(0.0, 1.0);
+    for (uint64_t i = 0; i < rank; ++i) {
+        double* v = &m[i * dim];
+        for (uint64_t k = 0; k < i; ++k) {
+            const double* u = &m[k * dim];
+            double dot = 0.0;
+            for (uint64_t j = 0; j < dim; ++j) dot += u[j] * v[j];
+            for (uint64_t j = 0; j < dim; ++j) v[j] -= dot * u[j];
+        }
+        double nn = 0.0;
+        for (uint64_t j = 0; j < dim; ++j) nn += v[j] * v[j];
+        const double inv = 1.0 / std::sqrt(nn);
+        for (uint64_t j = 0; j < dim; ++j) v[j] *= inv;
+    }
+    return m;
+}
+
+uint64_t lowrank_seed(int layer, int side) { return 0x4C524E470000ULL + 2ULL * layer + side; }
+
 }  // namespace host
 }  // namespace pnb

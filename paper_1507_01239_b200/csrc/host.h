@@ -83,6 +83,11 @@ double scale_lr_for_workers(double lr_init, uint64_t workers);
 void save_model(const std::string& path, const std::vector<uint64_t>& dims, int act, const std::vector<double>& p);
 void load_model(const std::string& path, std::vector<uint64_t>& dims, int& act, std::vector<double>& p);
 
+// NG low-rank initial basis: rank x dim, orthonormal rows. Rng(seed).gaussian
+// drawn row-major, then modified Gram-Schmidt in fp64 (oracle/ng_lowrank.py).
+std::vector<double> lowrank_basis(uint64_t dim, uint64_t rank, uint64_t seed);
+uint64_t lowrank_seed(int layer, int side);
+
 // fixed midpoint-tree mean (parallel.cpp:26-59) on host vectors
 std::vector<double> allreduce_average(const std::vector<const double*>& contrib, uint64_t len);
 

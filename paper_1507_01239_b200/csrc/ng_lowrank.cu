@@ -1,0 +1,721 @@
+// NG-SGD, low-rank online variant (the north star's
+// "per-layer low-rank Fisher projection and rank-R subspace update").
+// Not in the reference; restates Povey, Zhang & Khudanpur 2014 (arXiv
+// 1410.7455, §3 + appendix C). CPU restatement: oracle/ng_lowrank.py.
+//
+// Per layer and side (in: X = [A_prev | 1], out: X = dz), with the Fisher
+// estimate held as W = E^1/2 R (R x D, R <= 96) plus d, e, rho:
+//   precondition  H = X W^T        split-K tcgen05 GEMM  -> lr_hreduce_kernel
+//                 Xhat = X - H W   tcgen05 GEMM, EPI_RESID (sums of X^2, Xhat^2)
+//                 gamma = sqrt(tr X X^T / tr Xhat Xhat^T)   lr_stats_kernel
+//   gradient      dW = g_in g_out / B  Dhat^T Ahat   (dW GEMM, EPI_GRAD_SGD * coef)
+//                 db = g_in g_out / B  Dhat^T ahat_1 (lr_bias_kernel)
+//   update (every P steps, split across two graph launches)
+//     step t      J = H^T X        tcgen05 GEMM (+ lr_jcol_kernel for the ones column)
+//     step t+1    Gram [J; W][J; W]^T   split-K 3xTF32 GEMM -> lr_gram_reduce_kernel
+//                 Z = Y Y^T from K, L, G; Jacobi eigensolver (fp64, one CTA)
+//                 W' = M [J; W]    lr_wupdate_kernel
+// The update of step t is applied at the start of step t+1 (before that
+// step's preconditioning of the side), so the eigensolver overlaps the
+// forward pass; the math equals the oracle's immediate update.
+#include <cmath>
+#include <cstdlib>
+
+#include "host.h"
+#include "runtime.h"
+
+namespace pnb {
+
+namespace {
+
+constexpr double kEps = 1e-10;   // rho floor relative to tr(T)/D; initial d, rho
+constexpr double kDelta = 5e-4;  // c, d floor relative to c_max
+constexpr double kTiny = 1e-30;
+
+float* falloc(size_t n) {
+    void* p = nullptr;
+    CUDA_THROW(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(float)));
+    CUDA_THROW(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(float)));
+    return static_cast<float*>(p);
+}
+double* dalloc_d(size_t n) {
+    void* p = nullptr;
+    CUDA_THROW(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(double)));
+    CUDA_THROW(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(double)));
+    return static_cast<double*>(p);
+}
+void* valloc(size_t bytes) {
+    void* p = nullptr;
+    CUDA_THROW(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    CUDA_THROW(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+    return p;
+}
+
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) {
+    return v;
+}
+template <>
+__device__ __forceinline__ bf16 from_f<bf16>(float v) {
+    return __float2bfloat16_rn(v);
+}
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) {
+    return v;
+}
+template <>
+__device__ __forceinline__ float to_f<bf16>(bf16 v) {
+    return __bfloat162float(v);
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// H[b, r] = sum_s hpart[s, b, r] (+ w_1[r], the ones column's weight, in side),
+// the operand-typed copy of H, the preconditioned ones column
+// ohat[b] = 1 - sum_r H[b, r] w_1[r], and per-CTA column sums of H and of
+// ohat^2 (fixed order: deterministic). One warp per row.
+// bf16 operands (NS = 2): W is carried as W_hi + W_lo (two bf16 rows each),
+// so H = X W_hi^T + X W_lo^T (columns [0,R) + [R,2R) of the partials) is
+// accurate to ~2^-17 and H is stored twice ([H | H], the A operand of
+// Xhat = X - [H | H] [W_hi; W_lo]). A single bf16 W corrupts the small
+// directions of mean-dominated inputs (sigmoid activations) by ~10% and
+// the subspace update diverges.
+template <typename T, int NS>
+__global__ void __launch_bounds__(256) lr_hreduce_kernel(const float* __restrict__ hpart, int S, long B, int R,
+                                                         const float* __restrict__ wm, long ldY, long xcol, int in,
+                                                         T* __restrict__ H, long ldH, float* __restrict__ ohat,
+                                                         double* __restrict__ rpart) {
+    __shared__ float cs[8][LR_MAX_RANK + 1];
+    __shared__ float o2[8];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long b = blockIdx.x * 8L + w;
+    float ow = 0.f;
+    for (int r = lane; r < R; r += 32) {
+        float h = 0.f;
+        if (b < B) {
+            for (int s = 0; s < S; ++s) {
+                const float* p = hpart + (s * B + b) * (NS * R);
+                h += NS == 2 ? p[r] + p[R + r] : p[r];
+            }
+            if (in) {
+                const float w1 = wm[r * ldY + xcol];
+                h += w1;
+                ow = fmaf(h, w1, ow);
+            }
+            H[b * ldH + r] = from_f<T>(h);
+            if (NS == 2) H[b * ldH + R + r] = from_f<T>(h);
+        }
+        cs[w][r] = h;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ow += __shfl_xor_sync(0xffffffffu, ow, o);
+    if (lane == 0) {
+        const float o = 1.f - ow;
+        const bool ok = in && b < B;
+        if (ok) ohat[b] = o;
+        o2[w] = ok ? o * o : 0.f;
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < R) {
+        double s = 0.0;
+        for (int i = 0; i < 8; ++i) s += cs[i][t];
+        rpart[blockIdx.x * (R + 1L) + t] = s;
+    } else if (t == R) {
+        double s = 0.0;
+        for (int i = 0; i < 8; ++i) s += o2[i];
+        rpart[blockIdx.x * (R + 1L) + R] = s;
+    }
+}
+
+// tr(X X^T), tr(Xhat Xhat^T) and gamma of one side (one warp, fixed order).
+__global__ void lr_stats_kernel(const double* __restrict__ xpart, int nx, const double* __restrict__ rpart, int nrb,
+                                int R, int in, long B, double* __restrict__ st) {
+    const int lane = threadIdx.x;
+    double sx = 0.0, sh = 0.0;
+    for (int i = lane; i < nx; i += 32) {
+        sx += xpart[2 * i];
+        sh += xpart[2 * i + 1];
+    }
+    if (in)
+        for (int i = lane; i < nrb; i += 32) sh += rpart[i * (R + 1L) + R];
+    sx = warp_sum_d(sx);
+    sh = warp_sum_d(sh);
+    if (lane == 0) {
+        if (in) sx += static_cast<double>(B);  // the ones column
+        st[2 * R + 1] = sx;
+        st[2 * R + 2] = sh > 0.0 ? sqrt(sx / sh) : 1.0;
+    }
+}
+
+// Bias step of the preconditioned gradient: g_b = g_in g_out / B sum_b
+// Dhat[b, j] ohat[b]; b -= lr g_b; non-finite flag. Block (0,0) also
+// publishes coef = g_in g_out for the dW epilogue that follows on the stream.
+template <typename T>
+__global__ void lr_bias_kernel(const T* __restrict__ dh, long ld, long B, long C, const float* __restrict__ ohat,
+                               const double* __restrict__ st_in, int rin, const double* __restrict__ st_out,
+                               int rout, float* __restrict__ bias, const float* __restrict__ lr,
+                               const int* __restrict__ step, unsigned* __restrict__ flags, unsigned bit,
+                               float* __restrict__ coef) {
+    __shared__ float sh[32][33];
+    const double g = st_in[2 * rin + 2] * st_out[2 * rout + 2];
+    const long j = blockIdx.x * 32 + threadIdx.x;
+    float acc = 0.f;
+    if (j < C) {
+#pragma unroll 8
+        for (long b = threadIdx.y; b < B; b += 32) acc = fmaf(to_f<T>(dh[b * ld + j]), ohat[b], acc);
+    }
+    sh[threadIdx.y][threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.y == 0 && j < C) {
+        float s = 0.f;
+        for (int r = 0; r < 32; ++r) s += sh[r][threadIdx.x];
+        const float gb = s * static_cast<float>(g / static_cast<double>(B));
+        if (!isfinite(gb) && flags) atomicOr(flags, 1u << bit);
+        bias[j] -= lr[step ? *step : 0] * gb;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) coef[0] = static_cast<float>(g);
+}
+
+// J[r, xcol] = sum_b H[b, r]: the ones column of J = H^T [A | 1].
+__global__ void lr_jcol_kernel(const double* __restrict__ rpart, int nrb, int R, float* __restrict__ YW, long ldY,
+                               long xcol) {
+    const int r = threadIdx.x;
+    if (r >= R) return;
+    double s = 0.0;
+    for (int i = 0; i < nrb; ++i) s += rpart[i * (R + 1L) + r];
+    YW[r * ldY + xcol] = static_cast<float>(s);
+}
+
+__global__ void lr_gram_reduce_kernel(const float* __restrict__ gpart, int S, long n2, float* __restrict__ gram) {
+    const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (i >= n2) return;
+    float s = 0.f;
+    for (int k = 0; k < S; ++k) s += gpart[k * n2 + i];
+    gram[i] = s;
+}
+
+// Subspace update of one side (one CTA, fp64 in shared memory):
+//   Z = E^-1/2 [a^2 K + a(1-eta)(L Dr + Dr L) + (1-eta)^2 Dr G Dr] E^-1/2
+//   with a = eta/B, Dr = diag(d + rho), K = J J^T, L = W J^T, G = W W^T
+//   (from the Gram of [J; W]), symmetrised. Z = U C^2 U^T by one-sided
+//   (Hestenes) Jacobi on the columns of Z itself: rotating column pairs until
+//   they are mutually orthogonal gives Z V = [lambda_i v_i], so the
+//   normalised columns are the eigenvectors and their norms the eigenvalues
+//   (Z is PSD) -- no separate accumulation of U. fp64 (the eigenvalues of
+//   mean-dominated inputs span > 1e6), eight lanes per column pair holding
+//   their rows in registers, every pair of a round concurrently, round-robin
+//   pair order, one barrier per round; a sweep without a rotation above the
+//   relative threshold |a_p.a_q| <= 1e-12 |a_p||a_q| ends it.
+//   Then: eigenpairs sorted descending; scale-relative floors; rho', d', e'
+//   and M = E'^1/2 C^-1 U^T E^-1/2 [a I | (1-eta) Dr].
+__global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, const float* __restrict__ gram, int R,
+                                                     long D, double eta, double a, double alpha,
+                                                     float* __restrict__ M, int max_sweeps) {
+    extern __shared__ double sh[];
+    const int n = (R + 1) & ~1;
+    const int h = n / 2;
+    const int ldb = n + ((24 - (n & 15)) & 15);  // ldb = 8 (mod 16): column parity alternates banks
+    double* dr = sh;            // [n]
+    double* ih = dr + n;        // [n]
+    double* sig = ih + n;       // [n] column norms (eigenvalues)
+    double* misc = sig + n;     // [8]
+    double* cv = misc + 8;      // [n] sorted c
+    double* dv = cv + n;        // [n] sorted d'
+    double* Bc = dv + n;        // [n cols][ldb rows]: Bc[c * ldb + r] = Z[r][c]
+    int* perm = reinterpret_cast<int*>(Bc + n * ldb);  // [n]
+    const int t = threadIdx.x;
+    const int R2 = 2 * R;
+    const double rho = st[2 * R];
+    for (int i = t; i < n; i += blockDim.x) {
+        dr[i] = i < R ? st[i] + rho : 0.0;
+        ih[i] = i < R ? 1.0 / sqrt(st[R + i]) : 0.0;
+    }
+    __syncthreads();
+    const double ce = a * (1.0 - eta), cg = (1.0 - eta) * (1.0 - eta), ck = a * a;
+    for (int idx = t; idx < n * n; idx += blockDim.x) {
+        const int i = idx % n, j = idx / n;  // row i of column j
+        double z = 0.0;
+        if (i < R && j < R) {
+            const double kij = gram[i * R2 + j], kji = gram[j * R2 + i];
+            const double lij = gram[(R + i) * R2 + j], lji = gram[(R + j) * R2 + i];
+            const double gij = gram[(R + i) * R2 + R + j], gji = gram[(R + j) * R2 + R + i];
+            const double zij = ck * kij + ce * (lij * dr[j] + dr[i] * lij) + cg * dr[i] * gij * dr[j];
+            const double zji = ck * kji + ce * (lji * dr[i] + dr[j] * lji) + cg * dr[j] * gji * dr[i];
+            z = 0.5 * (zij + zji) * ih[i] * ih[j];
+        }
+        Bc[j * ldb + i] = z;
+    }
+    // One group of 8 lanes per column pair, every pair of a round concurrently
+    // (launched with 8 * n/2 threads); each lane keeps its <= 12 rows of both
+    // columns in registers between the dot products and the rotation.
+    constexpr int kRows = (LR_MAX_RANK + 7) / 8;
+    const int grp = t >> 3, gl = t & 7;
+    const int ngrp = blockDim.x >> 3;
+    int sweep = 0;
+    const long long clk0 = clock64();
+    for (; sweep < max_sweeps; ++sweep) {
+        int rot = 0;
+        for (int k = 0; k < n - 1; ++k) {
+            for (int pr = grp; pr < h; pr += ngrp) {  // whole warps stay converged: h % 4 == 0 or tail groups idle
+                int p, q;
+                if (pr == 0) {
+                    p = 0;
+                    q = (k % (n - 1)) + 1;
+                } else {
+                    p = ((pr + k) % (n - 1)) + 1;
+                    q = ((n - 1 - pr + k) % (n - 1)) + 1;
+                }
+                double* cp = Bc + p * ldb;
+                double* cq = Bc + q * ldb;
+                double x[kRows], y[kRows];
+                double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+                for (int i = 0; i < kRows; ++i) {
+                    const int r = gl + 8 * i;
+                    x[i] = r < n ? cp[r] : 0.0;
+                    y[i] = r < n ? cq[r] : 0.0;
+                    al = fma(x[i], x[i], al);
+                    be = fma(y[i], y[i], be);
+                    ga = fma(x[i], y[i], ga);
+                }
+                const unsigned gmask = 0xFFu << (t & 24);
+#pragma unroll
+                for (int o = 4; o; o >>= 1) {
+                    al += __shfl_xor_sync(gmask, al, o, 8);
+                    be += __shfl_xor_sync(gmask, be, o, 8);
+                    ga += __shfl_xor_sync(gmask, ga, o, 8);
+                }
+                if (ga * ga > 1e-24 * al * be) {  // |a_p.a_q| > 1e-12 |a_p||a_q|
+                    // angle in fp32 (the residual is removed by the next sweep); the rotation
+                    // itself exactly orthogonal in fp64 (c refined by two Newton steps)
+                    const float zeta = static_cast<float>((be - al) / (2.0 * ga));
+                    const float az = fabsf(zeta);
+                    const float tf = az > 1e18f ? 0.5f / az : 1.f / (az + sqrtf(fmaf(az, az, 1.f)));
+                    const double tt = zeta >= 0.f ? static_cast<double>(tf) : -static_cast<double>(tf);
+                    const double w = fma(tt, tt, 1.0);
+                    double c = static_cast<double>(rsqrtf(static_cast<float>(w)));
+                    c = c * (1.5 - 0.5 * w * c * c);
+                    c = c * (1.5 - 0.5 * w * c * c);
+                    const double sn = c * tt;
+#pragma unroll
+                    for (int i = 0; i < kRows; ++i) {
+                        const int r = gl + 8 * i;
+                        if (r < n) {
+                            cp[r] = c * x[i] - sn * y[i];
+                            cq[r] = sn * x[i] + c * y[i];
+                        }
+                    }
+                    rot = 1;
+                }
+            }
+            __syncthreads();
+        }
+        if (!__syncthreads_or(rot)) break;  // no rotation anywhere in this sweep
+    }
+    const long long clk1 = clock64();
+    // eigenvalues = column norms (PSD); sort descending (ties by index; NaN last)
+    for (int c = t; c < n; c += blockDim.x) {
+        double s2 = 0.0;
+        for (int r = 0; r < n; ++r) s2 = fma(Bc[c * ldb + r], Bc[c * ldb + r], s2);
+        const double v = sqrt(s2);
+        sig[c] = v == v ? v : -1.0;
+    }
+    __syncthreads();
+    if (t < R) {
+        const double li = sig[t];
+        int rank = 0;
+        for (int j = 0; j < R; ++j) {
+            const double lj = sig[j];
+            rank += (lj > li) || (lj == li && j < t);
+        }
+        perm[rank] = t;
+    }
+    __syncthreads();
+    if (t == 0) {
+        // scale-relative floors (oracle/ng_lowrank.py: DELTA, EPS, TINY)
+        double sd = 0.0;
+        for (int k = 0; k < R; ++k) sd += st[k];
+        const double trxx = st[2 * R + 1];
+        const double trt = a * trxx + (1.0 - eta) * (static_cast<double>(D) * rho + sd);
+        const double c0 = sqrt(fmax(sig[perm[0]], 0.0));
+        const double floor = fmax(fmax(kDelta * c0, kEps * trt / static_cast<double>(D)), kTiny);
+        double sc = 0.0;
+        for (int k = 0; k < R; ++k) {
+            const double c = fmax(sqrt(fmax(sig[perm[k]], 0.0)), floor);
+            cv[k] = c;
+            sc += c;
+        }
+        const double rho1 =
+            fmax(fmax((trt - sc) / static_cast<double>(D - R), kEps * trt / static_cast<double>(D)), kTiny);
+        double sd1 = 0.0;
+        for (int k = 0; k < R; ++k) {
+            dv[k] = fmax(cv[k] - rho1, floor);
+            sd1 += dv[k];
+        }
+        misc[0] = rho1;
+        misc[1] = rho1 * (1.0 + alpha) + alpha * sd1 / static_cast<double>(D);
+    }
+    __syncthreads();
+    const double beta1 = misc[1];
+    for (int idx = t; idx < R * R2; idx += blockDim.x) {
+        const int k = idx / R2, j = idx % R2, jj = j % R;
+        const int col = perm[k];
+        const double e1 = dv[k] / (dv[k] + beta1);
+        const double u = sig[col] > 0.0 ? Bc[col * ldb + jj] / sig[col] : 0.0;  // eigenvector k, entry jj
+        const double f = sqrt(e1) / cv[k] * u * ih[jj] * (j < R ? a : (1.0 - eta) * dr[jj]);
+        M[idx] = static_cast<float>(f);
+    }
+    __syncthreads();
+    for (int k = t; k < R; k += blockDim.x) {
+        st[k] = dv[k];
+        st[R + k] = dv[k] / (dv[k] + beta1);
+    }
+    if (t == 0) {
+        st[2 * R] = misc[0];
+        st[2 * R + 3] = sweep;                             // diagnostics: Jacobi sweeps used,
+        st[2 * R + 4] = static_cast<double>(clk1 - clk0);  // and their SM cycles
+    }
+}
+
+size_t eig_smem(int R) {
+    const int n = (R + 1) & ~1;
+    const int ldb = n + ((24 - (n & 15)) & 15);
+    return (5 * static_cast<size_t>(n) + 8 + static_cast<size_t>(n) * ldb) * sizeof(double) + (n + 4) * sizeof(int);
+}
+
+__global__ void lr_split_kernel(const float* __restrict__ w, long n, long rstride, bf16* __restrict__ wop) {
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += gridDim.x * (long)blockDim.x) {
+        const bf16 hi = __float2bfloat16_rn(w[i]);
+        wop[i] = hi;
+        wop[rstride + i] = __float2bfloat16_rn(w[i] - __bfloat162float(hi));
+    }
+}
+
+
+// W' = M [J; W] per 32-column chunk (in place: the chunk is staged in shared
+// memory first), plus the bf16 operand copy.
+template <typename T>
+__global__ void __launch_bounds__(256) lr_wupdate_kernel(float* __restrict__ YW, long ldY, int R, long D,
+                                                         const float* __restrict__ M, T* __restrict__ wop) {
+    extern __shared__ float smf[];
+    const int R2 = 2 * R;
+    float* Ms = smf;             // [R][2R]
+    float* Ys = Ms + R * R2;     // [2R][32]
+    const long c0 = blockIdx.x * 32L;
+    const int t = threadIdx.x;
+    for (int i = t; i < R * R2; i += blockDim.x) Ms[i] = M[i];
+    for (int i = t; i < R2 * 32; i += blockDim.x) {
+        const int r = i >> 5, c = i & 31;
+        Ys[i] = (c0 + c < D) ? YW[r * ldY + c0 + c] : 0.f;
+    }
+    __syncthreads();
+    const int c = t & 31, rg = t >> 5;
+    if (c0 + c >= D) return;
+    for (int k = rg; k < R; k += 8) {
+        float acc = 0.f;
+        const float* mk = Ms + k * R2;
+#pragma unroll 8
+        for (int j = 0; j < R2; ++j) acc = fmaf(mk[j], Ys[j * 32 + c], acc);
+        YW[(R + k) * ldY + c0 + c] = acc;
+        if (wop) {  // bf16: W_hi and W_lo = W - W_hi
+            const T hi = from_f<T>(acc);
+            wop[k * ldY + c0 + c] = hi;
+            wop[(R + k) * ldY + c0 + c] = from_f<T>(acc - to_f<T>(hi));
+        }
+    }
+}
+
+int lr_rank(int want, long dim) { return static_cast<int>(std::max<long>(1, std::min<long>(want, dim - 1))); }
+
+void side_alloc(Replica& r, LrSide& sd, bool in, long dx, int want_rank, int layer) {
+    sd.in = in;
+    sd.dx = dx;
+    sd.D = dx + (in ? 1 : 0);
+    sd.R = lr_rank(want_rank, sd.D);
+    if (sd.R > LR_MAX_RANK) throw std::runtime_error("ng lowrank: rank " + std::to_string(sd.R) + " exceeds " +
+                                                     std::to_string(LR_MAX_RANK));
+    const int R = sd.R;
+    const long B = r.B;
+    sd.ldY = pad32(sd.D);
+    sd.ns = r.f32() ? 1 : 2;
+    sd.ldH = pad32(sd.ns * R);
+    sd.ldx = pad32(dx);
+    const size_t es = r.esz();
+    sd.YW = falloc(2 * R * sd.ldY);
+    sd.wop = r.f32() ? static_cast<void*>(sd.YW + R * sd.ldY) : valloc(2 * R * sd.ldY * 2);  // fp32: alias
+    sd.H = valloc(B * sd.ldH * es);
+    sd.ohat = falloc(B);
+    sd.nrb = static_cast<int>((B + 7) / 8);
+    sd.rpart = dalloc_d(sd.nrb * (R + 1L));
+    sd.xpart = dalloc_d(2 * 1024);
+    sd.gram = falloc(4L * R * R);
+    sd.st = dalloc_d(2 * R + 8);
+    sd.M = falloc(2L * R * R);
+    sd.xhat = valloc(B * sd.ldx * es);
+    CUDA_THROW(cudaStreamCreateWithFlags(&sd.stream, cudaStreamNonBlocking));
+    CUDA_THROW(cudaEventCreateWithFlags(&sd.ready, cudaEventDisableTiming));
+    CUDA_THROW(cudaEventCreateWithFlags(&sd.done, cudaEventDisableTiming));
+    // initial state: d = rho = eps, e = d / (d + beta), W = E^1/2 R0
+    const std::vector<double> basis = host::lowrank_basis(sd.D, R, host::lowrank_seed(layer, in ? 0 : 1));
+    const double alpha = r.lrc.alpha;
+    const double beta = kEps * (1.0 + alpha) + alpha * (R * kEps) / static_cast<double>(sd.D);
+    const double e0 = kEps / (kEps + beta);
+    std::vector<double> sth(2 * R + 8, 0.0);
+    for (int i = 0; i < R; ++i) {
+        sth[i] = kEps;
+        sth[R + i] = e0;
+    }
+    sth[2 * R] = kEps;
+    CUDA_THROW(cudaMemcpy(sd.st, sth.data(), sth.size() * 8, cudaMemcpyHostToDevice));
+    std::vector<float> w(R * sd.ldY, 0.f);
+    const double se = std::sqrt(e0);
+    for (int i = 0; i < R; ++i)
+        for (long j = 0; j < sd.D; ++j) w[i * sd.ldY + j] = static_cast<float>(se * basis[i * sd.D + j]);
+    CUDA_THROW(cudaMemcpy(sd.YW + R * sd.ldY, w.data(), w.size() * 4, cudaMemcpyHostToDevice));
+    if (!r.f32()) {
+        lr_split_kernel<<<64, 256>>>(sd.YW + R * sd.ldY, R * sd.ldY, R * sd.ldY, static_cast<bf16*>(sd.wop));
+        CUDA_THROW(cudaGetLastError());
+    }
+    CUDA_THROW(cudaDeviceSynchronize());
+}
+
+void side_free(LrSide& sd) {
+    auto f = [](void* p) {
+        if (p) cudaFree(p);
+    };
+    f(sd.YW);
+    if (sd.wop && sd.wop != static_cast<void*>(sd.YW + sd.R * sd.ldY)) f(sd.wop);
+    f(sd.hpart);
+    f(sd.H);
+    f(sd.ohat);
+    f(sd.rpart);
+    f(sd.xpart);
+    f(sd.gpart);
+    f(sd.gram);
+    f(sd.st);
+    f(sd.M);
+    f(sd.xhat);
+    if (sd.ready) cudaEventDestroy(sd.ready);
+    if (sd.done) cudaEventDestroy(sd.done);
+    if (sd.stream) cudaStreamDestroy(sd.stream);
+    sd = LrSide();
+}
+
+void side_plans(Replica& r, LrSide& sd, const void* X) {
+    const int sms = r.ctx->num_sms;
+    const int prec = r.prec;
+    const long B = r.B;
+    const int R = sd.R;
+    sd.X = X;
+    // H = X W^T: M = B, N = R, K = dx; split-K so the skinny product fills the GPU
+    {
+        GemmEpi e;
+        e.mode = EPI_PARTIAL;
+        const int NR = sd.ns * R;  // bf16: [W_hi; W_lo]
+        const int bn = NR <= 64 ? 64 : (NR <= 128 ? 128 : 256);
+        const int tiles = static_cast<int>((B + 127) / 128);
+        e.ksplit = std::max(1, sms / tiles);
+        const int bk = r.f32() ? 32 : 64;
+        const int nk = static_cast<int>((sd.dx + bk - 1) / bk);
+        const int per = (nk + e.ksplit - 1) / e.ksplit;
+        const int S = (nk + per - 1) / per;
+        if (sd.hpart) cudaFree(sd.hpart);
+        sd.hpart = falloc(static_cast<size_t>(S) * B * NR);
+        e.out32 = sd.hpart;
+        e.ld_out32 = NR;
+        e.split_stride = B * NR;
+        gemm_plan(sd.hg, prec, false, X, sd.ldx, false, sd.wop, sd.ldY, static_cast<int>(B), NR,
+                  static_cast<int>(sd.dx), e, sms, bn);
+    }
+    // Xhat = X - H W: M = B, N = dx, K = R
+    {
+        GemmEpi e;
+        e.mode = EPI_RESID;
+        e.out = sd.xhat;
+        e.ld_out = sd.ldx;
+        e.aux = X;
+        e.ld_aux = sd.ldx;
+        e.part = sd.xpart;
+        gemm_plan(sd.xg, prec, false, sd.H, sd.ldH, true, sd.wop, sd.ldY, static_cast<int>(B),
+                  static_cast<int>(sd.dx), sd.ns * R, e, sms);
+        if (sd.xg.grid.x > 1024) throw std::runtime_error("ng lowrank: residual grid too large");
+    }
+    // J = H^T X: M = R, N = dx, K = B (fp32 out into the J rows of YW)
+    {
+        GemmEpi e;
+        e.mode = EPI_GRAD;
+        e.alpha = 1.f;
+        e.out32 = sd.YW;
+        e.ld_out32 = sd.ldY;
+        gemm_plan(sd.jg, prec, true, sd.H, sd.ldH, true, X, sd.ldx, R, static_cast<int>(sd.dx),
+                  static_cast<int>(B), e, sms);
+    }
+    // Gram of [J; W] (2R x 2R, K = D), fp32-accurate, split-K
+    {
+        GemmEpi e;
+        e.mode = EPI_PARTIAL;
+        const int n2 = 2 * R;
+        const int tiles = ((n2 + 127) / 128) * ((n2 + 63) / 64);
+        e.ksplit = std::max(1, sms / tiles);
+        const int nk = static_cast<int>((sd.D + 31) / 32);
+        const int per = (nk + e.ksplit - 1) / e.ksplit;
+        const int S = (nk + per - 1) / per;
+        if (sd.gpart) cudaFree(sd.gpart);
+        sd.gpart = falloc(static_cast<size_t>(S) * n2 * n2);
+        e.out32 = sd.gpart;
+        e.ld_out32 = n2;
+        e.split_stride = static_cast<long>(n2) * n2;
+        gemm_plan(sd.gg, PREC_FP32, false, sd.YW, sd.ldY, false, sd.YW, sd.ldY, n2, n2, static_cast<int>(sd.D), e,
+                  sms, 64);
+    }
+}
+
+}  // namespace
+
+void lr_alloc(Replica& r) {
+    r.lrl.resize(r.L);
+    for (int l = 0; l < r.L; ++l) {
+        side_alloc(r, r.lrl[l].in, true, r.dims[l], r.lrc.rank_in, l);
+        side_alloc(r, r.lrl[l].out, false, r.dims[l + 1], r.lrc.rank_out, l);
+        r.lrl[l].coef = falloc(4);
+    }
+}
+
+void lr_free(Replica& r) {
+    for (auto& ly : r.lrl) {
+        side_free(ly.in);
+        side_free(ly.out);
+        if (ly.coef) cudaFree(ly.coef);
+    }
+    r.lrl.clear();
+}
+
+void lr_build_plans(Replica& r) {
+    static bool attr = false;
+    if (!attr) {
+        CUDA_THROW(cudaFuncSetAttribute(lr_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(eig_smem(LR_MAX_RANK))));
+        const int ws = (LR_MAX_RANK * 2 * LR_MAX_RANK + 2 * LR_MAX_RANK * 32) * 4;
+        CUDA_THROW(cudaFuncSetAttribute(lr_wupdate_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, ws));
+        CUDA_THROW(cudaFuncSetAttribute(lr_wupdate_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, ws));
+        attr = true;
+    }
+    for (int l = 0; l < r.L; ++l) {
+        side_plans(r, r.lrl[l].in, r.acts[l]);
+        side_plans(r, r.lrl[l].out, r.dz[l]);
+    }
+}
+
+void lr_precondition_side(Replica& r, LrSide& sd, cudaStream_t s) {
+    gemm_launch(sd.hg, s);
+    const float* wm = sd.YW + sd.R * sd.ldY;
+    if (r.f32())
+        lr_hreduce_kernel<float, 1><<<sd.nrb, 256, 0, s>>>(sd.hpart, sd.hg.ep.ksplit, r.B, sd.R, wm, sd.ldY, sd.dx,
+                                                          sd.in, static_cast<float*>(sd.H), sd.ldH, sd.ohat, sd.rpart);
+    else
+        lr_hreduce_kernel<bf16, 2><<<sd.nrb, 256, 0, s>>>(sd.hpart, sd.hg.ep.ksplit, r.B, sd.R, wm, sd.ldY, sd.dx,
+                                                         sd.in, static_cast<bf16*>(sd.H), sd.ldH, sd.ohat, sd.rpart);
+    CUDA_THROW(cudaGetLastError());
+    gemm_launch(sd.xg, s);
+    lr_stats_kernel<<<1, 32, 0, s>>>(sd.xpart, static_cast<int>(sd.xg.grid.x), sd.rpart, sd.nrb, sd.R, sd.in, r.B,
+                                     sd.st);
+    CUDA_THROW(cudaGetLastError());
+}
+
+void lr_start_update(Replica& r, LrSide& sd, cudaStream_t s) {
+    gemm_launch(sd.jg, s);
+    if (sd.in) {
+        lr_jcol_kernel<<<1, 128, 0, s>>>(sd.rpart, sd.nrb, sd.R, sd.YW, sd.ldY, sd.dx);
+        CUDA_THROW(cudaGetLastError());
+    }
+}
+
+void lr_apply_update(Replica& r, LrSide& sd, cudaStream_t s) {
+    gemm_launch(sd.gg, s);
+    const long n2 = 4L * sd.R * sd.R;
+    lr_gram_reduce_kernel<<<static_cast<unsigned>((n2 + 255) / 256), 256, 0, s>>>(sd.gpart, sd.gg.ep.ksplit, n2,
+                                                                                  sd.gram);
+    const double eta = 1.0 - std::exp(-static_cast<double>(r.B) * r.lrc.update_period / r.lrc.history);
+    const double a = eta / static_cast<double>(r.B);
+    const int npair = ((sd.R + 1) & ~1) / 2;
+    const int ethreads = std::max(128, (npair * 8 + 31) / 32 * 32);  // 8 lanes per pair, all pairs concurrently
+    lr_eig_kernel<<<1, ethreads, eig_smem(sd.R), s>>>(sd.st, sd.gram, sd.R, sd.D, eta, a, r.lrc.alpha, sd.M, 40);
+    const int R2 = 2 * sd.R;
+    const size_t ws = (static_cast<size_t>(sd.R) * R2 + R2 * 32) * 4;
+    const unsigned grid = static_cast<unsigned>((sd.D + 31) / 32);
+    if (r.f32())
+        lr_wupdate_kernel<float><<<grid, 256, ws, s>>>(sd.YW, sd.ldY, sd.R, sd.D, sd.M, nullptr);
+    else
+        lr_wupdate_kernel<bf16><<<grid, 256, ws, s>>>(sd.YW, sd.ldY, sd.R, sd.D, sd.M, static_cast<bf16*>(sd.wop));
+    CUDA_THROW(cudaGetLastError());
+}
+
+void lr_layer_update(Replica& r, int l, cudaStream_t s) {
+    LrLayer& ly = r.lrl[l];
+    const long dout = r.dims[l + 1];
+    dim3 grid((dout + 31) / 32), block(32, 32);
+    float* bias = r.params + r.b_off[l];
+    if (r.f32())
+        lr_bias_kernel<float><<<grid, block, 0, s>>>(static_cast<const float*>(ly.out.xhat), ly.out.ldx, r.B, dout,
+                                                     ly.in.ohat, ly.in.st, ly.in.R, ly.out.st, ly.out.R, bias, r.d_lr,
+                                                     r.d_step, r.d_flags, 2 * l + 1, ly.coef);
+    else
+        lr_bias_kernel<bf16><<<grid, block, 0, s>>>(static_cast<const bf16*>(ly.out.xhat), ly.out.ldx, r.B, dout,
+                                                    ly.in.ohat, ly.in.st, ly.in.R, ly.out.st, ly.out.R, bias, r.d_lr,
+                                                    r.d_step, r.d_flags, 2 * l + 1, ly.coef);
+    CUDA_THROW(cudaGetLastError());
+    gemm_launch(r.dw[l], s);
+}
+
+int Replica::lr_variant(long t) const {
+    const long P = std::max(1, lrc.update_period);
+    int v = 0;
+    if (t == 0) v |= 1;
+    if (t % P == 0) v |= 2;
+    if (t >= 1 && (t - 1) % P == 0) v |= 4;
+    return v;
+}
+
+void Replica::set_lowrank(const LrConfig& c) {
+    if (opt != OPT_NG_LOWRANK) throw std::runtime_error("replica: not a low-rank NG-SGD replica");
+    if (c.rank_in < 1 || c.rank_out < 1 || c.rank_in > LR_MAX_RANK || c.rank_out > LR_MAX_RANK)
+        throw std::runtime_error("ng lowrank: ranks must be in [1, " + std::to_string(LR_MAX_RANK) + "]");
+    if (c.update_period < 1) throw std::runtime_error("ng lowrank: update_period must be >= 1");
+    if (c.init_iters < 0) throw std::runtime_error("ng lowrank: init_iters must be >= 0");
+    if (!(c.history > 0.0)) throw std::runtime_error("ng lowrank: num_samples_history must be positive");
+    if (!(c.alpha > 0.0)) throw std::runtime_error("ng lowrank: alpha must be positive");
+    CUDA_THROW(cudaDeviceSynchronize());
+    lr_free(*this);
+    lrc = c;
+    lr_t = 0;
+    lr_alloc(*this);
+    if (bound) bind(bound);
+}
+
+void Replica::get_lowrank_state(int layer, int side, double* w, double* d, double* rho) const {
+    if (opt != OPT_NG_LOWRANK) throw std::runtime_error("replica: not a low-rank NG-SGD replica");
+    if (layer < 0 || layer >= L || side < 0 || side > 1) throw std::runtime_error("ng lowrank: bad layer/side");
+    const LrSide& sd = side == 0 ? lrl[layer].in : lrl[layer].out;
+    CUDA_THROW(cudaDeviceSynchronize());
+    std::vector<float> wf(sd.R * sd.ldY);
+    CUDA_THROW(cudaMemcpy(wf.data(), sd.YW + sd.R * sd.ldY, wf.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<double> sth(2 * sd.R + 1);
+    CUDA_THROW(cudaMemcpy(sth.data(), sd.st, sth.size() * 8, cudaMemcpyDeviceToHost));
+    if (w)
+        for (int i = 0; i < sd.R; ++i)
+            for (long j = 0; j < sd.D; ++j) w[i * sd.D + j] = wf[i * sd.ldY + j];
+    if (d)
+        for (int i = 0; i < sd.R; ++i) d[i] = sth[i];
+    if (rho) *rho = sth[2 * sd.R];
+}
+
+}  // namespace pnb

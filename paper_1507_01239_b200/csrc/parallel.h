@@ -40,7 +40,7 @@ struct Averager {
 
 struct TrainConfig {
     uint64_t workers = 1, avg_frequency = 10, minibatch = 128, base_seed = 0;
-    int optimizer = 1;   // 0 sgd, 1 ngsgd (parallel.hpp:31-38 default)
+    int optimizer = 1;   // 0 sgd, 1 ngsgd kron-full (parallel.hpp:31-38 default), 2 ngsgd low-rank
     int newbob = 0;      // 0 exponential (default), 1 newbob
     double lr_init = 0.32;
     uint64_t epochs = 15;
@@ -50,6 +50,7 @@ struct TrainConfig {
     uint64_t rank0 = 0;   // first global worker rank hosted by this process
     uint64_t local = 0;   // workers hosted by this process (0 = all)
     int serial = 0;       // serial_train semantics (errors not wrapped)
+    LrConfig lr;          // optimizer 2: low-rank NG-SGD knobs (alpha = ng_smoothing)
 };
 
 struct EpochRec {

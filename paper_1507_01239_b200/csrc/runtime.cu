@@ -131,6 +131,7 @@ Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision
     params = dalloc<float>(n_pad);
     if (!f32()) wshadow = dalloc<bf16>(n_pad);
     if (opt == OPT_NG_KRON) grads = dalloc<float>(n_pad);
+    if (opt == OPT_NG_LOWRANK) lrc.alpha = ng_smoothing;
     for (int l = 0; l <= L; ++l) ld_act.push_back(pad32(dims[l]));
     for (int l = 0; l < L; ++l) acts.push_back(f32() ? (void*)dalloc<float>(B * ld_act[l]) : (void*)dalloc<bf16>(B * ld_act[l]));
     acts.push_back(nullptr);  // the last layer keeps Z (fp32) in zout
@@ -143,6 +144,12 @@ Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision
             r_out.push_back(dalloc<float>(dims[l + 1] * pad32(dims[l + 1])));
         }
         ng_alloc(*this);
+    }
+    if (opt == OPT_NG_LOWRANK) {
+        lr_alloc(*this);
+        ev_act.resize(L);
+        for (auto& e : ev_act) CUDA_THROW(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_THROW(cudaEventCreateWithFlags(&ev_t0, cudaEventDisableTiming));
     }
     scal = dalloc<double>(16 * (L + 1) + 512);
     d_step = dalloc<int>(4);
@@ -158,6 +165,11 @@ Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision
 Replica::~Replica() {
     if (stream) cudaStreamSynchronize(stream);
     if (graph) cudaGraphExecDestroy(graph);
+    for (auto g : vgraphs)
+        if (g) cudaGraphExecDestroy(g);
+    lr_free(*this);
+    for (auto e : ev_act) cudaEventDestroy(e);
+    if (ev_t0) cudaEventDestroy(ev_t0);
     dfree(params);
     dfree(wshadow);
     dfree(grads);
@@ -290,7 +302,7 @@ void Replica::bind(DeviceDataset* ds) {
         g.alpha = 1.f / static_cast<float>(B);
         g.flag = d_flags;
         g.flag_bit = 2 * l;
-        if (opt == OPT_SGD) {
+        if (opt == OPT_SGD || opt == OPT_NG_LOWRANK) {
             g.mode = EPI_GRAD_SGD;
             g.out32 = params + w_off[l];
             g.ld_out32 = ldw[l];
@@ -303,7 +315,14 @@ void Replica::bind(DeviceDataset* ds) {
             g.out32 = grads + w_off[l];
             g.ld_out32 = ldw[l];
         }
-        gemm_plan(dw[l], prec, true, dz[l], ld_act[l + 1], true, acts[l], ld_act[l], dout, din, B, g, sms);
+        if (opt == OPT_NG_LOWRANK) {
+            // dW = g_in g_out / B  Dhat^T Ahat  (preconditioned vectors; coef written by lr_bias_kernel)
+            g.coef = lrl[l].coef;
+            gemm_plan(dw[l], prec, true, lrl[l].out.xhat, lrl[l].out.ldx, true, lrl[l].in.xhat, lrl[l].in.ldx, dout,
+                      din, B, g, sms);
+        } else {
+            gemm_plan(dw[l], prec, true, dz[l], ld_act[l + 1], true, acts[l], ld_act[l], dout, din, B, g, sms);
+        }
 
         if (l > 0) {
             // dz_{l-1} = (dz_l W_l) * act'(A_{l-1})   (M = B, N = din, K = dout)
@@ -329,10 +348,18 @@ void Replica::bind(DeviceDataset* ds) {
         }
     }
     if (opt == OPT_NG_KRON) ng_build_plans(*this);
+    if (opt == OPT_NG_LOWRANK) lr_build_plans(*this);
     if (graph) {
         cudaGraphExecDestroy(graph);
         graph = nullptr;
     }
+    for (auto& g : vgraphs)
+        if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+    vgraphs.assign(8, nullptr);
+    vnodes.assign(8, 0);
     if (std::getenv("PARNN_NO_GRAPH")) use_graph = false;  // debugging: eager launches
     tl.clear();
     if (std::getenv("PARNN_TIMELINE") && tl_pool.empty()) {
@@ -340,21 +367,33 @@ void Replica::bind(DeviceDataset* ds) {
         for (auto& e : tl_pool) CUDA_THROW(cudaEventCreate(&e));
     }
     if (use_graph) {
-        cudaStream_t s = stream;
-        cudaGraph_t g;
-        CUDA_THROW(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        try {
-            enqueue_step(s);
-        } catch (...) {
-            cudaStreamEndCapture(s, &g);
-            throw;
+        auto capture = [&](int v, cudaGraphExec_t* out, long* nodes_out) {
+            variant = v;
+            cudaStream_t s = stream;
+            cudaGraph_t g;
+            CUDA_THROW(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue_step(s);
+            } catch (...) {
+                cudaStreamEndCapture(s, &g);
+                throw;
+            }
+            CUDA_THROW(cudaStreamEndCapture(s, &g));
+            size_t nodes = 0;
+            CUDA_THROW(cudaGraphGetNodes(g, nullptr, &nodes));
+            *nodes_out = static_cast<long>(nodes);
+            CUDA_THROW(cudaGraphInstantiate(out, g, 0));
+            cudaGraphDestroy(g);
+        };
+        if (opt == OPT_NG_LOWRANK) {
+            // one graph per step kind; kernels_per_step = the average over one update period
+            const int P = std::max(1, lrc.update_period);
+            const std::vector<int> kinds = P == 1 ? std::vector<int>{3, 6} : std::vector<int>{3, 0, 2, 4};
+            for (int v : kinds) capture(v, &vgraphs[v], &vnodes[v]);
+            kernels_per_step = P == 1 ? vnodes[6] : (vnodes[2] + vnodes[4] + (P - 2) * vnodes[0]) / P;
+        } else {
+            capture(0, &graph, &kernels_per_step);
         }
-        CUDA_THROW(cudaStreamEndCapture(s, &g));
-        size_t nodes = 0;
-        CUDA_THROW(cudaGraphGetNodes(g, nullptr, &nodes));
-        kernels_per_step = static_cast<long>(nodes);
-        CUDA_THROW(cudaGraphInstantiate(&graph, g, 0));
-        cudaGraphDestroy(g);
     }
 }
 
@@ -393,7 +432,119 @@ void Replica::mark(const char* kind, int layer, double flops, cudaStream_t s) {
     prof->flops.push_back(flops);
 }
 
+namespace {
+
+// One side's in-step chain on its own stream: [init updates], precondition,
+// [J of the update applied at the start of the next step].
+void lr_side_chain(Replica& r, LrSide& sd, cudaEvent_t wait, cudaStream_t ss) {
+    if (wait) CUDA_THROW(cudaStreamWaitEvent(ss, wait, 0));
+    if (r.variant & 1)
+        for (int it = 0; it < r.lrc.init_iters; ++it) {
+            lr_precondition_side(r, sd, ss);
+            lr_start_update(r, sd, ss);
+            lr_apply_update(r, sd, ss);
+        }
+    lr_precondition_side(r, sd, ss);
+    CUDA_THROW(cudaEventRecord(sd.ready, ss));
+    if (r.variant & 2) lr_start_update(r, sd, ss);
+    CUDA_THROW(cudaEventRecord(sd.done, ss));
+}
+
+// The low-rank NG step. Concurrency: the pending subspace updates run from
+// t0 alongside the forward pass; each layer's in-side chain starts as soon
+// as the forward has produced its input, each out-side chain as soon as the
+// backward has produced its dz; dW_l (+ bias) runs on the side stream once
+// dA_l has read W_l and both sides of layer l are preconditioned.
+void enqueue_lowrank(Replica& r, cudaStream_t s) {
+    const bool F = r.f32();
+    const int L = r.L;
+    DeviceDataset* ds = r.bound;
+    auto gf = [](const GemmPlan& p) { return 2.0 * p.M * p.N * p.K; };
+    if (r.prof) {
+        // profiled: serial on one stream so event regions are well defined
+        r.mark("start", -1, 0, s);
+        if (r.variant & 4) {
+            for (int l = 0; l < L; ++l) {
+                lr_apply_update(r, r.lrl[l].in, s);
+                lr_apply_update(r, r.lrl[l].out, s);
+            }
+            r.mark("ng_lr_apply", -1, 0, s);
+        }
+        launch_gather(ds->features(r.prec), ds->ld, ds->y, r.d_rows, r.d_step, r.B, r.dims[0], r.acts[0],
+                      r.ld_act[0], r.d_ybatch, F, s);
+        r.mark("gather", 0, 0, s);
+        for (int l = 0; l < L; ++l) {
+            gemm_launch(r.fwd[l], s);
+            r.mark("gemm_fwd", l, gf(r.fwd[l]), s);
+        }
+        launch_softmax_ce(r.zout, r.ld_act[L], r.B, r.dims[L], r.d_ybatch, r.dz[L - 1], r.ld_act[L], r.ce_rows, F, s);
+        r.mark("softmax_ce", L - 1, 0, s);
+        for (int l = L - 1; l > 0; --l) {
+            gemm_launch(r.da[l], s);
+            r.mark("gemm_da", l, gf(r.da[l]), s);
+        }
+        for (int l = L - 1; l >= 0; --l) {
+            lr_side_chain(r, r.lrl[l].in, nullptr, s);
+            lr_side_chain(r, r.lrl[l].out, nullptr, s);
+            r.mark("ng_lr_precondition", l, 0, s);
+            lr_layer_update(r, l, s);
+            r.mark("gemm_dw_sgd", l, gf(r.dw[l]), s);
+        }
+    } else {
+        static const bool serial = std::getenv("PARNN_LR_SERIAL") != nullptr;  // debugging: one stream
+        auto S = [&](cudaStream_t x) { return serial ? s : x; };
+        r.tmark("t0", s);
+        CUDA_THROW(cudaEventRecord(r.ev_t0, s));
+        for (int l = 0; l < L; ++l)
+            for (LrSide* sd : {&r.lrl[l].in, &r.lrl[l].out}) {
+                CUDA_THROW(cudaStreamWaitEvent(S(sd->stream), r.ev_t0, 0));
+                if (r.variant & 4) lr_apply_update(r, *sd, S(sd->stream));
+            }
+        launch_gather(ds->features(r.prec), ds->ld, ds->y, r.d_rows, r.d_step, r.B, r.dims[0], r.acts[0],
+                      r.ld_act[0], r.d_ybatch, F, s);
+        CUDA_THROW(cudaEventRecord(r.ev_act[0], s));
+        lr_side_chain(r, r.lrl[0].in, r.ev_act[0], S(r.lrl[0].in.stream));
+        for (int l = 0; l < L; ++l) {
+            gemm_launch(r.fwd[l], s);
+            if (l + 1 < L) {
+                CUDA_THROW(cudaEventRecord(r.ev_act[l + 1], s));
+                lr_side_chain(r, r.lrl[l + 1].in, r.ev_act[l + 1], S(r.lrl[l + 1].in.stream));
+            }
+        }
+        launch_softmax_ce(r.zout, r.ld_act[L], r.B, r.dims[L], r.d_ybatch, r.dz[L - 1], r.ld_act[L], r.ce_rows, F, s);
+        r.tmark("fwd", s);
+        CUDA_THROW(cudaEventRecord(r.ev_dw[L - 1], s));  // dz[L-1] ready
+        lr_side_chain(r, r.lrl[L - 1].out, r.ev_dw[L - 1], S(r.lrl[L - 1].out.stream));
+        for (int l = L - 1; l >= 0; --l) {
+            if (l > 0) gemm_launch(r.da[l], s);
+            CUDA_THROW(cudaEventRecord(r.ev_bwd[l], s));  // W_l read; dz[l-1] ready
+            if (l > 0) lr_side_chain(r, r.lrl[l - 1].out, r.ev_bwd[l], S(r.lrl[l - 1].out.stream));
+            CUDA_THROW(cudaStreamWaitEvent(S(r.side), r.ev_bwd[l], 0));
+            CUDA_THROW(cudaStreamWaitEvent(S(r.side), r.lrl[l].in.ready, 0));
+            CUDA_THROW(cudaStreamWaitEvent(S(r.side), r.lrl[l].out.ready, 0));
+            lr_layer_update(r, l, S(r.side));
+            r.tmark("dw" + std::to_string(l), S(r.side));
+        }
+        CUDA_THROW(cudaEventRecord(r.ev_side, S(r.side)));
+        CUDA_THROW(cudaStreamWaitEvent(s, r.ev_side, 0));
+        for (int l = 0; l < L; ++l) {
+            CUDA_THROW(cudaStreamWaitEvent(s, r.lrl[l].in.done, 0));
+            CUDA_THROW(cudaStreamWaitEvent(s, r.lrl[l].out.done, 0));
+        }
+    }
+    flags_latch_kernel<<<1, 1, 0, s>>>(r.d_flags, r.d_step);
+    launch_ce_reduce(r.ce_rows, r.B, r.d_ce, r.d_step, 1, s);
+    r.mark("ce_reduce", 0, 0, s);
+    r.tmark("end", s);
+}
+
+}  // namespace
+
 void Replica::enqueue_step(cudaStream_t s) {
+    if (opt == OPT_NG_LOWRANK) {
+        enqueue_lowrank(*this, s);
+        return;
+    }
     const bool F = f32();
     DeviceDataset* ds = bound;
     auto gf = [](const GemmPlan& p) { return 2.0 * p.M * p.N * p.K; };
@@ -499,6 +650,7 @@ void Replica::profile_steps(long steps, std::vector<std::string>& names, std::ve
     for (long it = 0; it < steps; ++it) {
         Profile p;
         prof = &p;
+        if (opt == OPT_NG_LOWRANK) variant = lr_variant(lr_t++);
         try {
             enqueue_step(stream);
         } catch (...) {
@@ -546,6 +698,17 @@ void Replica::upload_epoch(const uint32_t* rows, const float* lrs, long steps) {
 
 void Replica::run_step(cudaStream_t s) {
     if (!bound) throw std::runtime_error("replica: no dataset bound");
+    if (opt == OPT_NG_LOWRANK) {
+        variant = lr_variant(lr_t);
+        static const char* force = std::getenv("PARNN_LR_FORCE_VARIANT");  // timing aid: 0 plain, 2 J, 4 apply
+        if (force && lr_t > 0) variant = std::atoi(force);
+        if (use_graph && vgraphs[variant])
+            CUDA_THROW(cudaGraphLaunch(vgraphs[variant], s));
+        else
+            enqueue_step(s);
+        ++lr_t;
+        return;
+    }
     if (graph)
         CUDA_THROW(cudaGraphLaunch(graph, s));
     else

@@ -40,7 +40,7 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
 void gemm_launch(const GemmPlan& p, cudaStream_t s);
 
 enum Precision : int { PREC_BF16 = 0, PREC_TF32 = 1, PREC_FP32 = 2 };
-enum Optimizer : int { OPT_SGD = 0, OPT_NG_KRON = 1 };
+enum Optimizer : int { OPT_SGD = 0, OPT_NG_KRON = 1, OPT_NG_LOWRANK = 2 };
 
 inline long pad32(long v) { return (v + 31) / 32 * 32; }
 
@@ -99,6 +99,47 @@ struct NgLayer {
     cudaEvent_t done = nullptr, ev_ready = nullptr, ev_in_done = nullptr;
 };
 
+// NG-SGD low-rank online preconditioner (ng_lowrank.cu; SURVEY §8a A17,
+// Povey et al. 2014). One side = one of the two per-example vector sets of a
+// layer: "in" = [A_prev | 1] (D = din + 1), "out" = dz (D = dout).
+constexpr int LR_MAX_RANK = 96;
+struct LrConfig {
+    int rank_in = 20, rank_out = 80;  // Kaldi nnet2/3 defaults
+    int update_period = 4;            // subspace update every P minibatches
+    int init_iters = 3;               // updates on the first minibatch before use
+    double history = 2000.0;          // S: eta = 1 - exp(-B P / S)
+    double alpha = 4.0;               // smoothing (the reference's ng_smoothing)
+};
+struct LrSide {
+    bool in = false;
+    long dx = 0;  // columns of X proper (din or dout)
+    long D = 0;   // dx (+1 for the ones column)
+    int R = 0;
+    int ns = 1;  // W operand rows per direction: 1 (fp32 modes), 2 (bf16: W_hi, W_lo)
+    long ldY = 0, ldH = 0, ldx = 0;
+    float* YW = nullptr;    // [2R x ldY] fp32: rows [0,R) J = H^T X, rows [R,2R) W (master)
+    void* wop = nullptr;    // bf16 operand copy [W_hi; W_lo] [2R x ldY] (fp32 modes: the W rows of YW)
+    float* hpart = nullptr; // [S x B x ns*R] split-K partials of H = X W^T
+    void* H = nullptr;      // [B x ldH] operand-typed H (bf16: [H | H])
+    float* ohat = nullptr;  // [B] preconditioned ones column (in side)
+    double* rpart = nullptr;  // [nrb x (R+1)]: per-CTA column sums of H, sum of ohat^2
+    double* xpart = nullptr;  // [grid x 2]: per-CTA sums of X^2 and Xhat^2
+    float* gpart = nullptr;   // [S2 x 2R x 2R] Gram partials of [J; W]
+    float* gram = nullptr;    // [2R x 2R]
+    double* st = nullptr;     // d[R], e[R], rho, tr(X X^T), gamma
+    float* M = nullptr;       // [R x 2R]: W' = M [J; W]
+    void* xhat = nullptr;     // [B x ldx] preconditioned vectors (operand dtype)
+    const void* X = nullptr;  // [B x ldx] the layer's vectors (acts[l] or dz[l])
+    GemmPlan hg, xg, jg, gg;
+    int nrb = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ready = nullptr, done = nullptr;
+};
+struct LrLayer {
+    LrSide in, out;
+    float* coef = nullptr;  // gamma_in * gamma_out (device)
+};
+
 struct Profile {
     std::vector<cudaEvent_t> events;
     std::vector<std::string> names;
@@ -153,6 +194,21 @@ struct Replica {
     cudaGraphExec_t graph = nullptr;
     bool use_graph = true;
     long kernels_per_step = 0;
+
+    // NG low-rank (OPT_NG_LOWRANK): per-layer state, the host step counter
+    // that selects the graph variant (init / Fisher-update / plain), one
+    // captured graph per variant
+    LrConfig lrc;
+    std::vector<LrLayer> lrl;
+    long lr_t = 0;
+    int variant = 0;  // bit 0: init, bit 1: J (start an update), bit 2: apply the pending update
+    std::vector<cudaGraphExec_t> vgraphs;
+    std::vector<long> vnodes;
+    std::vector<cudaEvent_t> ev_act;  // acts[l] ready (in-side chains start)
+    cudaEvent_t ev_t0 = nullptr;
+    int lr_variant(long t) const;
+    void set_lowrank(const LrConfig& c);
+    void get_lowrank_state(int layer, int side, double* w, double* d, double* rho) const;
 
     Replica(Context* c, const std::vector<long>& dims, int act, Precision p, Optimizer o, long batch,
             long max_steps, double decay, double smoothing);
@@ -210,5 +266,14 @@ void ng_free(Replica& r);
 void ng_build_plans(Replica& r);
 void ng_precondition_layer(Replica& r, int l, cudaStream_t s);
 void ng_apply_update(Replica& r, int l, cudaStream_t s);
+
+// NG low-rank (ng_lowrank.cu)
+void lr_alloc(Replica& r);
+void lr_free(Replica& r);
+void lr_build_plans(Replica& r);
+void lr_precondition_side(Replica& r, LrSide& sd, cudaStream_t s);  // H, Xhat, gamma
+void lr_start_update(Replica& r, LrSide& sd, cudaStream_t s);       // J = H^T X
+void lr_apply_update(Replica& r, LrSide& sd, cudaStream_t s);       // Gram, eig, W'
+void lr_layer_update(Replica& r, int l, cudaStream_t s);            // bias + dW with gamma
 
 }  // namespace pnb

@@ -46,8 +46,13 @@ void train(Context* ctx, Comm* comm, const TrainConfig& cfg, const std::vector<l
     std::vector<host::Rng> rngs;
     for (uint64_t i = 0; i < local; ++i) {
         owned.emplace_back(new Replica(ctx, dims, cfg.activation, static_cast<Precision>(cfg.precision),
-                                       cfg.optimizer ? OPT_NG_KRON : OPT_SGD, static_cast<long>(B),
+                                       static_cast<Optimizer>(cfg.optimizer), static_cast<long>(B),
                                        static_cast<long>(std::max<uint64_t>(nb, 1)), cfg.ng_decay, cfg.ng_smoothing));
+        if (cfg.optimizer == OPT_NG_LOWRANK) {
+            LrConfig lc = cfg.lr;
+            lc.alpha = cfg.ng_smoothing;
+            owned.back()->set_lowrank(lc);
+        }
         reps.push_back(owned.back().get());
         reps.back()->set_params(params0);
         reps.back()->bind(train_ds);

@@ -43,7 +43,8 @@ class Activation(enum.IntEnum):
 
 class OptimizerKind(enum.IntEnum):
     sgd = 0
-    ngsgd = 1
+    ngsgd = 1          # the reference's kron-full NG-SGD (optimizer.cpp:44-157)
+    ngsgd_lowrank = 2  # online low-rank NG-SGD (north star; not in the reference)
 
 
 class LrVariant(enum.IntEnum):
@@ -98,6 +99,11 @@ class TrainOptions:
     ng_decay: float = 0.95
     ng_smoothing: float = 4.0
     precision: Precision = Precision.bf16  # B200 knob; bf16 operands + fp32 accumulation
+    # low-rank NG-SGD knobs (optimizer ngsgd_lowrank; alpha = ng_smoothing)
+    ng_rank_in: int = 20
+    ng_rank_out: int = 80
+    ng_update_period: int = 4
+    ng_history: float = 2000.0
 
 
 @dataclass
@@ -220,6 +226,17 @@ def newbob_sequence(lr_init: float, accs) -> tuple[np.ndarray, np.ndarray]:
     lr = np.zeros(max(len(a) - 1, 1)); st = np.zeros(max(len(a) - 1, 1), np.int32)
     check(lib().parnn_newbob_sequence(lr_init, ptr(a), len(a), ptr(lr), ptr(st)))
     return lr[:len(a) - 1], st[:len(a) - 1].astype(bool)
+
+
+def lowrank_basis(dim: int, rank: int, seed: int) -> np.ndarray:
+    """Initial orthonormal basis of the low-rank NG state (host, fp64)."""
+    out = np.zeros((rank, dim))
+    check(lib().parnn_lowrank_basis(dim, rank, seed, ptr(out)))
+    return out
+
+
+def lowrank_seed(layer: int, side: int) -> int:
+    return int(lib().parnn_lowrank_seed(layer, side))
 
 
 def scale_lr_for_workers(lr_init: float, workers: int) -> float:
@@ -349,6 +366,26 @@ class Replica:
         flat = f64(np.concatenate([np.concatenate([ri.ravel(), ro.ravel()]) for ri, ro in factors]))
         check(lib().parnn_replica_set_ng_state(self.h, ptr(flat), flat.size, update_count))
 
+    def set_lowrank(self, rank_in: int = 20, rank_out: int = 80, update_period: int = 4, init_iters: int = 3,
+                    num_samples_history: float = 2000.0):
+        check(lib().parnn_replica_set_lowrank(self.h, rank_in, rank_out, update_period, init_iters,
+                                              num_samples_history))
+
+    def lowrank_state(self, layer: int, side: int):
+        """(W = E^1/2 R, d, rho) of one side (0 = in [A_prev | 1], 1 = out dz)."""
+        rank, dim = C.c_uint64(), C.c_uint64()
+        check(lib().parnn_replica_lowrank_state(self.h, layer, side, None, None, None, C.byref(rank), C.byref(dim)))
+        w = np.zeros((rank.value, dim.value))
+        d = np.zeros(rank.value)
+        rho = C.c_double()
+        check(lib().parnn_replica_lowrank_state(self.h, layer, side, ptr(w), ptr(d), C.byref(rho), None, None))
+        return w, d, rho.value
+
+    def lowrank_diag(self, layer: int, side: int) -> dict:
+        out = np.zeros(4)
+        check(lib().parnn_replica_lowrank_diag(self.h, layer, side, ptr(out)))
+        return {"trxx": out[0], "gamma": out[1], "sweeps": int(out[2]), "jacobi_cycles": out[3]}
+
     def bind(self, ds: DeviceDataset):
         check(lib().parnn_replica_bind(self.h, ds.h))
         self.bound = ds
@@ -460,7 +497,8 @@ def _train(plan: ParallelPlan, model0: MlpModel, train: Dataset, cv: Dataset, op
     cvd = DeviceDataset(ctx, cv) if cv is not None and cv.size() > 0 else None
     cfg = TrainConfig(plan.workers, plan.avg_frequency, plan.minibatch, plan.base_seed, int(opts.optimizer),
                       int(opts.lr_schedule), opts.lr_init, opts.epochs, opts.ng_decay, opts.ng_smoothing,
-                      int(opts.precision), int(model0.activation), rank0, local_workers, int(serial))
+                      int(opts.precision), int(model0.activation), rank0, local_workers, int(serial),
+                      opts.ng_rank_in, opts.ng_rank_out, opts.ng_update_period, opts.ng_history)
     d = u64(model0.layer_dims)
     out = np.zeros(param_count(model0.layer_dims))
     met = np.zeros((max(opts.epochs, 1), 7))
