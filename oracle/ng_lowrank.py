@@ -120,24 +120,20 @@ def precondition(st: Side, x):
     return h, xh, gamma, trxx
 
 
-def update(st: Side, x, h, trxx: float, eta: float, alpha: float) -> None:
-    n = x.shape[0]
-    D, R = st.dim, st.rank
-    j = h.T @ x
-    K = j @ j.T
-    L = st.W @ j.T
-    G = st.W @ st.W.T
-    dr = st.d + st.rho
-    a = eta / n
+def eig_update(d, e, rho, K, L, G, trxx, D, eta, a, alpha):
+    """The R x R part of the subspace update: (d', rho', e', M) with
+    W' = M [J; W] = [M1 | M2] [J; W] (ng_lowrank.cu lr_eig_kernel)."""
+    R = d.shape[0]
+    dr = d + rho
     zi = a * a * K + a * (1.0 - eta) * (L * dr[None, :] + dr[:, None] * L) \
         + (1.0 - eta) ** 2 * (dr[:, None] * G * dr[None, :])
-    ih = 1.0 / np.sqrt(st.e)
+    ih = 1.0 / np.sqrt(e)
     z = ih[:, None] * zi * ih[None, :]
     z = 0.5 * (z + z.T)
     lam, u = np.linalg.eigh(z)
     order = np.argsort(-lam, kind="stable")
     lam, u = lam[order], u[:, order]
-    trt = a * trxx + (1.0 - eta) * (D * st.rho + float(st.d.sum()))
+    trt = a * trxx + (1.0 - eta) * (D * rho + float(d.sum()))
     c = np.sqrt(np.maximum(lam, 0.0))
     floor = max(DELTA * float(c.max()), EPS * trt / D, TINY)  # scale-relative floors
     c = np.maximum(c, floor)
@@ -145,7 +141,16 @@ def update(st: Side, x, h, trxx: float, eta: float, alpha: float) -> None:
     d1 = np.maximum(c - rho1, floor)
     e1 = e_of(d1, rho1, D, alpha)
     m = (np.sqrt(e1) / c)[:, None] * u.T * ih[None, :]
-    st.W = m @ (a * j + (1.0 - eta) * dr[:, None] * st.W)
+    return d1, rho1, e1, np.concatenate([a * m, (1.0 - eta) * m * dr[None, :]], axis=1)
+
+
+def update(st: Side, x, h, trxx: float, eta: float, alpha: float) -> None:
+    n = x.shape[0]
+    j = h.T @ x
+    a = eta / n
+    d1, rho1, e1, m = eig_update(st.d, st.e, st.rho, j @ j.T, st.W @ j.T, st.W @ st.W.T, trxx, st.dim, eta, a,
+                                 alpha)
+    st.W = m @ np.concatenate([j, st.W], axis=0)
     st.d, st.rho, st.e = d1, rho1, e1
 
 

@@ -52,6 +52,7 @@ SIGNATURES = [
     ("parnn_save_model", c_int, [C.c_char_p, vp, c_int, c_int, vp]),
     ("parnn_load_model", c_int, [C.c_char_p, vp, vp, vp, vp, c_u64]),
     ("parnn_lowrank_basis", c_int, [c_u64, c_u64, c_u64, vp]),
+    ("parnn_debug_lowrank_eig", c_int, [c_int, c_u64, c_f64, c_f64, c_f64, vp, vp, vp, vp, vp]),
     ("parnn_lowrank_seed", c_u64, [c_int, c_int]),
     ("parnn_allreduce_average_host", c_int, [vp, c_u64, c_u64, vp]),
     ("parnn_ctx_create", c_int, [c_int, vp]),

@@ -282,6 +282,14 @@ int parnn_replica_lowrank_diag(parnn_replica* r, int layer, int side, double out
     });
 }
 
+int parnn_debug_lowrank_eig(int rank, uint64_t dim, double eta, double a, double alpha, const double* state_in,
+                            const float* gram, double* state_out, float* m_out, int* sweeps) {
+    return guarded([&] {
+        if (rank < 1 || rank > LR_MAX_RANK) throw std::runtime_error("ng lowrank: bad rank");
+        lr_debug_eig(rank, static_cast<long>(dim), eta, a, alpha, state_in, gram, state_out, m_out, sweeps);
+    });
+}
+
 int parnn_lowrank_basis(uint64_t dim, uint64_t rank, uint64_t seed, double* out) {
     return guarded([&] {
         const std::vector<double> b = host::lowrank_basis(dim, rank, seed);

@@ -254,23 +254,28 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
         }
         Bc[j * ldb + i] = z;
     }
+    __syncthreads();
     // One group of 8 lanes per column pair, every pair of a round concurrently
     // (launched with 8 * n/2 threads); each lane keeps its <= 12 rows of both
     // columns in registers between the dot products and the rotation.
-    constexpr int kRows = (LR_MAX_RANK + 7) / 8;
-    const int grp = t >> 3, gl = t & 7;
-    const int ngrp = blockDim.x >> 3;
+    constexpr int kLanes = 8;  // lanes per column pair; 4 pairs per warp
+    constexpr int kRows = (LR_MAX_RANK + kLanes - 1) / kLanes;
+    const int wid = t >> 5, nwarp = blockDim.x >> 5;
+    const int gl = t & (kLanes - 1);
     int sweep = 0;
     const long long clk0 = clock64();
     for (; sweep < max_sweeps; ++sweep) {
         int rot = 0;
         for (int k = 0; k < n - 1; ++k) {
-            for (int pr = grp; pr < h; pr += ngrp) {  // whole warps stay converged: h % 4 == 0 or tail groups idle
-                int p, q;
+            // warp-uniform trip count: every lane executes the full-mask shuffles
+            // (per-group masks inside one converged warp give wrong sums)
+            for (int base = wid * 4; base < h; base += nwarp * 4) {
+                const int pr = base + ((t & 31) >> 3);
+                const bool active = pr < h;
+                int p = 0, q = 1;
                 if (pr == 0) {
-                    p = 0;
                     q = (k % (n - 1)) + 1;
-                } else {
+                } else if (active) {
                     p = ((pr + k) % (n - 1)) + 1;
                     q = ((n - 1 - pr + k) % (n - 1)) + 1;
                 }
@@ -280,21 +285,20 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
                 double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
                 for (int i = 0; i < kRows; ++i) {
-                    const int r = gl + 8 * i;
-                    x[i] = r < n ? cp[r] : 0.0;
-                    y[i] = r < n ? cq[r] : 0.0;
+                    const int r = gl + kLanes * i;
+                    x[i] = (active && r < n) ? cp[r] : 0.0;
+                    y[i] = (active && r < n) ? cq[r] : 0.0;
                     al = fma(x[i], x[i], al);
                     be = fma(y[i], y[i], be);
                     ga = fma(x[i], y[i], ga);
                 }
-                const unsigned gmask = 0xFFu << (t & 24);
 #pragma unroll
-                for (int o = 4; o; o >>= 1) {
-                    al += __shfl_xor_sync(gmask, al, o, 8);
-                    be += __shfl_xor_sync(gmask, be, o, 8);
-                    ga += __shfl_xor_sync(gmask, ga, o, 8);
+                for (int o = kLanes / 2; o; o >>= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o, kLanes);
+                    be += __shfl_xor_sync(0xffffffffu, be, o, kLanes);
+                    ga += __shfl_xor_sync(0xffffffffu, ga, o, kLanes);
                 }
-                if (ga * ga > 1e-24 * al * be) {  // |a_p.a_q| > 1e-12 |a_p||a_q|
+                if (active && ga * ga > 1e-24 * al * be) {  // |a_p.a_q| > 1e-12 |a_p||a_q|
                     // angle in fp32 (the residual is removed by the next sweep); the rotation
                     // itself exactly orthogonal in fp64 (c refined by two Newton steps)
                     const float zeta = static_cast<float>((be - al) / (2.0 * ga));
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
                     const double sn = c * tt;
 #pragma unroll
                     for (int i = 0; i < kRows; ++i) {
-                        const int r = gl + 8 * i;
+                        const int r = gl + kLanes * i;
                         if (r < n) {
                             cp[r] = c * x[i] - sn * y[i];
                             cq[r] = sn * x[i] + c * y[i];
@@ -580,6 +584,31 @@ void side_plans(Replica& r, LrSide& sd, const void* X) {
 }
 
 }  // namespace
+
+// Test hook: one subspace-update eigensolve on a given Gram of [J; W] and
+// state (d, e, rho, tr(XX^T)); returns the new state and M.
+void lr_debug_eig(int R, long D, double eta, double a, double alpha, const double* st_in, const float* gram,
+                  double* st_out, float* m_out, int* sweeps) {
+    const size_t ns = 2 * R + 8;
+    double* dst = dalloc_d(ns);
+    float* dg = falloc(4L * R * R);
+    float* dm = falloc(2L * R * R);
+    CUDA_THROW(cudaMemcpy(dst, st_in, ns * 8, cudaMemcpyHostToDevice));
+    CUDA_THROW(cudaMemcpy(dg, gram, 16L * R * R, cudaMemcpyHostToDevice));
+    CUDA_THROW(cudaFuncSetAttribute(lr_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(eig_smem(LR_MAX_RANK))));
+    const int npair = ((R + 1) & ~1) / 2;
+    const int threads = std::max(128, (npair * 8 + 31) / 32 * 32);
+    lr_eig_kernel<<<1, threads, eig_smem(R)>>>(dst, dg, R, D, eta, a, alpha, dm, 40);
+    CUDA_THROW(cudaGetLastError());
+    CUDA_THROW(cudaDeviceSynchronize());
+    CUDA_THROW(cudaMemcpy(st_out, dst, ns * 8, cudaMemcpyDeviceToHost));
+    CUDA_THROW(cudaMemcpy(m_out, dm, 8L * R * R, cudaMemcpyDeviceToHost));
+    *sweeps = static_cast<int>(st_out[2 * R + 3]);
+    cudaFree(dst);
+    cudaFree(dg);
+    cudaFree(dm);
+}
 
 void lr_alloc(Replica& r) {
     r.lrl.resize(r.L);

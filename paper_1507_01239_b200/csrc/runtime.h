@@ -275,5 +275,7 @@ void lr_precondition_side(Replica& r, LrSide& sd, cudaStream_t s);  // H, Xhat, 
 void lr_start_update(Replica& r, LrSide& sd, cudaStream_t s);       // J = H^T X
 void lr_apply_update(Replica& r, LrSide& sd, cudaStream_t s);       // Gram, eig, W'
 void lr_layer_update(Replica& r, int l, cudaStream_t s);            // bias + dW with gamma
+void lr_debug_eig(int R, long D, double eta, double a, double alpha, const double* st_in, const float* gram,
+                  double* st_out, float* m_out, int* sweeps);
 
 }  // namespace pnb

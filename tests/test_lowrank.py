@@ -210,3 +210,49 @@ def test_lowrank_config2_shape_steps(ctx, prec):
     assert np.all(np.isfinite(ce)) and ce[-1] < ce[0]
     assert np.all(np.isfinite(r.get_params()))
     assert r.kernels_per_step() > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["isotropic", "mean_dominated", "decaying"])
+@pytest.mark.parametrize("R", [20, 80])
+def test_lowrank_eig_kernel_matches_oracle(kind, R):
+    """The device eigensolver of the subspace update (one-sided Jacobi) against
+    numpy eigh on the same Gram: new d, rho exactly (1e-6) and the updated
+    basis W' = M [J; W] up to row signs (W'^T W')."""
+    import ctypes as C
+    from paper_1507_01239_b200 import parnn as P
+    from paper_1507_01239_b200._lib import check, lib, ptr
+    rng = np.random.default_rng(R)
+    D, N = 2048, 1024
+    if kind == "isotropic":
+        x = rng.standard_normal((N, D)) * 1e-2
+    elif kind == "mean_dominated":
+        x = 1 / (1 + np.exp(-(rng.standard_normal((N, D)) * 1.5 + rng.standard_normal(D))))
+    else:
+        x = rng.standard_normal((N, D)) * (1.0 / (1 + np.arange(D)) ** 0.7)
+    st = LR.side_init(D, R, 5, 4.0)
+    cfg = LR.LowRankConfig(rank_in=R, update_period=1)
+    eta = LR.eta_of(N, cfg)
+    for _ in range(2):  # move away from the cold start
+        h, _, _, trxx = LR.precondition(st, x)
+        LR.update(st, x, h, trxx, eta, 4.0)
+    h, _, _, trxx = LR.precondition(st, x)
+    j = h.T @ x
+    Y = np.concatenate([j, st.W], axis=0).astype(np.float32)
+    gram = (Y.astype(np.float64) @ Y.astype(np.float64).T).astype(np.float32)
+    a = eta / N
+    d1, rho1, e1, m = LR.eig_update(st.d, st.e, st.rho, gram[:R, :R].astype(np.float64),
+                                    gram[R:, :R].astype(np.float64), gram[R:, R:].astype(np.float64), trxx, D, eta,
+                                    a, 4.0)
+    sin = np.zeros(2 * R + 8)
+    sin[:R], sin[R:2 * R], sin[2 * R], sin[2 * R + 1] = st.d, st.e, st.rho, trxx
+    sout = np.zeros(2 * R + 8)
+    mg = np.zeros((R, 2 * R), np.float32)
+    sw = C.c_int()
+    g32 = np.ascontiguousarray(gram, np.float32)
+    check(lib().parnn_debug_lowrank_eig(R, D, eta, a, 4.0, ptr(sin), ptr(g32), ptr(sout), ptr(mg), C.byref(sw)))
+    assert 0 < sw.value < 40
+    assert rel(sout[:R], d1) < 1e-5 and abs(sout[2 * R] - rho1) / rho1 < 1e-5
+    w_ref = m @ Y.astype(np.float64)
+    w_gpu = mg.astype(np.float64) @ Y.astype(np.float64)
+    assert rel(w_gpu.T @ w_gpu, w_ref.T @ w_ref) < 1e-4
