@@ -135,6 +135,9 @@ int parnn_replica_step(parnn_replica* r, uint64_t steps);
 int parnn_replica_sync(parnn_replica* r);
 /* Per-step batch CE (cross_entropy, network.cpp:145-160) of the current epoch. */
 int parnn_replica_ce(parnn_replica* r, double* out, uint64_t steps);
+/* Batch CE of step `step` of the current epoch, waiting only for that step
+ * (later steps may still run): the pipelined per-step loss readback. */
+int parnn_replica_step_ce(parnn_replica* r, uint64_t step, double* out);
 /* forward (network.cpp:119-143): last-layer pre-activations for given rows. */
 int parnn_replica_forward(parnn_replica* r, parnn_dataset* ds, const uint32_t* rows, uint64_t b, float* z_out);
 /* accuracy (network.cpp:274-289) on a whole dataset */

@@ -74,6 +74,7 @@ SIGNATURES = [
     ("parnn_replica_step", c_int, [vp, c_u64]),
     ("parnn_replica_sync", c_int, [vp]),
     ("parnn_replica_ce", c_int, [vp, vp, c_u64]),
+    ("parnn_replica_step_ce", c_int, [vp, c_u64, vp]),
     ("parnn_replica_forward", c_int, [vp, vp, vp, c_u64, vp]),
     ("parnn_replica_accuracy", c_int, [vp, vp, vp]),
     ("parnn_replica_kernels_per_step", c_int, [vp, vp]),

@@ -368,6 +368,10 @@ int parnn_replica_ce(parnn_replica* r, double* out, uint64_t steps) {
     });
 }
 
+int parnn_replica_step_ce(parnn_replica* r, uint64_t step, double* out) {
+    return guarded([&] { *out = r->r->step_ce(static_cast<long>(step)); });
+}
+
 int parnn_replica_forward(parnn_replica* r, parnn_dataset* ds, const uint32_t* rows, uint64_t b, float* z) {
     return guarded([&] {
         if (!r->r->bound) r->r->bind(ds->d.get());

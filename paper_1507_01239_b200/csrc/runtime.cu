@@ -78,6 +78,7 @@ DeviceDataset::DeviceDataset(Context* c, const double* x, const int32_t* labels,
 }
 
 DeviceDataset::~DeviceDataset() {
+    if (written) cudaEventDestroy(written);
     dfree(x32);
     dfree(x16);
     dfree(y);
@@ -98,6 +99,8 @@ void DeviceDataset::write_rows(const float* x, const int32_t* labels, long row0,
     CUDA_THROW(cudaMemcpy2DAsync(x32 + row0 * ld, ld * 4, x, d * 4, d * 4, cnt, cudaMemcpyHostToDevice, s));
     if (labels) CUDA_THROW(cudaMemcpyAsync(y + row0, labels, cnt * 4, cudaMemcpyHostToDevice, s));
     if (x16) launch_f32_to_bf16_rows(x32 + row0 * ld, ld, cnt, ld, x16 + row0 * ld, s);
+    if (!written) CUDA_THROW(cudaEventCreateWithFlags(&written, cudaEventDisableTiming));
+    CUDA_THROW(cudaEventRecord(written, s));
 }
 
 Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision p, Optimizer o, long batch,
@@ -169,6 +172,7 @@ Replica::~Replica() {
         if (g) cudaGraphExecDestroy(g);
     lr_free(*this);
     for (auto e : ev_act) cudaEventDestroy(e);
+    for (auto e : step_ev) cudaEventDestroy(e);
     if (ev_t0) cudaEventDestroy(ev_t0);
     dfree(params);
     dfree(wshadow);
@@ -659,15 +663,18 @@ void Replica::profile_steps(long steps, std::vector<std::string>& names, std::ve
         }
         prof = nullptr;
         CUDA_THROW(cudaStreamSynchronize(stream));
+        // accumulate by region name: step kinds (low-rank init / update / plain) differ in regions
         for (size_t i = 1; i < p.events.size(); ++i) {
             float t = 0.f;
             CUDA_THROW(cudaEventElapsedTime(&t, p.events[i - 1], p.events[i]));
-            if (it == 0) {
+            size_t k = 0;
+            while (k < names.size() && names[k] != p.names[i]) ++k;
+            if (k == names.size()) {
                 names.push_back(p.names[i]);
                 ms.push_back(0.0);
                 flops.push_back(p.flops[i]);
             }
-            ms[i - 1] += t / static_cast<double>(steps);
+            ms[k] += t / static_cast<double>(steps);
         }
         for (auto e : p.events) cudaEventDestroy(e);
     }
@@ -694,10 +701,32 @@ void Replica::upload_epoch(const uint32_t* rows, const float* lrs, long steps) {
     CUDA_THROW(cudaMemcpyAsync(d_rows, rows, steps * B * 4, cudaMemcpyHostToDevice, s));
     CUDA_THROW(cudaMemcpyAsync(d_lr, lrs, steps * 4, cudaMemcpyHostToDevice, s));
     CUDA_THROW(cudaMemsetAsync(d_step, 0, 4, s));
+    epoch_steps = 0;
+}
+
+double Replica::step_ce(long j) {
+    if (j < 0 || j >= epoch_steps) throw std::runtime_error("replica: step " + std::to_string(j) + " not launched");
+    if (epoch_steps - j > kStepRing)
+        CUDA_THROW(cudaStreamSynchronize(stream));  // its event slot was reused
+    else
+        CUDA_THROW(cudaEventSynchronize(step_ev[j % kStepRing]));
+    double v = 0.0;
+    CUDA_THROW(cudaMemcpy(&v, d_ce + j, sizeof(double), cudaMemcpyDeviceToHost));
+    return v;
 }
 
 void Replica::run_step(cudaStream_t s) {
     if (!bound) throw std::runtime_error("replica: no dataset bound");
+    if (bound->written) CUDA_THROW(cudaStreamWaitEvent(s, bound->written, 0));  // inputs written by the host
+    if (step_ev.empty()) {
+        step_ev.resize(kStepRing);
+        for (auto& e : step_ev) CUDA_THROW(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    struct Rec {
+        Replica* r;
+        cudaStream_t s;
+        ~Rec() { cudaEventRecord(r->step_ev[r->epoch_steps++ % kStepRing], s); }
+    } rec{this, s};
     if (opt == OPT_NG_LOWRANK) {
         variant = lr_variant(lr_t);
         static const char* force = std::getenv("PARNN_LR_FORCE_VARIANT");  // timing aid: 0 plain, 2 J, 4 apply

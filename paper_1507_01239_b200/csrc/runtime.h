@@ -58,6 +58,7 @@ struct DeviceDataset {
     float* x32 = nullptr;  // [n x ld] fp32 (zero padded)
     bf16* x16 = nullptr;   // [n x ld] bf16 copy, created on first bf16 use
     int32_t* y = nullptr;
+    cudaEvent_t written = nullptr;  // last write_rows; steps of replicas bound here wait on it
     DeviceDataset(Context* c, const double* x, const int32_t* labels, long n, long d, long classes);
     ~DeviceDataset();
     const void* features(Precision p);
@@ -223,6 +224,12 @@ struct Replica {
 
     void bind(DeviceDataset* ds);  // build GEMM plans + graph for this dataset
     void upload_epoch(const uint32_t* rows, const float* lrs, long steps);
+    // per-step completion events (ring): the loss of step j of the epoch can be
+    // read while later steps run (pipelined end-to-end loop)
+    static constexpr int kStepRing = 64;
+    std::vector<cudaEvent_t> step_ev;
+    long epoch_steps = 0;  // steps launched since upload_epoch
+    double step_ce(long j);
     void run_step(cudaStream_t s);  // one minibatch (graph or eager)
     void enqueue_step(cudaStream_t s);
     void sync_shadow(cudaStream_t s);  // recompute bf16 copy after external param writes

@@ -406,6 +406,12 @@ class Replica:
         check(lib().parnn_replica_ce(self.h, ptr(out), steps))
         return out
 
+    def step_ce(self, step: int) -> float:
+        """CE of one step of the epoch; waits for that step only."""
+        out = C.c_double()
+        check(lib().parnn_replica_step_ce(self.h, step, C.byref(out)))
+        return out.value
+
     def forward(self, ds: DeviceDataset, rows) -> np.ndarray:
         r = np.ascontiguousarray(rows, np.uint32)
         z = np.zeros((r.size, self.dims[-1]), np.float32)

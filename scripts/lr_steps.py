@@ -40,3 +40,7 @@ else:
     r.step(a.steps)
     r.sync()
 print("ce", r.ce(a.warmup + (40 if a.time else a.steps))[-3:])
+if os.environ.get("LR_PROFILE"):
+    for rep in range(2):
+        prof = r.profile(2)
+        print("profile", rep, [(n, round(t, 4)) for n, t, f in prof][:12])
