@@ -119,7 +119,7 @@ int parnn_replica_lowrank_state(parnn_replica* r, int layer, int side, double* w
 int parnn_replica_lowrank_diag(parnn_replica* r, int layer, int side, double out[4]);
 /* Test hook: one low-rank subspace-update eigensolve (the device kernel of
  * the update) on a given Gram of [J; W] (2R x 2R fp32) and state
- * {d[R], e[R], rho, tr(XX^T), ...} (2R+8 doubles); returns the new state
+ * {d[R], e[R], rho, tr(XX^T), ...} (2R+12 doubles); returns the new state
  * and M (R x 2R, W' = M [J; W]). */
 int parnn_debug_lowrank_eig(int rank, uint64_t dim, double eta, double a, double alpha, const double* state_in,
                             const float* gram, double* state_out, float* m_out, int* sweeps);

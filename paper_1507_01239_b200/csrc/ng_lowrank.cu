@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
     extern __shared__ double sh[];
     const int n = (R + 1) & ~1;
     const int h = n / 2;
-    const int ldb = n + ((24 - (n & 15)) & 15);  // ldb = 8 (mod 16): column parity alternates banks
+    const int ldb = (n + 15) & ~15;  // 128-B aligned columns; rows [n, ldb) are zero
     double* dr = sh;            // [n]
     double* ih = dr + n;        // [n]
     double* sig = ih + n;       // [n] column norms (eigenvalues)
@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
     }
     __syncthreads();
     const double ce = a * (1.0 - eta), cg = (1.0 - eta) * (1.0 - eta), ck = a * a;
-    for (int idx = t; idx < n * n; idx += blockDim.x) {
-        const int i = idx % n, j = idx / n;  // row i of column j
+    for (int idx = t; idx < n * ldb; idx += blockDim.x) {
+        const int i = idx % ldb, j = idx / ldb;  // row i of column j
         double z = 0.0;
         if (i < R && j < R) {
             const double kij = gram[i * R2 + j], kji = gram[j * R2 + i];
@@ -259,16 +259,31 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
     // (launched with 8 * n/2 threads); each lane keeps its <= 12 rows of both
     // columns in registers between the dot products and the rotation.
     constexpr int kLanes = 8;  // lanes per column pair; 4 pairs per warp
-    constexpr int kRows = (LR_MAX_RANK + kLanes - 1) / kLanes;
+    constexpr int kRows = ((LR_MAX_RANK + 15) & ~15) / kLanes;
     const int wid = t >> 5, nwarp = blockDim.x >> 5;
     const int gl = t & (kLanes - 1);
+    const int nchunk = ldb / kLanes;  // row chunks of 8 (64 B) per column
+    // odd groups start one chunk later: the two groups of a half-warp then hit
+    // opposite 64-B halves of the bank space whatever their columns (conflict-free)
+    const int cshift = (t >> 3) & 1;
     int sweep = 0;
     const long long clk0 = clock64();
+    long long ph[5] = {0, 0, 0, 0, 0};  // PNB_EIG_PHASES: load+dot, reduce, angle, rotate, barrier
     for (; sweep < max_sweeps; ++sweep) {
+        // exact column norms once per sweep; within the sweep they are carried
+        // through the rotations (|x'|^2 = c^2 a - 2cs g + s^2 b), so a pair needs one
+        // dot product (a_p . a_q) instead of three
+        for (int c = t; c < n; c += blockDim.x) {
+            double s2 = 0.0;
+            for (int r = 0; r < n; ++r) s2 = fma(Bc[c * ldb + r], Bc[c * ldb + r], s2);
+            sig[c] = s2;
+        }
+        __syncthreads();
         int rot = 0;
         for (int k = 0; k < n - 1; ++k) {
             // warp-uniform trip count: every lane executes the full-mask shuffles
             // (per-group masks inside one converged warp give wrong sums)
+            long long q0 = clock64();
             for (int base = wid * 4; base < h; base += nwarp * 4) {
                 const int pr = base + ((t & 31) >> 3);
                 const bool active = pr < h;
@@ -282,46 +297,74 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
                 double* cp = Bc + p * ldb;
                 double* cq = Bc + q * ldb;
                 double x[kRows], y[kRows];
-                double al = 0.0, be = 0.0, ga = 0.0;
+                double ga = 0.0, gb = 0.0;
 #pragma unroll
                 for (int i = 0; i < kRows; ++i) {
-                    const int r = gl + kLanes * i;
-                    x[i] = (active && r < n) ? cp[r] : 0.0;
-                    y[i] = (active && r < n) ? cq[r] : 0.0;
-                    al = fma(x[i], x[i], al);
-                    be = fma(y[i], y[i], be);
-                    ga = fma(x[i], y[i], ga);
+                    int ch = i + cshift;
+                    ch = ch >= nchunk ? ch - nchunk : ch;
+                    const int r = gl + kLanes * ch;
+                    x[i] = (active && i < nchunk) ? cp[r] : 0.0;
+                    y[i] = (active && i < nchunk) ? cq[r] : 0.0;
+                    if (i & 1)
+                        gb = fma(x[i], y[i], gb);
+                    else
+                        ga = fma(x[i], y[i], ga);
                 }
+                ga += gb;
+                long long q1 = clock64();
+                ph[0] += q1 - q0;
 #pragma unroll
-                for (int o = kLanes / 2; o; o >>= 1) {
-                    al += __shfl_xor_sync(0xffffffffu, al, o, kLanes);
-                    be += __shfl_xor_sync(0xffffffffu, be, o, kLanes);
-                    ga += __shfl_xor_sync(0xffffffffu, ga, o, kLanes);
-                }
+                for (int o = kLanes / 2; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o, kLanes);
+                const double al = active ? sig[p] : 0.0, be = active ? sig[q] : 0.0;
+                long long q2 = clock64();
+                ph[1] += q2 - q1;
+                q0 = q2;
                 if (active && ga * ga > 1e-24 * al * be) {  // |a_p.a_q| > 1e-12 |a_p||a_q|
                     // angle in fp32 (the residual is removed by the next sweep); the rotation
                     // itself exactly orthogonal in fp64 (c refined by two Newton steps)
-                    const float zeta = static_cast<float>((be - al) / (2.0 * ga));
+                    // zeta = (b - a) / 2g in fp32 after removing g's binary exponent (exact
+                    // power-of-two scale built from the exponent bits: no ilogb/ldexp calls)
+                    const long long gbits = __double_as_longlong(ga);
+                    const int ex = static_cast<int>((gbits >> 52) & 0x7FF);  // biased; g != 0 here
+                    const double sc = __longlong_as_double(static_cast<long long>(2046 - ex) << 52);  // 2^(1023-ex)
+                    const float zeta = __fdividef(static_cast<float>((be - al) * sc), 2.f * static_cast<float>(ga * sc));
                     const float az = fabsf(zeta);
-                    const float tf = az > 1e18f ? 0.5f / az : 1.f / (az + sqrtf(fmaf(az, az, 1.f)));
+                    const float v = fmaf(az, az, 1.f);
+                    // approximate fp32 is enough for the angle (MUFU rsqrt/rcp)
+                    const float tf = az > 1e18f ? __fdividef(0.5f, az) : __fdividef(1.f, az + v * rsqrtf(v));
                     const double tt = zeta >= 0.f ? static_cast<double>(tf) : -static_cast<double>(tf);
                     const double w = fma(tt, tt, 1.0);
                     double c = static_cast<double>(rsqrtf(static_cast<float>(w)));
                     c = c * (1.5 - 0.5 * w * c * c);
                     c = c * (1.5 - 0.5 * w * c * c);
                     const double sn = c * tt;
+                    long long q3 = clock64();
+                    ph[2] += q3 - q0;
+                    q0 = q3;
 #pragma unroll
                     for (int i = 0; i < kRows; ++i) {
-                        const int r = gl + kLanes * i;
-                        if (r < n) {
+                        int ch = i + cshift;
+                        ch = ch >= nchunk ? ch - nchunk : ch;
+                        const int r = gl + kLanes * ch;
+                        if (i < nchunk) {
                             cp[r] = c * x[i] - sn * y[i];
                             cq[r] = sn * x[i] + c * y[i];
                         }
                     }
+                    if (gl == 0) {
+                        const double cs2 = 2.0 * c * sn * ga;
+                        sig[p] = fmax(c * c * al - cs2 + sn * sn * be, 0.0);
+                        sig[q] = fmax(sn * sn * al + cs2 + c * c * be, 0.0);
+                    }
                     rot = 1;
+                    long long q4 = clock64();
+                    ph[3] += q4 - q0;
+                    q0 = q4;
                 }
             }
+            long long q5 = clock64();
             __syncthreads();
+            ph[4] += clock64() - q5;
         }
         if (!__syncthreads_or(rot)) break;  // no rotation anywhere in this sweep
     }
@@ -387,12 +430,13 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
         st[2 * R] = misc[0];
         st[2 * R + 3] = sweep;                             // diagnostics: Jacobi sweeps used,
         st[2 * R + 4] = static_cast<double>(clk1 - clk0);  // and their SM cycles
+        for (int i = 0; i < 5; ++i) st[2 * R + 5 + i] = static_cast<double>(ph[i]);  // thread 0's phases
     }
 }
 
 size_t eig_smem(int R) {
     const int n = (R + 1) & ~1;
-    const int ldb = n + ((24 - (n & 15)) & 15);
+    const int ldb = (n + 15) & ~15;
     return (5 * static_cast<size_t>(n) + 8 + static_cast<size_t>(n) * ldb) * sizeof(double) + (n + 4) * sizeof(int);
 }
 
@@ -462,7 +506,7 @@ void side_alloc(Replica& r, LrSide& sd, bool in, long dx, int want_rank, int lay
     sd.rpart = dalloc_d(sd.nrb * (R + 1L));
     sd.xpart = dalloc_d(2 * 1024);
     sd.gram = falloc(4L * R * R);
-    sd.st = dalloc_d(2 * R + 8);
+    sd.st = dalloc_d(2 * R + 12);
     sd.M = falloc(2L * R * R);
     sd.xhat = valloc(B * sd.ldx * es);
     CUDA_THROW(cudaStreamCreateWithFlags(&sd.stream, cudaStreamNonBlocking));
@@ -473,7 +517,7 @@ void side_alloc(Replica& r, LrSide& sd, bool in, long dx, int want_rank, int lay
     const double alpha = r.lrc.alpha;
     const double beta = kEps * (1.0 + alpha) + alpha * (R * kEps) / static_cast<double>(sd.D);
     const double e0 = kEps / (kEps + beta);
-    std::vector<double> sth(2 * R + 8, 0.0);
+    std::vector<double> sth(2 * R + 12, 0.0);
     for (int i = 0; i < R; ++i) {
         sth[i] = kEps;
         sth[R + i] = e0;
@@ -589,7 +633,7 @@ void side_plans(Replica& r, LrSide& sd, const void* X) {
 // state (d, e, rho, tr(XX^T)); returns the new state and M.
 void lr_debug_eig(int R, long D, double eta, double a, double alpha, const double* st_in, const float* gram,
                   double* st_out, float* m_out, int* sweeps) {
-    const size_t ns = 2 * R + 8;
+    const size_t ns = 2 * R + 12;
     double* dst = dalloc_d(ns);
     float* dg = falloc(4L * R * R);
     float* dm = falloc(2L * R * R);

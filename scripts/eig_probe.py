@@ -16,15 +16,18 @@ for R in [20, 40, 64, 66, 72, 80, 96]:
     gram = np.zeros((2 * R, 2 * R), np.float32)
     gram[:R, :R] = K
     D = 4096
-    st = np.zeros(2 * R + 8)
+    st = np.zeros(2 * R + 12)
     st[:R] = 1.0
     st[R:2 * R] = 1.0
     st[2 * R] = 0.0
     st[2 * R + 1] = 1.0
     d1, rho1, e1, m = LR.eig_update(st[:R], st[R:2 * R], 0.0, K.astype(np.float64), np.zeros((R, R)), np.zeros((R, R)),
                                     1.0, D, 1.0, 1.0, 4.0)
-    sout = np.zeros(2 * R + 8)
+    sout = np.zeros(2 * R + 12)
     mg = np.zeros((R, 2 * R), np.float32)
     sw = C.c_int()
     check(lib().parnn_debug_lowrank_eig(R, D, 1.0, 1.0, 4.0, ptr(st), ptr(gram), ptr(sout), ptr(mg), C.byref(sw)))
-    print(R, "sweeps", sw.value, "d rel err", np.abs(sout[:R] - d1).max() / d1.max())
+    ph = sout[2 * R + 5:2 * R + 10]
+    rounds = sw.value * (R - 1)
+    print(R, "sweeps", sw.value, "d rel err", np.abs(sout[:R] - d1).max() / d1.max(), "cycles/round", round(sout[2 * R + 4] / max(rounds, 1)),
+          "phases/round (load+dot, reduce, angle, rotate, barrier)", [round(v / max(rounds, 1)) for v in ph])

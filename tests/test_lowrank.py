@@ -244,9 +244,9 @@ def test_lowrank_eig_kernel_matches_oracle(kind, R):
     d1, rho1, e1, m = LR.eig_update(st.d, st.e, st.rho, gram[:R, :R].astype(np.float64),
                                     gram[R:, :R].astype(np.float64), gram[R:, R:].astype(np.float64), trxx, D, eta,
                                     a, 4.0)
-    sin = np.zeros(2 * R + 8)
+    sin = np.zeros(2 * R + 12)
     sin[:R], sin[R:2 * R], sin[2 * R], sin[2 * R + 1] = st.d, st.e, st.rho, trxx
-    sout = np.zeros(2 * R + 8)
+    sout = np.zeros(2 * R + 12)
     mg = np.zeros((R, 2 * R), np.float32)
     sw = C.c_int()
     g32 = np.ascontiguousarray(gram, np.float32)
