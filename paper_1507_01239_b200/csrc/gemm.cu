@@ -125,7 +125,7 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     else
         p.fn = reinterpret_cast<void*>(pick<__nv_bfloat16, false>(bn, a_mn, b_mn, &p.smem));
     p.bn = bn;
-    p.threads = split ? 320 : 192;  // GemmSmem::kThreads
+    p.threads = split ? 448 : 320;  // GemmSmem::kThreads
 }
 
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {

@@ -26,6 +26,22 @@
 
 namespace pnb {
 
+#ifdef PNB_GEMM_TRACE
+// per-CTA %globaltimer stamps: entry, setup done, first operands in smem,
+// last MMA issued, accumulator ready, epilogue done, exit
+__device__ unsigned long long g_gemm_trace[1024][8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define PNB_TRACE(i) g_gemm_trace[blockIdx.x][i] = gtime()
+#else
+#define PNB_TRACE(i) \
+    do {             \
+    } while (0)
+#endif
+
 enum EpiMode : int {
     EPI_FWD_ACT = 0,     // out(T)   = act(acc + bias[n])
     EPI_FWD_LINEAR = 1,  // out32    = acc + bias[n]
@@ -79,7 +95,9 @@ struct OpTraits<float> {
 };
 
 __device__ __forceinline__ float act_fwd(int act, float z) {
-    return act == 0 ? 1.f / (1.f + expf(-z)) : (act == 1 ? tanhf(z) : z);
+    // sigmoid on the MUFU path (ex2 + approximate reciprocal, ~2 ulp); tanh keeps
+    // the accurate tanhf (its 1 - 2/(1+e^2z) form cancels near 0)
+    return act == 0 ? __fdividef(1.f, 1.f + __expf(-z)) : (act == 1 ? tanhf(z) : z);
 }
 __device__ __forceinline__ float act_grad(int act, float a) {
     return act == 0 ? a * (1.f - a) : 1.f - a * a;
@@ -177,7 +195,7 @@ struct GemmSmem {
     static constexpr int kLoad = kABytes + kBBytes;          // bytes TMA brings per stage
     static constexpr int kStage = kLoad * (SPLIT ? 2 : 1);   // + low-part copies for 3xTF32
     static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 512 /*barriers*/;
-    static constexpr int kThreads = SPLIT ? 320 : 192;       // + 4 splitter warps
+    static constexpr int kThreads = SPLIT ? 448 : 320;       // TMA, MMA, 8 epilogue (+ 4 splitter) warps
     static constexpr uint32_t kTmemCols = 2 * BN;            // double-buffered accumulator
 };
 
@@ -205,15 +223,18 @@ __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, float (&v)[32]
             break;
         }
         case EPI_FWD_ACT: {
+            float b[32];
+            load_row32<float>(ep.bias + n, b, valid);  // 8 vector loads, broadcast across the warp
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                v[j] = ep.out_scale * act_fwd(ep.act, v[j] + (j < valid ? ep.bias[n + j] : 0.f));
+            for (int j = 0; j < 32; ++j) v[j] = ep.out_scale * act_fwd(ep.act, v[j] + b[j]);
             store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
             break;
         }
         case EPI_FWD_LINEAR: {
+            float b[32];
+            load_row32<float>(ep.bias + n, b, valid);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += (j < valid ? ep.bias[n + j] : 0.f);
+            for (int j = 0; j < 32; ++j) v[j] += b[j];
             store_row32<float>(ep.out32 + row * ep.ld_out32 + n, v, valid);
             break;
         }
@@ -289,8 +310,9 @@ __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, float (&v)[32]
 // tiles c, c + grid, ... (m fastest). Roles:
 //   warp 0      TMA producer (one elected lane), STAGES-deep smem ring
 //   warp 1      MMA issuer (one elected lane); owns the TMEM allocation
-//   warps 2-5   epilogue: TMEM lane quadrant (warp % 4) -> registers -> global
-//   warps 6-9   (SPLIT only) 3xTF32 splitters
+//   warps 2-9   epilogue: TMEM lane quadrant (warp % 4) -> registers -> global,
+//               two sets of four splitting the tile's column chunks
+//   warps 10-13 (SPLIT only) 3xTF32 splitters
 // The accumulator is double buffered in TMEM (2 x BN columns), so the
 // epilogue of tile i overlaps the mainloop of tile i+1.
 //
@@ -333,6 +355,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
     };
 
     if (threadIdx.x == 0) {
+        PNB_TRACE(0);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -340,7 +363,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 128);
+            mbar_init(&tempty[i], 256);
         }
         fence_barrier_init();
         tma_prefetch_desc(&tmA);
@@ -351,6 +374,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+    if (threadIdx.x == 0) PNB_TRACE(1);
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
@@ -412,6 +436,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(SPLIT ? &split_done[s] : &full[s], (it / STAGES) & 1);
+                    if (it == 0) PNB_TRACE(2);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + s * S::kStage);
                     const uint32_t sb = sa + S::kABytes;
@@ -427,12 +452,17 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[acc]);
+                PNB_TRACE(3);
                 ++local;
             }
         }
-    } else if (warp < 6) {
-        // ---------------- epilogue (4 warps = 128 TMEM lanes) ----------------
+    } else if (warp < 10) {
+        // ---------------- epilogue (8 warps: 2 sets x 128 TMEM lanes) ----------------
+        // a warp may only touch its TMEM lane quadrant (warp % 4); the two sets
+        // split the tile's 32-column chunks (even / odd), which halves the serial
+        // per-row work of each thread
         const int quad = warp & 3;
+        const int eset = (warp - 2) >> 2;
         float lr = 0.f;
         if (ep.mode == EPI_GRAD_SGD) lr = ep.lr[ep.step ? *ep.step : 0];
         bool bad = false;
@@ -448,7 +478,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
             // Pull this tile's epilogue source rows (weights / activations /
             // factors being read-modify-written) into L2 while the MMAs run:
             // otherwise each 32-column chunk pays a full DRAM round trip.
-            if (row_ok) {
+            if (row_ok && eset == 0) {
                 const char* src = nullptr;
                 long bytes = 0;
                 if (ep.mode == EPI_GRAD_SGD || ep.mode == EPI_EMA || ep.mode == EPI_SUB || ep.mode == EPI_AXPY) {
@@ -461,9 +491,10 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
                 for (long o = 0; o < bytes; o += 128) prefetch_l2(src + o);
             }
             mbar_wait(&tfull[acc], (local >> 1) & 1);
+            if (warp == 2 && lane == 0) PNB_TRACE(4);
             tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = eset; c < BN / 32; c += 2) {
                 const int n = n0 + c * 32;
                 if (n >= N) break;  // warp-uniform
                 uint32_t r[32];
@@ -477,30 +508,36 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
+            if (warp == 2 && lane == 0) PNB_TRACE(5);
             ++local;
         }
         if (bad && ep.flag) atomicOr(ep.flag, 1u << ep.flag_bit);
         if (ep.mode == EPI_RESID) {
             // deterministic per-CTA sums: fixed tile order, fixed reduction tree
-            __shared__ float red[2][4];
+            __shared__ float red[2][8];
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
                 s_aux += __shfl_xor_sync(0xffffffffu, s_aux, o);
                 s_out += __shfl_xor_sync(0xffffffffu, s_out, o);
             }
             if (lane == 0) {
-                red[0][quad] = s_aux;
-                red[1][quad] = s_out;
+                red[0][warp - 2] = s_aux;
+                red[1][warp - 2] = s_out;
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
             if (warp == 2 && lane == 0) {
-                ep.part[2 * blockIdx.x] = (double)red[0][0] + red[0][1] + red[0][2] + red[0][3];
-                ep.part[2 * blockIdx.x + 1] = (double)red[1][0] + red[1][1] + red[1][2] + red[1][3];
+                double a = 0.0, b = 0.0;
+                for (int i = 0; i < 8; ++i) {
+                    a += red[0][i];
+                    b += red[1][i];
+                }
+                ep.part[2 * blockIdx.x] = a;
+                ep.part[2 * blockIdx.x + 1] = b;
             }
         }
     } else if (SPLIT) {
-        // ---------------- 3xTF32 splitters (warps 6-9) ----------------
-        const int t = threadIdx.x - 192;
+        // ---------------- 3xTF32 splitters (warps 10-13) ----------------
+        const int t = threadIdx.x - 320;
         int it = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
             const int m0 = (tile % tiles_m) * 128, n0 = ((tile % tiles_mn) / tiles_m) * BN;
@@ -531,6 +568,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<S::kTmemCols>(tmem);
+    if (threadIdx.x == 0) PNB_TRACE(6);
 }
 
 }  // namespace pnb
