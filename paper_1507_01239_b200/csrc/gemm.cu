@@ -118,6 +118,7 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     if (p.ep.ksplit > 1 && ep.mode != EPI_PARTIAL) throw std::runtime_error("gemm: split-K needs EPI_PARTIAL");
     const long tiles = static_cast<long>((N + bn - 1) / bn) * ((M + 127) / 128) * p.ep.ksplit;
     p.grid = dim3(static_cast<unsigned>(std::min<long>(tiles, num_sms)), 1, 1);  // persistent
+    p.tiles = static_cast<int>(tiles);
     if (split)
         p.fn = reinterpret_cast<void*>(pick<float, true>(bn, a_mn, b_mn, &p.smem));
     else if (f32)

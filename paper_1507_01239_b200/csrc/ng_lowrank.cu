@@ -101,10 +101,20 @@ __global__ void __launch_bounds__(256) lr_hreduce_kernel(const float* __restrict
     for (int r = lane; r < R; r += 32) {
         float h = 0.f;
         if (b < B) {
-            for (int s = 0; s < S; ++s) {
-                const float* p = hpart + (s * B + b) * (NS * R);
-                h += NS == 2 ? p[r] + p[R + r] : p[r];
+            // four partial slabs in flight per step (independent accumulators,
+            // fixed combination order: deterministic)
+            const long sstride = B * static_cast<long>(NS * R);
+            const float* p = hpart + b * (NS * R) + r;
+            float h0 = 0.f, h1 = 0.f, h2 = 0.f, h3 = 0.f;
+            int s = 0;
+            for (; s + 3 < S; s += 4) {
+                h0 += NS == 2 ? p[s * sstride] + p[s * sstride + R] : p[s * sstride];
+                h1 += NS == 2 ? p[(s + 1) * sstride] + p[(s + 1) * sstride + R] : p[(s + 1) * sstride];
+                h2 += NS == 2 ? p[(s + 2) * sstride] + p[(s + 2) * sstride + R] : p[(s + 2) * sstride];
+                h3 += NS == 2 ? p[(s + 3) * sstride] + p[(s + 3) * sstride + R] : p[(s + 3) * sstride];
             }
+            for (; s < S; ++s) h0 += NS == 2 ? p[s * sstride] + p[s * sstride + R] : p[s * sstride];
+            h = (h0 + h1) + (h2 + h3);
             if (in) {
                 const float w1 = wm[r * ldY + xcol];
                 h += w1;

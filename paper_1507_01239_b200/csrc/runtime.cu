@@ -448,7 +448,9 @@ void lr_side_chain(Replica& r, LrSide& sd, cudaEvent_t wait, cudaStream_t ss) {
             lr_start_update(r, sd, ss);
             lr_apply_update(r, sd, ss);
         }
-    lr_precondition_side(r, sd, ss);
+    // timing aid: PARNN_LR_SKIP=1 (in sides) / 2 (out sides) / 3 drops the precondition work
+    static const int skip = std::getenv("PARNN_LR_SKIP") ? std::atoi(std::getenv("PARNN_LR_SKIP")) : 0;
+    if (!(skip & (sd.in ? 1 : 2))) lr_precondition_side(r, sd, ss);
     CUDA_THROW(cudaEventRecord(sd.ready, ss));
     if (r.variant & 2) lr_start_update(r, sd, ss);
     CUDA_THROW(cudaEventRecord(sd.done, ss));

@@ -28,7 +28,7 @@ using bf16 = __nv_bfloat16;
 struct GemmPlan {
     CUtensorMap ta, tb;
     dim3 grid;
-    int smem = 0, M = 0, N = 0, K = 0, bn = 0, threads = 128;
+    int smem = 0, M = 0, N = 0, K = 0, bn = 0, threads = 128, tiles = 0;
     GemmEpi ep;
     void* fn = nullptr;
 };
