@@ -231,8 +231,7 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
                                                      long D, double eta, double a, double alpha,
                                                      float* __restrict__ M, int max_sweeps) {
     extern __shared__ double sh[];
-    const int n = (R + 1) & ~1;
-    const int h = n / 2;
+    const int n = (R + 7) & ~7;      // columns padded to whole 4-column block pairs (zero columns)
     const int ldb = (n + 15) & ~15;  // 128-B aligned columns; rows [n, ldb) are zero
     double* dr = sh;            // [n]
     double* ih = dr + n;        // [n]
@@ -268,21 +267,84 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
     // One group of 8 lanes per column pair, every pair of a round concurrently
     // (launched with 8 * n/2 threads); each lane keeps its <= 12 rows of both
     // columns in registers between the dot products and the rotation.
-    constexpr int kLanes = 8;  // lanes per column pair; 4 pairs per warp
-    constexpr int kRows = ((LR_MAX_RANK + 15) & ~15) / kLanes;
+    // Block one-sided Jacobi: the columns form nb = n/4 blocks of four; one warp
+    // owns a pair of blocks (A, B) per round (round-robin over blocks, nb-1 rounds
+    // per sweep) and keeps their eight columns in registers for the round: lane
+    // group g (8 lanes, rows g_l + 8i) holds A_g and one B column. Four
+    // warp-synchronous stages rotate all 16 cross pairs (stage s: A_g with
+    // B_(g+s)%4; the B columns then move one group down by shuffles), and in
+    // the sweep's first round three more stages rotate the six pairs inside
+    // each block (group g pairs its columns with those of group g^x, fetched by
+    // shuffle; both groups compute the same rotation and each updates its own
+    // column). Shared memory is touched once per column per round.
+    constexpr int kLanes = 8;
+    constexpr int kRows = ((LR_MAX_RANK + 7) & ~7) / kLanes;
     const int wid = t >> 5, nwarp = blockDim.x >> 5;
-    const int gl = t & (kLanes - 1);
-    const int nchunk = ldb / kLanes;  // row chunks of 8 (64 B) per column
-    // odd groups start one chunk later: the two groups of a half-warp then hit
-    // opposite 64-B halves of the bank space whatever their columns (conflict-free)
-    const int cshift = (t >> 3) & 1;
+    const int lane = t & 31, gl = lane & 7, grp = lane >> 3;
+    const int nr = n / kLanes;  // rows per lane
+    const int nb = n / 4, hb = nb / 2;
+    // Rotation of (own column x, norm sx) against (partner y, norm sy); returns the
+    // new own column and norm. Symmetric: the partner group, calling with the
+    // roles swapped, computes the same (c, s) with s negated and gets its half.
+    auto rot_own = [&](double (&x)[kRows], double& sx, const double (&y)[kRows], double sy, bool update_y,
+                       double (&yo)[kRows], double& syo) -> int {
+        // exact norms (register data: cheap) -- norms carried through rotations lose
+        // the small columns when the eigenvalues span > 1e6
+        double ga = 0.0, al = 0.0, be = 0.0;
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            ga = fma(x[i], y[i], ga);
+            al = fma(x[i], x[i], al);
+            be = fma(y[i], y[i], be);
+        }
+#pragma unroll
+        for (int o = kLanes / 2; o; o >>= 1) {
+            ga += __shfl_xor_sync(0xffffffffu, ga, o, kLanes);
+            al += __shfl_xor_sync(0xffffffffu, al, o, kLanes);
+            be += __shfl_xor_sync(0xffffffffu, be, o, kLanes);
+        }
+        if (!(ga * ga > 1e-24 * al * be)) {  // |a.b| <= 1e-12 |a||b|: no rotation
+            if (update_y) {
+#pragma unroll
+                for (int i = 0; i < kRows; ++i) yo[i] = y[i];
+                syo = sy;
+            }
+            return 0;
+        }
+        const long long gbits = __double_as_longlong(ga);
+        const int ex = static_cast<int>((gbits >> 52) & 0x7FF);
+        const double sc = __longlong_as_double(static_cast<long long>(2046 - ex) << 52);
+        const float zeta = __fdividef(static_cast<float>((be - al) * sc), 2.f * static_cast<float>(ga * sc));
+        const float az = fabsf(zeta);
+        const float v = fmaf(az, az, 1.f);
+        const float tf = az > 1e18f ? __fdividef(0.5f, az) : __fdividef(1.f, az + v * rsqrtf(v));
+        const double tt = zeta >= 0.f ? static_cast<double>(tf) : -static_cast<double>(tf);
+        const double w = fma(tt, tt, 1.0);
+        double c = static_cast<double>(rsqrtf(static_cast<float>(w)));
+        c = c * (1.5 - 0.5 * w * c * c);
+        c = c * (1.5 - 0.5 * w * c * c);
+        const double sn = c * tt;
+        const double cs2 = 2.0 * c * sn * ga;
+        if (update_y) {
+#pragma unroll
+            for (int i = 0; i < kRows; ++i) {
+                const double xi = x[i];
+                x[i] = c * xi - sn * y[i];
+                yo[i] = sn * xi + c * y[i];
+            }
+            syo = fmax(sn * sn * al + cs2 + c * c * be, 0.0);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kRows; ++i) x[i] = c * x[i] - sn * y[i];
+        }
+        sx = fmax(c * c * al - cs2 + sn * sn * be, 0.0);
+        return 1;
+    };
     int sweep = 0;
     const long long clk0 = clock64();
-    long long ph[5] = {0, 0, 0, 0, 0};  // PNB_EIG_PHASES: load+dot, reduce, angle, rotate, barrier
     for (; sweep < max_sweeps; ++sweep) {
         // exact column norms once per sweep; within the sweep they are carried
-        // through the rotations (|x'|^2 = c^2 a - 2cs g + s^2 b), so a pair needs one
-        // dot product (a_p . a_q) instead of three
+        // through the rotations (|x'|^2 = c^2 a - 2cs g + s^2 b)
         for (int c = t; c < n; c += blockDim.x) {
             double s2 = 0.0;
             for (int r = 0; r < n; ++r) s2 = fma(Bc[c * ldb + r], Bc[c * ldb + r], s2);
@@ -290,91 +352,71 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
         }
         __syncthreads();
         int rot = 0;
-        for (int k = 0; k < n - 1; ++k) {
-            // warp-uniform trip count: every lane executes the full-mask shuffles
-            // (per-group masks inside one converged warp give wrong sums)
-            long long q0 = clock64();
-            for (int base = wid * 4; base < h; base += nwarp * 4) {
-                const int pr = base + ((t & 31) >> 3);
-                const bool active = pr < h;
-                int p = 0, q = 1;
+        for (int k = 0; k < nb - 1; ++k) {
+            for (int pr = wid; pr < hb; pr += nwarp) {  // warp-uniform
+                int A, B;
                 if (pr == 0) {
-                    q = (k % (n - 1)) + 1;
-                } else if (active) {
-                    p = ((pr + k) % (n - 1)) + 1;
-                    q = ((n - 1 - pr + k) % (n - 1)) + 1;
+                    A = 0;
+                    B = (k % (nb - 1)) + 1;
+                } else {
+                    A = ((pr + k) % (nb - 1)) + 1;
+                    B = ((nb - 1 - pr + k) % (nb - 1)) + 1;
                 }
-                double* cp = Bc + p * ldb;
-                double* cq = Bc + q * ldb;
-                double x[kRows], y[kRows];
-                double ga = 0.0, gb = 0.0;
+                double xa[kRows], xb[kRows], tmp[kRows];
+                const int ca = 4 * A + grp;
+                int cb = 4 * B + grp;
 #pragma unroll
                 for (int i = 0; i < kRows; ++i) {
-                    int ch = i + cshift;
-                    ch = ch >= nchunk ? ch - nchunk : ch;
-                    const int r = gl + kLanes * ch;
-                    x[i] = (active && i < nchunk) ? cp[r] : 0.0;
-                    y[i] = (active && i < nchunk) ? cq[r] : 0.0;
-                    if (i & 1)
-                        gb = fma(x[i], y[i], gb);
-                    else
-                        ga = fma(x[i], y[i], ga);
+                    xa[i] = i < nr ? Bc[ca * ldb + gl + 8 * i] : 0.0;
+                    xb[i] = i < nr ? Bc[cb * ldb + gl + 8 * i] : 0.0;
                 }
-                ga += gb;
-                long long q1 = clock64();
-                ph[0] += q1 - q0;
+                double sa = sig[ca], sb = sig[cb];
+                if (k == 0) {  // pairs inside the blocks: stages x = 1, 2, 3 pair group g with g^x
+#pragma unroll 1
+                    for (int x = 1; x < 4; ++x) {
+                        const int src = lane ^ (8 * x);
 #pragma unroll
-                for (int o = kLanes / 2; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o, kLanes);
-                const double al = active ? sig[p] : 0.0, be = active ? sig[q] : 0.0;
-                long long q2 = clock64();
-                ph[1] += q2 - q1;
-                q0 = q2;
-                if (active && ga * ga > 1e-24 * al * be) {  // |a_p.a_q| > 1e-12 |a_p||a_q|
-                    // angle in fp32 (the residual is removed by the next sweep); the rotation
-                    // itself exactly orthogonal in fp64 (c refined by two Newton steps)
-                    // zeta = (b - a) / 2g in fp32 after removing g's binary exponent (exact
-                    // power-of-two scale built from the exponent bits: no ilogb/ldexp calls)
-                    const long long gbits = __double_as_longlong(ga);
-                    const int ex = static_cast<int>((gbits >> 52) & 0x7FF);  // biased; g != 0 here
-                    const double sc = __longlong_as_double(static_cast<long long>(2046 - ex) << 52);  // 2^(1023-ex)
-                    const float zeta = __fdividef(static_cast<float>((be - al) * sc), 2.f * static_cast<float>(ga * sc));
-                    const float az = fabsf(zeta);
-                    const float v = fmaf(az, az, 1.f);
-                    // approximate fp32 is enough for the angle (MUFU rsqrt/rcp)
-                    const float tf = az > 1e18f ? __fdividef(0.5f, az) : __fdividef(1.f, az + v * rsqrtf(v));
-                    const double tt = zeta >= 0.f ? static_cast<double>(tf) : -static_cast<double>(tf);
-                    const double w = fma(tt, tt, 1.0);
-                    double c = static_cast<double>(rsqrtf(static_cast<float>(w)));
-                    c = c * (1.5 - 0.5 * w * c * c);
-                    c = c * (1.5 - 0.5 * w * c * c);
-                    const double sn = c * tt;
-                    long long q3 = clock64();
-                    ph[2] += q3 - q0;
-                    q0 = q3;
+                        for (int i = 0; i < kRows; ++i) tmp[i] = __shfl_sync(0xffffffffu, xa[i], src);
+                        const double sp = __shfl_sync(0xffffffffu, sa, src);
+                        rot |= rot_own(xa, sa, tmp, sp, false, tmp, sb);
 #pragma unroll
-                    for (int i = 0; i < kRows; ++i) {
-                        int ch = i + cshift;
-                        ch = ch >= nchunk ? ch - nchunk : ch;
-                        const int r = gl + kLanes * ch;
-                        if (i < nchunk) {
-                            cp[r] = c * x[i] - sn * y[i];
-                            cq[r] = sn * x[i] + c * y[i];
-                        }
+                        for (int i = 0; i < kRows; ++i) tmp[i] = __shfl_sync(0xffffffffu, xb[i], src);
+                        const double sq = __shfl_sync(0xffffffffu, sb, src);
+                        rot |= rot_own(xb, sb, tmp, sq, false, tmp, sa);
                     }
-                    if (gl == 0) {
-                        const double cs2 = 2.0 * c * sn * ga;
-                        sig[p] = fmax(c * c * al - cs2 + sn * sn * be, 0.0);
-                        sig[q] = fmax(sn * sn * al + cs2 + c * c * be, 0.0);
+                }
+#pragma unroll 1
+                for (int st = 0; st < 4; ++st) {
+                    // A_g (own) with the B column this group holds; both updated here
+                    double sbn = sb;
+                    rot |= rot_own(xa, sa, xb, sb, true, tmp, sbn);
+                    if (st < 3) {
+                        // the B column moves to group g-1: group g receives from g+1
+                        const int src = (lane + 8) & 31;
+#pragma unroll
+                        for (int i = 0; i < kRows; ++i) xb[i] = __shfl_sync(0xffffffffu, tmp[i], src);
+                        sb = __shfl_sync(0xffffffffu, sbn, src);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < kRows; ++i) xb[i] = tmp[i];
+                        sb = sbn;
                     }
-                    rot = 1;
-                    long long q4 = clock64();
-                    ph[3] += q4 - q0;
-                    q0 = q4;
+                }
+                // after 3 moves group g holds B_(g+3)%4
+                cb = 4 * B + ((grp + 3) & 3);
+#pragma unroll
+                for (int i = 0; i < kRows; ++i) {
+                    if (i < nr) {
+                        Bc[ca * ldb + gl + 8 * i] = xa[i];
+                        Bc[cb * ldb + gl + 8 * i] = xb[i];
+                    }
+                }
+                if (gl == 0) {
+                    sig[ca] = sa;
+                    sig[cb] = sb;
                 }
             }
-            long long q5 = clock64();
             __syncthreads();
-            ph[4] += clock64() - q5;
         }
         if (!__syncthreads_or(rot)) break;  // no rotation anywhere in this sweep
     }
@@ -440,12 +482,11 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
         st[2 * R] = misc[0];
         st[2 * R + 3] = sweep;                             // diagnostics: Jacobi sweeps used,
         st[2 * R + 4] = static_cast<double>(clk1 - clk0);  // and their SM cycles
-        for (int i = 0; i < 5; ++i) st[2 * R + 5 + i] = static_cast<double>(ph[i]);  // thread 0's phases
     }
 }
 
 size_t eig_smem(int R) {
-    const int n = (R + 1) & ~1;
+    const int n = (R + 7) & ~7;
     const int ldb = (n + 15) & ~15;
     return (5 * static_cast<size_t>(n) + 8 + static_cast<size_t>(n) * ldb) * sizeof(double) + (n + 4) * sizeof(int);
 }
@@ -651,8 +692,8 @@ void lr_debug_eig(int R, long D, double eta, double a, double alpha, const doubl
     CUDA_THROW(cudaMemcpy(dg, gram, 16L * R * R, cudaMemcpyHostToDevice));
     CUDA_THROW(cudaFuncSetAttribute(lr_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(eig_smem(LR_MAX_RANK))));
-    const int npair = ((R + 1) & ~1) / 2;
-    const int threads = std::max(128, (npair * 8 + 31) / 32 * 32);
+    const int nblk = ((R + 7) & ~7) / 4;
+    const int threads = std::max(64, 32 * (nblk / 2));
     lr_eig_kernel<<<1, threads, eig_smem(R)>>>(dst, dg, R, D, eta, a, alpha, dm, 40);
     CUDA_THROW(cudaGetLastError());
     CUDA_THROW(cudaDeviceSynchronize());
@@ -729,8 +770,8 @@ void lr_apply_update(Replica& r, LrSide& sd, cudaStream_t s) {
                                                                                   sd.gram);
     const double eta = 1.0 - std::exp(-static_cast<double>(r.B) * r.lrc.update_period / r.lrc.history);
     const double a = eta / static_cast<double>(r.B);
-    const int npair = ((sd.R + 1) & ~1) / 2;
-    const int ethreads = std::max(128, (npair * 8 + 31) / 32 * 32);  // 8 lanes per pair, all pairs concurrently
+    const int nblk = ((sd.R + 7) & ~7) / 4;
+    const int ethreads = std::max(64, 32 * (nblk / 2));  // one warp per block pair
     lr_eig_kernel<<<1, ethreads, eig_smem(sd.R), s>>>(sd.st, sd.gram, sd.R, sd.D, eta, a, r.lrc.alpha, sd.M, 40);
     const int R2 = 2 * sd.R;
     const size_t ws = (static_cast<size_t>(sd.R) * R2 + R2 * 32) * 4;
