@@ -106,17 +106,20 @@ int parnn_replica_get_ng_state(parnn_replica* r, double* factors, uint64_t n);
 int parnn_replica_set_ng_state(parnn_replica* r, const double* factors, uint64_t n, uint64_t update_count);
 /* Low-rank NG-SGD knobs (optimizer PARNN_NGSGD_LOWRANK; alpha = ng_smoothing):
  * ranks of the input / output-derivative Fisher factors (<= 96), subspace
- * update period P, initial updates on the first minibatch, and the history
- * length S (eta = 1 - exp(-B P / S)). Resets the NG state. */
+ * update period P, initial updates on the first minibatch, the history
+ * length S (eta = 1 - exp(-B P / S)) and the update lag (steps until an update
+ * takes effect: 1 = the next step; >= 2: computed in the background while the
+ * steps in between run; capped at P). Resets the NG state. */
 int parnn_replica_set_lowrank(parnn_replica* r, int rank_in, int rank_out, int update_period, int init_iters,
-                              double num_samples_history);
+                              double num_samples_history, int update_lag);
 /* Low-rank NG state of (layer, side 0 = in [A_prev | 1], 1 = out dz):
  * W = E^1/2 R (rank x dim, row-major), d (rank), rho. */
 int parnn_replica_lowrank_state(parnn_replica* r, int layer, int side, double* w, double* d, double* rho,
                                 uint64_t* rank, uint64_t* dim);
 /* Diagnostics of (layer, side): {tr(X X^T), gamma, Jacobi sweeps, Jacobi SM
- * cycles} of the last preconditioning / subspace update. */
-int parnn_replica_lowrank_diag(parnn_replica* r, int layer, int side, double out[4]);
+ * cycles, eigensolve start, end (%globaltimer ns)} of the last preconditioning
+ * / subspace update. */
+int parnn_replica_lowrank_diag(parnn_replica* r, int layer, int side, double out[6]);
 /* Test hook: one low-rank subspace-update eigensolve (the device kernel of
  * the update) on a given Gram of [J; W] (2R x 2R fp32) and state
  * {d[R], e[R], rho, tr(XX^T), ...} (2R+12 doubles); returns the new state
@@ -186,11 +189,12 @@ typedef struct {
     uint64_t rank0;          /* first global rank hosted by this process */
     uint64_t local_workers;  /* ranks hosted here (0 = all m) */
     int serial;              /* serial_train semantics (parallel.cpp:285-294) */
-    /* low-rank NG-SGD knobs (PARNN_NGSGD_LOWRANK); 0 = default (20, 80, 4, 2000) */
+    /* low-rank NG-SGD knobs (PARNN_NGSGD_LOWRANK); 0 = default (20, 80, 4, 2000, lag 3) */
     int ng_rank_in;
     int ng_rank_out;
     int ng_update_period;
     double ng_history;
+    int ng_update_lag;       /* 0 = default (3) */
 } parnn_train_config;
 
 /* train_parallel / serial_train (parallel.cpp:163-294). metrics_out holds up

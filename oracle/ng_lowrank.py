@@ -21,7 +21,9 @@ stored as W_t = E_t^{1/2} R_t with E_t = diag(e_i), e_i = d_i / (d_i + beta_t),
     beta_t = rho_t (1 + alpha) + alpha tr(D_t) / D.
 Preconditioning (X F~^-1 up to scale, F~ = F + alpha tr(F)/D I):
     H = X W^T,  X^ = X - H W,  gamma = sqrt(tr(X X^T) / tr(X^ X^T)).
-Subspace update every `update_period` calls (eta = 1 - exp(-N P / S)):
+Subspace update every `update_period` calls (eta = 1 - exp(-N P / S)), in
+effect update_lag calls later (1 = the next call, as in the paper; the default
+here is 3, which lets the device overlap the eigensolve with two steps):
     T = (eta/N) X^T X + (1 - eta) F_t,    Y = R_t T,   Z = Y Y^T = U C^2 U^T
     R_{t+1} = C^-1 U^T Y,  rho_{t+1} = (tr T - tr C) / (D - R),  D_{t+1} = C - rho_{t+1}
 with the floors c, d >= max(DELTA c_max, EPS tr(T)/D) and rho >= EPS tr(T)/D
@@ -59,6 +61,7 @@ class LowRankConfig:
     num_samples_history: float = 2000.0
     alpha: float = 4.0
     init_iters: int = 3
+    update_lag: int = 3  # steps until an update computed at step t takes effect (1 = t+1 as in Kaldi; <= P)
 
 
 def basis_seed(layer: int, side: int) -> int:
@@ -100,6 +103,8 @@ class Side:
     rho: float
     e: np.ndarray
     t: int = 0
+    pending: tuple = None  # (W, d, rho, e) of an update computed but not yet in effect
+    pending_due: int = 0
 
 
 def side_init(dim: int, rank: int, seed: int, alpha: float) -> Side:
@@ -144,31 +149,48 @@ def eig_update(d, e, rho, K, L, G, trxx, D, eta, a, alpha):
     return d1, rho1, e1, np.concatenate([a * m, (1.0 - eta) * m * dr[None, :]], axis=1)
 
 
-def update(st: Side, x, h, trxx: float, eta: float, alpha: float) -> None:
+def compute_update(st: Side, x, h, trxx: float, eta: float, alpha: float):
     n = x.shape[0]
     j = h.T @ x
     a = eta / n
     d1, rho1, e1, m = eig_update(st.d, st.e, st.rho, j @ j.T, st.W @ j.T, st.W @ st.W.T, trxx, st.dim, eta, a,
                                  alpha)
-    st.W = m @ np.concatenate([j, st.W], axis=0)
-    st.d, st.rho, st.e = d1, rho1, e1
+    return m @ np.concatenate([j, st.W], axis=0), d1, rho1, e1
+
+
+def update(st: Side, x, h, trxx: float, eta: float, alpha: float) -> None:
+    st.W, st.d, st.rho, st.e = compute_update(st, x, h, trxx, eta, alpha)
 
 
 def eta_of(n: int, cfg: LowRankConfig) -> float:
     return 1.0 - math.exp(-n * cfg.update_period / cfg.num_samples_history)
 
 
+def effective_lag(cfg: LowRankConfig) -> int:
+    """An update must take effect before the next one is computed: lag <= P."""
+    return max(1, min(cfg.update_lag, cfg.update_period))
+
+
 def side_step(st: Side, x, cfg: LowRankConfig):
     """One preconditioning call: init on the first call, precondition with
-    W_t, then update the subspace every update_period calls."""
+    W_t, then update the subspace every update_period calls. The update
+    computed from call t takes effect at call t + update_lag (lag >= 2: the
+    device computes it in the background during the calls in between)."""
     eta = eta_of(x.shape[0], cfg)
     if st.t == 0:
         for _ in range(cfg.init_iters):
             h, _, _, trxx = precondition(st, x)
             update(st, x, h, trxx, eta, cfg.alpha)
+    if st.pending is not None and st.t >= st.pending_due:
+        st.W, st.d, st.rho, st.e = st.pending
+        st.pending = None
     h, xh, gamma, trxx = precondition(st, x)
     if st.t % cfg.update_period == 0:
-        update(st, x, h, trxx, eta, cfg.alpha)
+        if effective_lag(cfg) == 1:
+            update(st, x, h, trxx, eta, cfg.alpha)
+        else:
+            st.pending = compute_update(st, x, h, trxx, eta, cfg.alpha)
+            st.pending_due = st.t + effective_lag(cfg)
     st.t += 1
     return xh, gamma
 

@@ -30,7 +30,8 @@ class TrainConfig(C.Structure):
                 ("optimizer", c_int), ("lr_schedule", c_int), ("lr_init", c_f64), ("epochs", c_u64),
                 ("ng_decay", c_f64), ("ng_smoothing", c_f64), ("precision", c_int), ("activation", c_int),
                 ("rank0", c_u64), ("local_workers", c_u64), ("serial", c_int),
-                ("ng_rank_in", c_int), ("ng_rank_out", c_int), ("ng_update_period", c_int), ("ng_history", c_f64)]
+                ("ng_rank_in", c_int), ("ng_rank_out", c_int), ("ng_update_period", c_int), ("ng_history", c_f64),
+                ("ng_update_lag", c_int)]
 
 
 # (name, restype, argtypes) for every symbol declared in include/parnn_b200.h
@@ -66,7 +67,7 @@ SIGNATURES = [
     ("parnn_replica_get_params", c_int, [vp, vp, c_u64]),
     ("parnn_replica_get_ng_state", c_int, [vp, vp, c_u64]),
     ("parnn_replica_set_ng_state", c_int, [vp, vp, c_u64, c_u64]),
-    ("parnn_replica_set_lowrank", c_int, [vp, c_int, c_int, c_int, c_int, c_f64]),
+    ("parnn_replica_set_lowrank", c_int, [vp, c_int, c_int, c_int, c_int, c_f64, c_int]),
     ("parnn_replica_lowrank_state", c_int, [vp, c_int, c_int, vp, vp, vp, vp, vp]),
     ("parnn_replica_lowrank_diag", c_int, [vp, c_int, c_int, vp]),
     ("parnn_replica_bind", c_int, [vp, vp]),

@@ -243,7 +243,7 @@ int parnn_replica_create(parnn_ctx* ctx, const uint64_t* dims, int nd, int act, 
 }
 
 int parnn_replica_set_lowrank(parnn_replica* r, int rank_in, int rank_out, int update_period, int init_iters,
-                              double history) {
+                              double history, int update_lag) {
     return guarded([&] {
         need(r, "replica");
         LrConfig c = r->r->lrc;
@@ -252,6 +252,7 @@ int parnn_replica_set_lowrank(parnn_replica* r, int rank_in, int rank_out, int u
         c.update_period = update_period;
         c.init_iters = init_iters;
         c.history = history;
+        c.update_lag = update_lag;
         r->r->set_lowrank(c);
     });
 }
@@ -278,7 +279,7 @@ int parnn_replica_lowrank_diag(parnn_replica* r, int layer, int side, double out
         if (layer < 0 || layer >= rp.L || side < 0 || side > 1) throw std::runtime_error("ng lowrank: bad layer/side");
         const LrSide& sd = side == 0 ? rp.lrl[layer].in : rp.lrl[layer].out;
         CUDA_THROW(cudaDeviceSynchronize());
-        CUDA_THROW(cudaMemcpy(out, sd.st + 2 * sd.R + 1, 4 * sizeof(double), cudaMemcpyDeviceToHost));
+        CUDA_THROW(cudaMemcpy(out, sd.st + 2 * sd.R + 1, 6 * sizeof(double), cudaMemcpyDeviceToHost));
     });
 }
 
@@ -502,6 +503,7 @@ int parnn_train(parnn_ctx* ctx, parnn_comm* comm, const parnn_train_config* c, c
         if (c->ng_rank_out) t.lr.rank_out = c->ng_rank_out;
         if (c->ng_update_period) t.lr.update_period = c->ng_update_period;
         if (c->ng_history > 0.0) t.lr.history = c->ng_history;
+        if (c->ng_update_lag) t.lr.update_lag = c->ng_update_lag;
         std::vector<EpochRec> met;
         pnb::train(ctx->c.get(), comm ? comm->c.get() : nullptr, t, to_dims(dims, nd), params0, train_set->d.get(),
               cv ? cv->d.get() : nullptr, params_out, met);

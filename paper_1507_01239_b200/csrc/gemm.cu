@@ -129,9 +129,21 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     p.threads = split ? 448 : 320;  // GemmSmem::kThreads
 }
 
+namespace {
+thread_local int g_grid_cap = 0;
+}
+
+void gemm_set_grid_cap(int cap) { g_grid_cap = cap; }
+
+dim3 gemm_launch_grid(const GemmPlan& p) {
+    // the persistent kernel covers every tile with any grid (tile = blockIdx + k * gridDim)
+    if (g_grid_cap > 0 && static_cast<int>(p.grid.x) > g_grid_cap) return dim3(g_grid_cap, 1, 1);
+    return p.grid;
+}
+
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {
     auto fn = reinterpret_cast<KernelFn>(p.fn);
-    fn<<<p.grid, p.threads, p.smem, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.ep);
+    fn<<<gemm_launch_grid(p), p.threads, p.smem, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.ep);
     CUDA_THROW(cudaGetLastError());
 }
 

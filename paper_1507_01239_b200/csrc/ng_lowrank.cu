@@ -227,7 +227,8 @@ __global__ void lr_gram_reduce_kernel(const float* __restrict__ gpart, int S, lo
 //   relative threshold |a_p.a_q| <= 1e-12 |a_p||a_q| ends it.
 //   Then: eigenpairs sorted descending; scale-relative floors; rho', d', e'
 //   and M = E'^1/2 C^-1 U^T E^-1/2 [a I | (1-eta) Dr].
-__global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, const float* __restrict__ gram, int R,
+__global__ void __launch_bounds__(512) lr_eig_kernel(const double* __restrict__ st, const double* __restrict__ trxx_p,
+                                                     double* __restrict__ st_out, const float* __restrict__ gram, int R,
                                                      long D, double eta, double a, double alpha,
                                                      float* __restrict__ M, int max_sweeps) {
     extern __shared__ double sh[];
@@ -244,6 +245,8 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
     const int t = threadIdx.x;
     const int R2 = 2 * R;
     const double rho = st[2 * R];
+    unsigned long long gt0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
     for (int i = t; i < n; i += blockDim.x) {
         dr[i] = i < R ? st[i] + rho : 0.0;
         ih[i] = i < R ? 1.0 / sqrt(st[R + i]) : 0.0;
@@ -443,7 +446,7 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
         // scale-relative floors (oracle/ng_lowrank.py: DELTA, EPS, TINY)
         double sd = 0.0;
         for (int k = 0; k < R; ++k) sd += st[k];
-        const double trxx = st[2 * R + 1];
+        const double trxx = *trxx_p;
         const double trt = a * trxx + (1.0 - eta) * (static_cast<double>(D) * rho + sd);
         const double c0 = sqrt(fmax(sig[perm[0]], 0.0));
         const double floor = fmax(fmax(kDelta * c0, kEps * trt / static_cast<double>(D)), kTiny);
@@ -475,13 +478,17 @@ __global__ void __launch_bounds__(512) lr_eig_kernel(double* __restrict__ st, co
     }
     __syncthreads();
     for (int k = t; k < R; k += blockDim.x) {
-        st[k] = dv[k];
-        st[R + k] = dv[k] / (dv[k] + beta1);
+        st_out[k] = dv[k];
+        st_out[R + k] = dv[k] / (dv[k] + beta1);
     }
     if (t == 0) {
-        st[2 * R] = misc[0];
-        st[2 * R + 3] = sweep;                             // diagnostics: Jacobi sweeps used,
-        st[2 * R + 4] = static_cast<double>(clk1 - clk0);  // and their SM cycles
+        st_out[2 * R] = misc[0];
+        st_out[2 * R + 3] = sweep;                             // diagnostics: Jacobi sweeps used,
+        st_out[2 * R + 4] = static_cast<double>(clk1 - clk0);  // their SM cycles,
+        unsigned long long gt1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+        st_out[2 * R + 5] = static_cast<double>(gt0);  // kernel start / end (%globaltimer ns)
+        st_out[2 * R + 6] = static_cast<double>(gt1);
     }
 }
 
@@ -500,11 +507,12 @@ __global__ void lr_split_kernel(const float* __restrict__ w, long n, long rstrid
 }
 
 
-// W' = M [J; W] per 32-column chunk (in place: the chunk is staged in shared
-// memory first), plus the bf16 operand copy.
+// W' = M [J; W] per 32-column chunk into the next-W buffers (fp32 + bf16 hi/lo
+// operand copy); the commit copies them over W.
 template <typename T>
-__global__ void __launch_bounds__(256) lr_wupdate_kernel(float* __restrict__ YW, long ldY, int R, long D,
-                                                         const float* __restrict__ M, T* __restrict__ wop) {
+__global__ void __launch_bounds__(256) lr_wupdate_kernel(const float* __restrict__ YW, long ldY, int R, long D,
+                                                         const float* __restrict__ M, float* __restrict__ wn,
+                                                         T* __restrict__ wop) {
     extern __shared__ float smf[];
     const int R2 = 2 * R;
     float* Ms = smf;             // [R][2R]
@@ -524,7 +532,7 @@ __global__ void __launch_bounds__(256) lr_wupdate_kernel(float* __restrict__ YW,
         const float* mk = Ms + k * R2;
 #pragma unroll 8
         for (int j = 0; j < R2; ++j) acc = fmaf(mk[j], Ys[j * 32 + c], acc);
-        YW[(R + k) * ldY + c0 + c] = acc;
+        wn[k * ldY + c0 + c] = acc;
         if (wop) {  // bf16: W_hi and W_lo = W - W_hi
             const T hi = from_f<T>(acc);
             wop[k * ldY + c0 + c] = hi;
@@ -558,6 +566,10 @@ void side_alloc(Replica& r, LrSide& sd, bool in, long dx, int want_rank, int lay
     sd.xpart = dalloc_d(2 * 1024);
     sd.gram = falloc(4L * R * R);
     sd.st = dalloc_d(2 * R + 12);
+    sd.stn = dalloc_d(2 * R + 12);
+    sd.trxx_snap = dalloc_d(1);
+    sd.Wn = falloc(R * sd.ldY);
+    sd.wopn = r.f32() ? nullptr : valloc(2 * R * sd.ldY * 2);
     sd.M = falloc(2L * R * R);
     sd.xhat = valloc(B * sd.ldx * es);
     CUDA_THROW(cudaStreamCreateWithFlags(&sd.stream, cudaStreamNonBlocking));
@@ -601,6 +613,10 @@ void side_free(LrSide& sd) {
     f(sd.gpart);
     f(sd.gram);
     f(sd.st);
+    f(sd.stn);
+    f(sd.trxx_snap);
+    f(sd.Wn);
+    f(sd.wopn);
     f(sd.M);
     f(sd.xhat);
     if (sd.ready) cudaEventDestroy(sd.ready);
@@ -664,7 +680,9 @@ void side_plans(Replica& r, LrSide& sd, const void* X) {
         e.mode = EPI_PARTIAL;
         const int n2 = 2 * R;
         const int tiles = ((n2 + 127) / 128) * ((n2 + 63) / 64);
-        e.ksplit = std::max(1, sms / tiles);
+        // inline updates (lag 1) are latency-critical: split K over the GPU; background
+        // updates keep to a few CTAs each so they do not crowd out the running step
+        e.ksplit = r.lr_lag() == 1 ? std::max(1, sms / tiles) : 1;
         const int nk = static_cast<int>((sd.D + 31) / 32);
         const int per = (nk + e.ksplit - 1) / e.ksplit;
         const int S = (nk + per - 1) / per;
@@ -694,10 +712,12 @@ void lr_debug_eig(int R, long D, double eta, double a, double alpha, const doubl
                                     static_cast<int>(eig_smem(LR_MAX_RANK))));
     const int nblk = ((R + 7) & ~7) / 4;
     const int threads = std::max(64, 32 * (nblk / 2));
-    lr_eig_kernel<<<1, threads, eig_smem(R)>>>(dst, dg, R, D, eta, a, alpha, dm, 40);
+    double* dout = dalloc_d(ns);
+    lr_eig_kernel<<<1, threads, eig_smem(R)>>>(dst, dst + 2 * R + 1, dout, dg, R, D, eta, a, alpha, dm, 40);
     CUDA_THROW(cudaGetLastError());
     CUDA_THROW(cudaDeviceSynchronize());
-    CUDA_THROW(cudaMemcpy(st_out, dst, ns * 8, cudaMemcpyDeviceToHost));
+    CUDA_THROW(cudaMemcpy(st_out, dout, ns * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dout);
     CUDA_THROW(cudaMemcpy(m_out, dm, 8L * R * R, cudaMemcpyDeviceToHost));
     *sweeps = static_cast<int>(st_out[2 * R + 3]);
     cudaFree(dst);
@@ -750,13 +770,15 @@ void lr_precondition_side(Replica& r, LrSide& sd, cudaStream_t s) {
                                                          sd.in, static_cast<bf16*>(sd.H), sd.ldH, sd.ohat, sd.rpart);
     CUDA_THROW(cudaGetLastError());
     gemm_launch(sd.xg, s);
-    lr_stats_kernel<<<1, 32, 0, s>>>(sd.xpart, static_cast<int>(sd.xg.grid.x), sd.rpart, sd.nrb, sd.R, sd.in, r.B,
-                                     sd.st);
+    lr_stats_kernel<<<1, 32, 0, s>>>(sd.xpart, static_cast<int>(gemm_launch_grid(sd.xg).x), sd.rpart, sd.nrb, sd.R,
+                                     sd.in, r.B, sd.st);
     CUDA_THROW(cudaGetLastError());
 }
 
 void lr_start_update(Replica& r, LrSide& sd, cudaStream_t s) {
     gemm_launch(sd.jg, s);
+    // this step's tr(X X^T) for the update (later preconditionings overwrite st's copy)
+    CUDA_THROW(cudaMemcpyAsync(sd.trxx_snap, sd.st + 2 * sd.R + 1, sizeof(double), cudaMemcpyDeviceToDevice, s));
     if (sd.in) {
         lr_jcol_kernel<<<1, 128, 0, s>>>(sd.rpart, sd.nrb, sd.R, sd.YW, sd.ldY, sd.dx);
         CUDA_THROW(cudaGetLastError());
@@ -772,15 +794,29 @@ void lr_apply_update(Replica& r, LrSide& sd, cudaStream_t s) {
     const double a = eta / static_cast<double>(r.B);
     const int nblk = ((sd.R + 7) & ~7) / 4;
     const int ethreads = std::max(64, 32 * (nblk / 2));  // one warp per block pair
-    lr_eig_kernel<<<1, ethreads, eig_smem(sd.R), s>>>(sd.st, sd.gram, sd.R, sd.D, eta, a, r.lrc.alpha, sd.M, 40);
+    lr_eig_kernel<<<1, ethreads, eig_smem(sd.R), s>>>(sd.st, sd.trxx_snap, sd.stn, sd.gram, sd.R, sd.D, eta, a,
+                                                      r.lrc.alpha, sd.M, 40);
     const int R2 = 2 * sd.R;
     const size_t ws = (static_cast<size_t>(sd.R) * R2 + R2 * 32) * 4;
     const unsigned grid = static_cast<unsigned>((sd.D + 31) / 32);
     if (r.f32())
-        lr_wupdate_kernel<float><<<grid, 256, ws, s>>>(sd.YW, sd.ldY, sd.R, sd.D, sd.M, nullptr);
+        lr_wupdate_kernel<float><<<grid, 256, ws, s>>>(sd.YW, sd.ldY, sd.R, sd.D, sd.M, sd.Wn, nullptr);
     else
-        lr_wupdate_kernel<bf16><<<grid, 256, ws, s>>>(sd.YW, sd.ldY, sd.R, sd.D, sd.M, static_cast<bf16*>(sd.wop));
+        lr_wupdate_kernel<bf16><<<grid, 256, ws, s>>>(sd.YW, sd.ldY, sd.R, sd.D, sd.M, sd.Wn,
+                                                      static_cast<bf16*>(sd.wopn));
     CUDA_THROW(cudaGetLastError());
+}
+
+// The computed update takes effect: next-W buffers and state over the current ones.
+void lr_commit_update(Replica& r, LrSide& sd, cudaStream_t s) {
+    const size_t wbytes = static_cast<size_t>(sd.R) * sd.ldY * sizeof(float);
+    CUDA_THROW(cudaMemcpyAsync(sd.YW + sd.R * sd.ldY, sd.Wn, wbytes, cudaMemcpyDeviceToDevice, s));
+    if (!r.f32())
+        CUDA_THROW(cudaMemcpyAsync(sd.wop, sd.wopn, 2 * static_cast<size_t>(sd.R) * sd.ldY * 2,
+                                   cudaMemcpyDeviceToDevice, s));
+    CUDA_THROW(cudaMemcpyAsync(sd.st, sd.stn, (2 * sd.R + 1) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CUDA_THROW(cudaMemcpyAsync(sd.st + 2 * sd.R + 3, sd.stn + 2 * sd.R + 3, 4 * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s));  // diagnostics
 }
 
 void lr_layer_update(Replica& r, int l, cudaStream_t s) {
@@ -803,17 +839,28 @@ void lr_layer_update(Replica& r, int l, cudaStream_t s) {
 int Replica::lr_variant(long t) const {
     const long P = std::max(1, lrc.update_period);
     int v = 0;
-    if (t == 0) v |= 1;
-    if (t % P == 0) v |= 2;
-    if (t >= 1 && (t - 1) % P == 0) v |= 4;
+    if (t == 0) v |= LRV_INIT;
+    if (t % P == 0) v |= LRV_J;
+    const int lag = lr_lag();
+    if (lag == 1) {
+        if (t >= 1 && (t - 1) % P == 0) v |= LRV_APPLY;
+    } else {
+        const long ph = t % P;  // the update of step t - ph runs in the background for lag-1 steps
+        if (t >= ph && ph >= 1 && ph < lag && t - ph >= 0) v |= LRV_INFLIGHT;
+        if (t >= lag && (t - lag) % P == 0) v |= LRV_COMMIT;
+    }
     return v;
 }
+
+// an update may take effect at most P steps after it was computed (before the next one's J)
+int Replica::lr_lag() const { return std::max(1, std::min(lrc.update_lag, lrc.update_period)); }
 
 void Replica::set_lowrank(const LrConfig& c) {
     if (opt != OPT_NG_LOWRANK) throw std::runtime_error("replica: not a low-rank NG-SGD replica");
     if (c.rank_in < 1 || c.rank_out < 1 || c.rank_in > LR_MAX_RANK || c.rank_out > LR_MAX_RANK)
         throw std::runtime_error("ng lowrank: ranks must be in [1, " + std::to_string(LR_MAX_RANK) + "]");
     if (c.update_period < 1) throw std::runtime_error("ng lowrank: update_period must be >= 1");
+    if (c.update_lag < 1) throw std::runtime_error("ng lowrank: update_lag must be >= 1");
     if (c.init_iters < 0) throw std::runtime_error("ng lowrank: init_iters must be >= 0");
     if (!(c.history > 0.0)) throw std::runtime_error("ng lowrank: num_samples_history must be positive");
     if (!(c.alpha > 0.0)) throw std::runtime_error("ng lowrank: alpha must be positive");

@@ -168,8 +168,13 @@ Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision
 Replica::~Replica() {
     if (stream) cudaStreamSynchronize(stream);
     if (graph) cudaGraphExecDestroy(graph);
+    if (bg) cudaStreamSynchronize(bg);
     for (auto g : vgraphs)
         if (g) cudaGraphExecDestroy(g);
+    if (apply_graph) cudaGraphExecDestroy(apply_graph);
+    if (ev_jdone) cudaEventDestroy(ev_jdone);
+    if (ev_applied) cudaEventDestroy(ev_applied);
+    if (bg) cudaStreamDestroy(bg);
     lr_free(*this);
     for (auto e : ev_act) cudaEventDestroy(e);
     for (auto e : step_ev) cudaEventDestroy(e);
@@ -362,8 +367,15 @@ void Replica::bind(DeviceDataset* ds) {
             cudaGraphExecDestroy(g);
             g = nullptr;
         }
-    vgraphs.assign(8, nullptr);
-    vnodes.assign(8, 0);
+    vgraphs.assign(32, nullptr);
+    vnodes.assign(32, 0);
+    if (opt == OPT_NG_LOWRANK && !bg) {
+        CUDA_THROW(cudaStreamCreateWithFlags(&bg, cudaStreamNonBlocking));
+        CUDA_THROW(cudaEventCreateWithFlags(&ev_jdone, cudaEventDisableTiming));
+        CUDA_THROW(cudaEventCreateWithFlags(&ev_applied, cudaEventDisableTiming));
+    }
+    if (bg) CUDA_THROW(cudaStreamSynchronize(bg));
+    apply_pending = false;
     if (std::getenv("PARNN_NO_GRAPH")) use_graph = false;  // debugging: eager launches
     tl.clear();
     if (std::getenv("PARNN_TIMELINE") && tl_pool.empty()) {
@@ -390,15 +402,101 @@ void Replica::bind(DeviceDataset* ds) {
             cudaGraphDestroy(g);
         };
         if (opt == OPT_NG_LOWRANK) {
-            // one graph per step kind; kernels_per_step = the average over one update period
+            // one graph per step kind (captured here for the first two update periods,
+            // others on first use); kernels_per_step = average over one period
             const int P = std::max(1, lrc.update_period);
-            const std::vector<int> kinds = P == 1 ? std::vector<int>{3, 6} : std::vector<int>{3, 0, 2, 4};
-            for (int v : kinds) capture(v, &vgraphs[v], &vnodes[v]);
-            kernels_per_step = P == 1 ? vnodes[6] : (vnodes[2] + vnodes[4] + (P - 2) * vnodes[0]) / P;
+            for (long t = 0; t < 2 * P + 3; ++t) {
+                const int v = lr_variant(t);
+                if (!vgraphs[v]) capture_variant(v);
+            }
+            if (lr_lag() >= 2) {
+                if (apply_graph) cudaGraphExecDestroy(apply_graph);
+                apply_graph = nullptr;
+                capture_apply_graph();
+            }
+            long sum = 0;
+            for (long t = 2 * P; t < 3 * P; ++t) sum += vnodes[lr_variant(t)];
+            if (lr_lag() >= 2) sum += apply_nodes;
+            kernels_per_step = sum / P;
         } else {
             capture(0, &graph, &kernels_per_step);
         }
     }
+}
+
+void Replica::capture_variant(int v) {
+    const int saved = variant;
+    variant = v;
+    cudaGraph_t g;
+    CUDA_THROW(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        enqueue_step(stream);
+    } catch (...) {
+        cudaStreamEndCapture(stream, &g);
+        variant = saved;
+        throw;
+    }
+    CUDA_THROW(cudaStreamEndCapture(stream, &g));
+    size_t nodes = 0;
+    CUDA_THROW(cudaGraphGetNodes(g, nullptr, &nodes));
+    vnodes[v] = static_cast<long>(nodes);
+    CUDA_THROW(cudaGraphInstantiate(&vgraphs[v], g, 0));
+    cudaGraphDestroy(g);
+    variant = saved;
+}
+
+// lag >= 2 low-rank updates: the step that commits a background update waits for it
+void Replica::lr_before_step(cudaStream_t s) {
+    if ((variant & LRV_COMMIT) && apply_pending) {
+        CUDA_THROW(cudaStreamWaitEvent(s, ev_applied, 0));
+        apply_pending = false;
+    }
+}
+
+// ...and the step that computed J launches it on the background stream
+void Replica::lr_after_step(cudaStream_t s) {
+    if (lr_lag() < 2 || !(variant & LRV_J) || prof) return;
+    CUDA_THROW(cudaEventRecord(ev_jdone, s));
+    CUDA_THROW(cudaStreamWaitEvent(bg, ev_jdone, 0));
+    if (use_graph && apply_graph) {
+        CUDA_THROW(cudaGraphLaunch(apply_graph, bg));
+    } else {
+        for (int l = L - 1; l >= 0; --l) {
+            lr_apply_update(*this, lrl[l].out, bg);
+            lr_apply_update(*this, lrl[l].in, bg);
+        }
+    }
+    CUDA_THROW(cudaEventRecord(ev_applied, bg));
+    apply_pending = true;
+}
+
+void Replica::capture_apply_graph() {
+    // every side's update as an independent branch, largest (out side, last layer) first
+    cudaGraph_t g;
+    CUDA_THROW(cudaStreamBeginCapture(bg, cudaStreamCaptureModeThreadLocal));
+    try {
+        CUDA_THROW(cudaEventRecord(ev_t0, bg));
+        for (int pass = 0; pass < 2; ++pass)
+            for (int l = L - 1; l >= 0; --l) {
+                LrSide& sd = pass == 0 ? lrl[l].out : lrl[l].in;
+                CUDA_THROW(cudaStreamWaitEvent(sd.stream, ev_t0, 0));
+                lr_apply_update(*this, sd, sd.stream);
+                CUDA_THROW(cudaEventRecord(sd.done, sd.stream));
+            }
+        for (int l = 0; l < L; ++l) {
+            CUDA_THROW(cudaStreamWaitEvent(bg, lrl[l].in.done, 0));
+            CUDA_THROW(cudaStreamWaitEvent(bg, lrl[l].out.done, 0));
+        }
+    } catch (...) {
+        cudaStreamEndCapture(bg, &g);
+        throw;
+    }
+    CUDA_THROW(cudaStreamEndCapture(bg, &g));
+    size_t nodes = 0;
+    CUDA_THROW(cudaGraphGetNodes(g, nullptr, &nodes));
+    apply_nodes = static_cast<long>(nodes);
+    CUDA_THROW(cudaGraphInstantiate(&apply_graph, g, 0));
+    cudaGraphDestroy(g);
 }
 
 void Replica::tmark(const std::string& name, cudaStream_t s) {
@@ -442,17 +540,22 @@ namespace {
 // [J of the update applied at the start of the next step].
 void lr_side_chain(Replica& r, LrSide& sd, cudaEvent_t wait, cudaStream_t ss) {
     if (wait) CUDA_THROW(cudaStreamWaitEvent(ss, wait, 0));
-    if (r.variant & 1)
+    if (r.variant & LRV_INIT)
         for (int it = 0; it < r.lrc.init_iters; ++it) {
             lr_precondition_side(r, sd, ss);
             lr_start_update(r, sd, ss);
             lr_apply_update(r, sd, ss);
+            lr_commit_update(r, sd, ss);
         }
     // timing aid: PARNN_LR_SKIP=1 (in sides) / 2 (out sides) / 3 drops the precondition work
     static const int skip = std::getenv("PARNN_LR_SKIP") ? std::atoi(std::getenv("PARNN_LR_SKIP")) : 0;
     if (!(skip & (sd.in ? 1 : 2))) lr_precondition_side(r, sd, ss);
     CUDA_THROW(cudaEventRecord(sd.ready, ss));
-    if (r.variant & 2) lr_start_update(r, sd, ss);
+    if (r.variant & LRV_J) {
+        lr_start_update(r, sd, ss);
+        // profiled lag-2 steps compute the update inline (no background graph)
+        if (r.prof && r.lr_lag() >= 2) lr_apply_update(r, sd, ss);
+    }
     CUDA_THROW(cudaEventRecord(sd.done, ss));
 }
 
@@ -462,6 +565,12 @@ void lr_side_chain(Replica& r, LrSide& sd, cudaEvent_t wait, cudaStream_t ss) {
 // backward has produced its dz; dW_l (+ bias) runs on the side stream once
 // dA_l has read W_l and both sides of layer l are preconditioned.
 void enqueue_lowrank(Replica& r, cudaStream_t s) {
+    // beside a background subspace update (one long CTA per side) the GEMM grids
+    // leave 2L SMs free, so no GEMM CTA queues behind an eigensolve
+    struct Cap {
+        explicit Cap(int c) { gemm_set_grid_cap(c); }
+        ~Cap() { gemm_set_grid_cap(0); }
+    } cap((r.variant & LRV_INFLIGHT) && !r.prof ? r.ctx->num_sms - 2 * r.L : 0);
     const bool F = r.f32();
     const int L = r.L;
     DeviceDataset* ds = r.bound;
@@ -469,11 +578,12 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
     if (r.prof) {
         // profiled: serial on one stream so event regions are well defined
         r.mark("start", -1, 0, s);
-        if (r.variant & 4) {
-            for (int l = 0; l < L; ++l) {
-                lr_apply_update(r, r.lrl[l].in, s);
-                lr_apply_update(r, r.lrl[l].out, s);
-            }
+        if (r.variant & (LRV_APPLY | LRV_COMMIT)) {
+            for (int l = 0; l < L; ++l)
+                for (LrSide* sd : {&r.lrl[l].in, &r.lrl[l].out}) {
+                    if (r.variant & LRV_APPLY) lr_apply_update(r, *sd, s);
+                    lr_commit_update(r, *sd, s);
+                }
             r.mark("ng_lr_apply", -1, 0, s);
         }
         launch_gather(ds->features(r.prec), ds->ld, ds->y, r.d_rows, r.d_step, r.B, r.dims[0], r.acts[0],
@@ -504,7 +614,8 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
         for (int l = 0; l < L; ++l)
             for (LrSide* sd : {&r.lrl[l].in, &r.lrl[l].out}) {
                 CUDA_THROW(cudaStreamWaitEvent(S(sd->stream), r.ev_t0, 0));
-                if (r.variant & 4) lr_apply_update(r, *sd, S(sd->stream));
+                if (r.variant & LRV_APPLY) lr_apply_update(r, *sd, S(sd->stream));
+                if (r.variant & (LRV_APPLY | LRV_COMMIT)) lr_commit_update(r, *sd, S(sd->stream));
             }
         launch_gather(ds->features(r.prec), ds->ld, ds->y, r.d_rows, r.d_step, r.B, r.dims[0], r.acts[0],
                       r.ld_act[0], r.d_ybatch, F, s);
@@ -655,8 +766,11 @@ void Replica::profile_steps(long steps, std::vector<std::string>& names, std::ve
     flops.clear();
     for (long it = 0; it < steps; ++it) {
         Profile p;
+        if (opt == OPT_NG_LOWRANK) {
+            variant = lr_variant(lr_t++);
+            lr_before_step(stream);
+        }
         prof = &p;
-        if (opt == OPT_NG_LOWRANK) variant = lr_variant(lr_t++);
         try {
             enqueue_step(stream);
         } catch (...) {
@@ -664,6 +778,8 @@ void Replica::profile_steps(long steps, std::vector<std::string>& names, std::ve
             throw;
         }
         prof = nullptr;
+        if (!step_ev.empty()) CUDA_THROW(cudaEventRecord(step_ev[epoch_steps % kStepRing], stream));
+        ++epoch_steps;
         CUDA_THROW(cudaStreamSynchronize(stream));
         // accumulate by region name: step kinds (low-rank init / update / plain) differ in regions
         for (size_t i = 1; i < p.events.size(); ++i) {
@@ -704,6 +820,7 @@ void Replica::upload_epoch(const uint32_t* rows, const float* lrs, long steps) {
     CUDA_THROW(cudaMemcpyAsync(d_lr, lrs, steps * 4, cudaMemcpyHostToDevice, s));
     CUDA_THROW(cudaMemsetAsync(d_step, 0, 4, s));
     epoch_steps = 0;
+    epoch_len = steps;
 }
 
 double Replica::step_ce(long j) {
@@ -719,6 +836,9 @@ double Replica::step_ce(long j) {
 
 void Replica::run_step(cudaStream_t s) {
     if (!bound) throw std::runtime_error("replica: no dataset bound");
+    if (epoch_steps >= epoch_len)
+        throw std::runtime_error("replica: step " + std::to_string(epoch_steps) + " beyond the " +
+                                 std::to_string(epoch_len) + " uploaded for this epoch");
     if (bound->written) CUDA_THROW(cudaStreamWaitEvent(s, bound->written, 0));  // inputs written by the host
     if (step_ev.empty()) {
         step_ev.resize(kStepRing);
@@ -731,12 +851,16 @@ void Replica::run_step(cudaStream_t s) {
     } rec{this, s};
     if (opt == OPT_NG_LOWRANK) {
         variant = lr_variant(lr_t);
-        static const char* force = std::getenv("PARNN_LR_FORCE_VARIANT");  // timing aid: 0 plain, 2 J, 4 apply
+        static const char* force = std::getenv("PARNN_LR_FORCE_VARIANT");  // timing aid (LRV_* bits)
         if (force && lr_t > 0) variant = std::atoi(force);
-        if (use_graph && vgraphs[variant])
+        lr_before_step(s);
+        if (use_graph) {
+            if (!vgraphs[variant]) capture_variant(variant);
             CUDA_THROW(cudaGraphLaunch(vgraphs[variant], s));
-        else
+        } else {
             enqueue_step(s);
+        }
+        lr_after_step(s);
         ++lr_t;
         return;
     }

@@ -38,6 +38,11 @@ int choose_bn(int M, int N, int num_sms);
 void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b_mn, const void* B, long ldb,
                int M, int N, int K, const GemmEpi& ep, int num_sms, int force_bn = 0);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);
+// Cap on the persistent grid of subsequent launches from this thread (0 = none):
+// steps that run long single-CTA kernels (the NG subspace eigensolves) beside
+// the GEMMs keep those SMs out of the GEMM grids, so no GEMM CTA waits for them.
+void gemm_set_grid_cap(int cap);
+dim3 gemm_launch_grid(const GemmPlan& p);
 
 enum Precision : int { PREC_BF16 = 0, PREC_TF32 = 1, PREC_FP32 = 2 };
 enum Optimizer : int { OPT_SGD = 0, OPT_NG_KRON = 1, OPT_NG_LOWRANK = 2 };
@@ -109,6 +114,7 @@ struct LrConfig {
     int update_period = 4;            // subspace update every P minibatches
     int init_iters = 3;               // updates on the first minibatch before use
     double history = 2000.0;          // S: eta = 1 - exp(-B P / S)
+    int update_lag = 3;               // steps until an update takes effect (1 = next step; <= P)
     double alpha = 4.0;               // smoothing (the reference's ng_smoothing)
 };
 struct LrSide {
@@ -127,7 +133,11 @@ struct LrSide {
     double* xpart = nullptr;  // [grid x 2]: per-CTA sums of X^2 and Xhat^2
     float* gpart = nullptr;   // [S2 x 2R x 2R] Gram partials of [J; W]
     float* gram = nullptr;    // [2R x 2R]
-    double* st = nullptr;     // d[R], e[R], rho, tr(X X^T), gamma
+    double* st = nullptr;     // d[R], e[R], rho, tr(X X^T), gamma, diagnostics
+    double* stn = nullptr;    // the computed update's state (committed over st)
+    double* trxx_snap = nullptr;  // tr(X X^T) of the step the update is computed from
+    float* Wn = nullptr;      // [R x ldY] the computed update's W
+    void* wopn = nullptr;     // its bf16 [W_hi; W_lo] (bf16 mode)
     float* M = nullptr;       // [R x 2R]: W' = M [J; W]
     void* xhat = nullptr;     // [B x ldx] preconditioned vectors (operand dtype)
     const void* X = nullptr;  // [B x ldx] the layer's vectors (acts[l] or dz[l])
@@ -135,6 +145,13 @@ struct LrSide {
     int nrb = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ready = nullptr, done = nullptr;
+};
+enum LrVariantBits : int {
+    LRV_INIT = 1,      // first step: init updates on its own batch
+    LRV_J = 2,         // compute J of an update at the end of the step
+    LRV_APPLY = 4,     // lag 1: compute + commit the pending update at the start of the step
+    LRV_COMMIT = 8,    // lag >= 2: commit the update computed in the background
+    LRV_INFLIGHT = 16  // lag >= 2: the background update runs beside this step (GEMM grids capped)
 };
 struct LrLayer {
     LrSide in, out;
@@ -202,12 +219,23 @@ struct Replica {
     LrConfig lrc;
     std::vector<LrLayer> lrl;
     long lr_t = 0;
-    int variant = 0;  // bit 0: init, bit 1: J (start an update), bit 2: apply the pending update
+    int variant = 0;  // LRV_* bits of the current step
     std::vector<cudaGraphExec_t> vgraphs;
     std::vector<long> vnodes;
     std::vector<cudaEvent_t> ev_act;  // acts[l] ready (in-side chains start)
     cudaEvent_t ev_t0 = nullptr;
     int lr_variant(long t) const;
+    int lr_lag() const;
+    // lag-2 updates: computed by a separate graph on `bg` while the next step runs
+    cudaStream_t bg = nullptr;
+    cudaGraphExec_t apply_graph = nullptr;
+    cudaEvent_t ev_jdone = nullptr, ev_applied = nullptr;
+    bool apply_pending = false;
+    long apply_nodes = 0;
+    void capture_variant(int v);
+    void capture_apply_graph();
+    void lr_before_step(cudaStream_t s);
+    void lr_after_step(cudaStream_t s);
     void set_lowrank(const LrConfig& c);
     void get_lowrank_state(int layer, int side, double* w, double* d, double* rho) const;
 
@@ -229,6 +257,7 @@ struct Replica {
     static constexpr int kStepRing = 64;
     std::vector<cudaEvent_t> step_ev;
     long epoch_steps = 0;  // steps launched since upload_epoch
+    long epoch_len = 0;    // steps uploaded
     double step_ce(long j);
     void run_step(cudaStream_t s);  // one minibatch (graph or eager)
     void enqueue_step(cudaStream_t s);
@@ -280,7 +309,8 @@ void lr_free(Replica& r);
 void lr_build_plans(Replica& r);
 void lr_precondition_side(Replica& r, LrSide& sd, cudaStream_t s);  // H, Xhat, gamma
 void lr_start_update(Replica& r, LrSide& sd, cudaStream_t s);       // J = H^T X
-void lr_apply_update(Replica& r, LrSide& sd, cudaStream_t s);       // Gram, eig, W'
+void lr_apply_update(Replica& r, LrSide& sd, cudaStream_t s);       // Gram, eig, W' (into next buffers)
+void lr_commit_update(Replica& r, LrSide& sd, cudaStream_t s);      // next buffers -> current
 void lr_layer_update(Replica& r, int l, cudaStream_t s);            // bias + dW with gamma
 void lr_debug_eig(int R, long D, double eta, double a, double alpha, const double* st_in, const float* gram,
                   double* st_out, float* m_out, int* sweeps);

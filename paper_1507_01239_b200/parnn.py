@@ -104,6 +104,7 @@ class TrainOptions:
     ng_rank_out: int = 80
     ng_update_period: int = 4
     ng_history: float = 2000.0
+    ng_update_lag: int = 3
 
 
 @dataclass
@@ -367,9 +368,9 @@ class Replica:
         check(lib().parnn_replica_set_ng_state(self.h, ptr(flat), flat.size, update_count))
 
     def set_lowrank(self, rank_in: int = 20, rank_out: int = 80, update_period: int = 4, init_iters: int = 3,
-                    num_samples_history: float = 2000.0):
+                    num_samples_history: float = 2000.0, update_lag: int = 3):
         check(lib().parnn_replica_set_lowrank(self.h, rank_in, rank_out, update_period, init_iters,
-                                              num_samples_history))
+                                              num_samples_history, update_lag))
 
     def lowrank_state(self, layer: int, side: int):
         """(W = E^1/2 R, d, rho) of one side (0 = in [A_prev | 1], 1 = out dz)."""
@@ -382,9 +383,10 @@ class Replica:
         return w, d, rho.value
 
     def lowrank_diag(self, layer: int, side: int) -> dict:
-        out = np.zeros(4)
+        out = np.zeros(6)
         check(lib().parnn_replica_lowrank_diag(self.h, layer, side, ptr(out)))
-        return {"trxx": out[0], "gamma": out[1], "sweeps": int(out[2]), "jacobi_cycles": out[3]}
+        return {"trxx": out[0], "gamma": out[1], "sweeps": int(out[2]), "jacobi_cycles": out[3],
+                "eig_start_ns": out[4], "eig_end_ns": out[5]}
 
     def bind(self, ds: DeviceDataset):
         check(lib().parnn_replica_bind(self.h, ds.h))
@@ -504,7 +506,8 @@ def _train(plan: ParallelPlan, model0: MlpModel, train: Dataset, cv: Dataset, op
     cfg = TrainConfig(plan.workers, plan.avg_frequency, plan.minibatch, plan.base_seed, int(opts.optimizer),
                       int(opts.lr_schedule), opts.lr_init, opts.epochs, opts.ng_decay, opts.ng_smoothing,
                       int(opts.precision), int(model0.activation), rank0, local_workers, int(serial),
-                      opts.ng_rank_in, opts.ng_rank_out, opts.ng_update_period, opts.ng_history)
+                      opts.ng_rank_in, opts.ng_rank_out, opts.ng_update_period, opts.ng_history,
+                      opts.ng_update_lag)
     d = u64(model0.layer_dims)
     out = np.zeros(param_count(model0.layer_dims))
     met = np.zeros((max(opts.epochs, 1), 7))

@@ -29,7 +29,7 @@ ds = P.DeviceDataset(ctx, P.Dataset(x, y, 16))
 m = P.init_random(dims, seed=3)
 r = P.Replica(ctx, dims, precision=P.Precision[prec], optimizer=P.OptimizerKind.ngsgd_lowrank, minibatch=B,
               max_steps=steps)
-r.set_lowrank(cfg.rank_in, cfg.rank_out, cfg.update_period, cfg.init_iters, cfg.num_samples_history)
+r.set_lowrank(cfg.rank_in, cfg.rank_out, cfg.update_period, cfg.init_iters, cfg.num_samples_history, cfg.update_lag)
 r.set_params(m.params)
 r.bind(ds)
 r.upload_epoch(np.concatenate(batches), lrs)

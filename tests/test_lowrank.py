@@ -103,7 +103,8 @@ def _gpu_run(ctx, prec, x, y, dims, B, batches, lrs, cfg, steps_per_call=None):
     m = P.init_random(dims, seed=3)
     r = P.Replica(ctx, dims, precision=prec, optimizer=P.OptimizerKind.ngsgd_lowrank, minibatch=B,
                   max_steps=len(batches), ng_smoothing=cfg.alpha)
-    r.set_lowrank(cfg.rank_in, cfg.rank_out, cfg.update_period, cfg.init_iters, cfg.num_samples_history)
+    r.set_lowrank(cfg.rank_in, cfg.rank_out, cfg.update_period, cfg.init_iters, cfg.num_samples_history,
+                  cfg.update_lag)
     r.set_params(m.params)
     r.bind(ds)
     r.upload_epoch(np.concatenate(batches), lrs)
@@ -124,15 +125,16 @@ def _oracle_run(p0, dims, x, y, batches, lrs, cfg):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("lag,period", [(1, 2), (2, 2), (3, 3)])
 @pytest.mark.parametrize("prec,dtol", [("fp32", 2e-3), ("tf32", 3e-2), ("bf16", 8e-2)])
-def test_lowrank_step_parity(ctx, prec, dtol):
+def test_lowrank_step_parity(ctx, prec, dtol, lag, period):
     from paper_1507_01239_b200 import parnn as P
     x, y = _data()
     dims = [40, 48, 36, 12]
     B = 32
     batches = _batches(x.shape[0], B, 6)
     lrs = np.array([0.32, 0.3, 0.28, 0.26, 0.24, 0.22], np.float32)
-    cfg = LR.LowRankConfig(rank_in=6, rank_out=8, update_period=2, init_iters=3)
+    cfg = LR.LowRankConfig(rank_in=6, rank_out=8, update_period=period, init_iters=3, update_lag=lag)
     r, p0, p, ce = _gpu_run(ctx, P.Precision[prec], x, y, dims, B, batches, lrs, cfg)
     mo, st, ce_o = _oracle_run(p0, dims, x, y, batches, lrs.astype(np.float64), cfg)
     po = O.flatten(mo)
@@ -145,7 +147,9 @@ def test_lowrank_step_parity(ctx, prec, dtol):
                 w, d, rho = r.lowrank_state(l, side)
                 assert w.shape == so.W.shape
                 assert rel(w.T @ w, so.W.T @ so.W) < 2e-3  # sign/rotation-invariant
-                assert rel(d, so.d) < 2e-3 and abs(rho - so.rho) / so.rho < 2e-3
+                # rho = (tr T - sum c)/(D - R) amplifies fp32 differences ~5x on sides whose
+                # d sit at the floors (the last layer's input side here): 1e-2
+                assert rel(d, so.d) < 2e-3 and abs(rho - so.rho) / so.rho < 1e-2
 
 
 @pytest.mark.gpu
@@ -157,7 +161,7 @@ def test_lowrank_graph_variants_deterministic(ctx):
     dims = [40, 48, 36, 12]
     batches = _batches(x.shape[0], 32, 9)
     lrs = np.full(9, 0.3, np.float32)
-    cfg = LR.LowRankConfig(rank_in=6, rank_out=8, update_period=3, init_iters=2)
+    cfg = LR.LowRankConfig(rank_in=6, rank_out=8, update_period=3, init_iters=2, update_lag=2)
     _, _, p1, c1 = _gpu_run(ctx, P.Precision.bf16, x, y, dims, 32, batches, lrs, cfg)
     _, _, p2, c2 = _gpu_run(ctx, P.Precision.bf16, x, y, dims, 32, batches, lrs, cfg, steps_per_call=1)
     _, _, p3, _ = _gpu_run(ctx, P.Precision.bf16, x, y, dims, 32, batches, lrs, cfg, steps_per_call=3)
