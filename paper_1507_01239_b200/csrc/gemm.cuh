@@ -76,6 +76,12 @@ struct GemmEpi {
     unsigned* flag = nullptr;  // bit `flag_bit` set on a non-finite gradient
     unsigned flag_bit = 0;
     int lower = 0;  // skip tiles strictly above the diagonal (SYRK-style updates)
+    // GRAD_SGD extras (NG low-rank): alpha *= (*gscale_a) * (*gscale_b) (the two
+    // sides' gamma), and output column bias_col is the bias gradient -> bias32[row]
+    const double* gscale_a = nullptr;
+    const double* gscale_b = nullptr;
+    int bias_col = -1;
+    float* bias32 = nullptr;
     int ksplit = 1;         // split-K factor (set by gemm_plan; every split non-empty)
     long split_stride = 0;  // PARTIAL: floats between the per-split outputs
     double* part = nullptr; // RESID: [gridDim.x][2] per-CTA {sum aux^2, sum out^2}
@@ -202,7 +208,7 @@ struct GemmSmem {
 // Epilogue of one 32-column chunk of one accumulator row.
 template <typename T>
 __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, float (&v)[32], int row, int n, int valid,
-                                               float lr, int ks, float& s_aux, float& s_out) {
+                                               float lr, float alpha_eff, int ks, float& s_aux, float& s_out) {
     bool bad = false;
     switch (ep.mode) {
         case EPI_PARTIAL: {
@@ -250,16 +256,26 @@ __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, float (&v)[32]
         case EPI_GRAD_SGD: {
             float w[32];
             float* wp = ep.out32 + row * ep.ld_out32 + n;
-            load_row32<float>(wp, w, valid);
-            const float alpha = ep.coef ? ep.alpha * ep.coef[0] : ep.alpha;  // NG low-rank scale
+            const int bj = ep.bias_col - n;  // bias column inside this chunk?
+            const int wvalid = (bj >= 0 && bj < valid) ? bj : valid;
+            load_row32<float>(wp, w, wvalid);
+            const float alpha = alpha_eff;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const float g = v[j] * alpha;
-                bad |= (j < valid) && !isfinite(g);
+                bad |= (j < wvalid) && !isfinite(g);
                 w[j] -= lr * g;
             }
-            store_row32<float>(wp, w, valid);
-            if (ep.shadow) store_row32<__nv_bfloat16>(ep.shadow + row * ep.ld_shadow + n, w, valid);
+            store_row32<float>(wp, w, wvalid);
+            if (ep.shadow) store_row32<__nv_bfloat16>(ep.shadow + row * ep.ld_shadow + n, w, wvalid);
+            if (bj >= 0 && bj < valid) {
+                float vb = 0.f;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) vb = j == bj ? v[j] : vb;  // static register indexing
+                const float gb = vb * alpha;
+                if (!isfinite(gb) && ep.flag) atomicOr(ep.flag, 1u << (ep.flag_bit + 1));
+                ep.bias32[row] -= lr * gb;
+            }
             break;
         }
         case EPI_ACTGRAD: {
@@ -463,8 +479,12 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
         // per-row work of each thread
         const int quad = warp & 3;
         const int eset = (warp - 2) >> 2;
-        float lr = 0.f;
-        if (ep.mode == EPI_GRAD_SGD) lr = ep.lr[ep.step ? *ep.step : 0];
+        float lr = 0.f, alpha_eff = ep.alpha;
+        if (ep.mode == EPI_GRAD_SGD) {
+            lr = ep.lr[ep.step ? *ep.step : 0];
+            if (ep.coef) alpha_eff = ep.alpha * ep.coef[0];
+            if (ep.gscale_a) alpha_eff = static_cast<float>(ep.alpha * *ep.gscale_a * *ep.gscale_b);
+        }
         bool bad = false;
         float s_aux = 0.f, s_out = 0.f;  // RESID sums (per thread, this CTA's tiles)
         int local = 0;
@@ -504,7 +524,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
                 float v[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                bad |= epilogue_chunk<T>(ep, v, row, n, min(32, N - n), lr, ks, s_aux, s_out);
+                bad |= epilogue_chunk<T>(ep, v, row, n, min(32, N - n), lr, alpha_eff, ks, s_aux, s_out);
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);

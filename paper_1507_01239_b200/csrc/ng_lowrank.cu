@@ -89,60 +89,76 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // directions of mean-dominated inputs (sigmoid activations) by ~10% and
 // the subspace update diverges.
 template <typename T, int NS>
-__global__ void __launch_bounds__(256) lr_hreduce_kernel(const float* __restrict__ hpart, int S, long B, int R,
+__global__ void __launch_bounds__(768) lr_hreduce_kernel(const float* __restrict__ hpart, int S, long B, int R,
                                                          const float* __restrict__ wm, long ldY, long xcol, int in,
                                                          T* __restrict__ H, long ldH, float* __restrict__ ohat,
-                                                         double* __restrict__ rpart) {
+                                                         double* __restrict__ rpart, T* __restrict__ xhat,
+                                                         long ldxh) {
+    // one thread per (row, r) of an 8-row block: every thread keeps eight
+    // split-K slabs in flight (the sums are latency-bound otherwise)
     __shared__ float cs[8][LR_MAX_RANK + 1];
+    __shared__ float pw[8][LR_MAX_RANK + 1];
     __shared__ float o2[8];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = threadIdx.x;
+    const int w = t / R, r = t % R;
     const long b = blockIdx.x * 8L + w;
-    float ow = 0.f;
-    for (int r = lane; r < R; r += 32) {
-        float h = 0.f;
-        if (b < B) {
-            // four partial slabs in flight per step (independent accumulators,
-            // fixed combination order: deterministic)
-            const long sstride = B * static_cast<long>(NS * R);
-            const float* p = hpart + b * (NS * R) + r;
-            float h0 = 0.f, h1 = 0.f, h2 = 0.f, h3 = 0.f;
-            int s = 0;
-            for (; s + 3 < S; s += 4) {
-                h0 += NS == 2 ? p[s * sstride] + p[s * sstride + R] : p[s * sstride];
-                h1 += NS == 2 ? p[(s + 1) * sstride] + p[(s + 1) * sstride + R] : p[(s + 1) * sstride];
-                h2 += NS == 2 ? p[(s + 2) * sstride] + p[(s + 2) * sstride + R] : p[(s + 2) * sstride];
-                h3 += NS == 2 ? p[(s + 3) * sstride] + p[(s + 3) * sstride + R] : p[(s + 3) * sstride];
-            }
-            for (; s < S; ++s) h0 += NS == 2 ? p[s * sstride] + p[s * sstride + R] : p[s * sstride];
-            h = (h0 + h1) + (h2 + h3);
-            if (in) {
-                const float w1 = wm[r * ldY + xcol];
-                h += w1;
-                ow = fmaf(h, w1, ow);
-            }
-            H[b * ldH + r] = from_f<T>(h);
-            if (NS == 2) H[b * ldH + R + r] = from_f<T>(h);
-        }
-        cs[w][r] = h;
-    }
+    float h = 0.f;
+    if (w < 8 && b < B) {
+        const long sstride = B * static_cast<long>(NS * R);
+        const float* p = hpart + b * (NS * R) + r;
+        float acc[8];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) ow += __shfl_xor_sync(0xffffffffu, ow, o);
-    if (lane == 0) {
+        for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+        int s = 0;
+        for (; s + 7 < S; s += 8) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float* q = p + (s + i) * sstride;
+                acc[i] += NS == 2 ? q[0] + q[R] : q[0];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (s + i < S) {
+                const float* q = p + (s + i) * sstride;
+                acc[i] += NS == 2 ? q[0] + q[R] : q[0];
+            }
+        }
+        h = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        float w1 = 0.f;
+        if (in) {
+            w1 = wm[r * ldY + xcol];
+            h += w1;
+        }
+        H[b * ldH + r] = from_f<T>(h);
+        if (NS == 2) H[b * ldH + R + r] = from_f<T>(h);
+        pw[w][r] = h * w1;
+    } else if (w < 8) {
+        pw[w][r] = 0.f;
+    }
+    if (w < 8) cs[w][r] = h;
+    __syncthreads();
+    if (t < 8) {  // preconditioned ones column of row t (fixed order)
+        const long bb = blockIdx.x * 8L + t;
+        float ow = 0.f;
+        for (int k = 0; k < R; ++k) ow += pw[t][k];
         const float o = 1.f - ow;
-        const bool ok = in && b < B;
-        if (ok) ohat[b] = o;
-        o2[w] = ok ? o * o : 0.f;
+        const bool ok = in && bb < B;
+        if (ok) {
+            ohat[bb] = o;
+            xhat[bb * ldxh + xcol] = from_f<T>(o);  // the dW GEMM's extra column -> bias gradient
+        }
+        o2[t] = ok ? o * o : 0.f;
     }
     __syncthreads();
-    const int t = threadIdx.x;
     if (t < R) {
-        double s = 0.0;
-        for (int i = 0; i < 8; ++i) s += cs[i][t];
-        rpart[blockIdx.x * (R + 1L) + t] = s;
+        double sum = 0.0;
+        for (int i = 0; i < 8; ++i) sum += cs[i][t];
+        rpart[blockIdx.x * (R + 1L) + t] = sum;
     } else if (t == R) {
-        double s = 0.0;
-        for (int i = 0; i < 8; ++i) s += o2[i];
-        rpart[blockIdx.x * (R + 1L) + R] = s;
+        double sum = 0.0;
+        for (int i = 0; i < 8; ++i) sum += o2[i];
+        rpart[blockIdx.x * (R + 1L) + R] = sum;
     }
 }
 
@@ -556,6 +572,7 @@ void side_alloc(Replica& r, LrSide& sd, bool in, long dx, int want_rank, int lay
     sd.ns = r.f32() ? 1 : 2;
     sd.ldH = pad32(sd.ns * R);
     sd.ldx = pad32(dx);
+    sd.ldxh = pad32(sd.D);
     const size_t es = r.esz();
     sd.YW = falloc(2 * R * sd.ldY);
     sd.wop = r.f32() ? static_cast<void*>(sd.YW + R * sd.ldY) : valloc(2 * R * sd.ldY * 2);  // fp32: alias
@@ -571,7 +588,7 @@ void side_alloc(Replica& r, LrSide& sd, bool in, long dx, int want_rank, int lay
     sd.Wn = falloc(R * sd.ldY);
     sd.wopn = r.f32() ? nullptr : valloc(2 * R * sd.ldY * 2);
     sd.M = falloc(2L * R * R);
-    sd.xhat = valloc(B * sd.ldx * es);
+    sd.xhat = valloc(B * sd.ldxh * es);
     CUDA_THROW(cudaStreamCreateWithFlags(&sd.stream, cudaStreamNonBlocking));
     CUDA_THROW(cudaEventCreateWithFlags(&sd.ready, cudaEventDisableTiming));
     CUDA_THROW(cudaEventCreateWithFlags(&sd.done, cudaEventDisableTiming));
@@ -656,7 +673,7 @@ void side_plans(Replica& r, LrSide& sd, const void* X) {
         GemmEpi e;
         e.mode = EPI_RESID;
         e.out = sd.xhat;
-        e.ld_out = sd.ldx;
+        e.ld_out = sd.ldxh;
         e.aux = X;
         e.ld_aux = sd.ldx;
         e.part = sd.xpart;
@@ -763,11 +780,13 @@ void lr_precondition_side(Replica& r, LrSide& sd, cudaStream_t s) {
     gemm_launch(sd.hg, s);
     const float* wm = sd.YW + sd.R * sd.ldY;
     if (r.f32())
-        lr_hreduce_kernel<float, 1><<<sd.nrb, 256, 0, s>>>(sd.hpart, sd.hg.ep.ksplit, r.B, sd.R, wm, sd.ldY, sd.dx,
-                                                          sd.in, static_cast<float*>(sd.H), sd.ldH, sd.ohat, sd.rpart);
+        lr_hreduce_kernel<float, 1><<<sd.nrb, 8 * std::max(sd.R, 32), 0, s>>>(sd.hpart, sd.hg.ep.ksplit, r.B, sd.R, wm, sd.ldY, sd.dx,
+                                                          sd.in, static_cast<float*>(sd.H), sd.ldH, sd.ohat, sd.rpart,
+                                                          static_cast<float*>(sd.xhat), sd.ldxh);
     else
-        lr_hreduce_kernel<bf16, 2><<<sd.nrb, 256, 0, s>>>(sd.hpart, sd.hg.ep.ksplit, r.B, sd.R, wm, sd.ldY, sd.dx,
-                                                         sd.in, static_cast<bf16*>(sd.H), sd.ldH, sd.ohat, sd.rpart);
+        lr_hreduce_kernel<bf16, 2><<<sd.nrb, 8 * std::max(sd.R, 32), 0, s>>>(sd.hpart, sd.hg.ep.ksplit, r.B, sd.R, wm, sd.ldY, sd.dx,
+                                                         sd.in, static_cast<bf16*>(sd.H), sd.ldH, sd.ohat, sd.rpart,
+                                                         static_cast<bf16*>(sd.xhat), sd.ldxh);
     CUDA_THROW(cudaGetLastError());
     gemm_launch(sd.xg, s);
     lr_stats_kernel<<<1, 32, 0, s>>>(sd.xpart, static_cast<int>(gemm_launch_grid(sd.xg).x), sd.rpart, sd.nrb, sd.R,
@@ -820,19 +839,8 @@ void lr_commit_update(Replica& r, LrSide& sd, cudaStream_t s) {
 }
 
 void lr_layer_update(Replica& r, int l, cudaStream_t s) {
-    LrLayer& ly = r.lrl[l];
-    const long dout = r.dims[l + 1];
-    dim3 grid((dout + 31) / 32), block(32, 32);
-    float* bias = r.params + r.b_off[l];
-    if (r.f32())
-        lr_bias_kernel<float><<<grid, block, 0, s>>>(static_cast<const float*>(ly.out.xhat), ly.out.ldx, r.B, dout,
-                                                     ly.in.ohat, ly.in.st, ly.in.R, ly.out.st, ly.out.R, bias, r.d_lr,
-                                                     r.d_step, r.d_flags, 2 * l + 1, ly.coef);
-    else
-        lr_bias_kernel<bf16><<<grid, block, 0, s>>>(static_cast<const bf16*>(ly.out.xhat), ly.out.ldx, r.B, dout,
-                                                    ly.in.ohat, ly.in.st, ly.in.R, ly.out.st, ly.out.R, bias, r.d_lr,
-                                                    r.d_step, r.d_flags, 2 * l + 1, ly.coef);
-    CUDA_THROW(cudaGetLastError());
+    // W and b in one GEMM: its extra output column (the preconditioned ones
+    // column of the input side) is the bias gradient (EPI_GRAD_SGD bias_col)
     gemm_launch(r.dw[l], s);
 }
 

@@ -325,10 +325,15 @@ void Replica::bind(DeviceDataset* ds) {
             g.ld_out32 = ldw[l];
         }
         if (opt == OPT_NG_LOWRANK) {
-            // dW = g_in g_out / B  Dhat^T Ahat  (preconditioned vectors; coef written by lr_bias_kernel)
-            g.coef = lrl[l].coef;
-            gemm_plan(dw[l], prec, true, lrl[l].out.xhat, lrl[l].out.ldx, true, lrl[l].in.xhat, lrl[l].in.ldx, dout,
-                      din, B, g, sms);
+            // [dW | db] = g_in g_out / B  Dhat^T [Ahat | ahat_1]  (preconditioned vectors; the
+            // extra column din of the input side's xhat is its preconditioned ones column)
+            LrSide& si = lrl[l].in;
+            LrSide& so = lrl[l].out;
+            g.gscale_a = si.st + 2 * si.R + 2;
+            g.gscale_b = so.st + 2 * so.R + 2;
+            g.bias_col = static_cast<int>(din);
+            g.bias32 = params + b_off[l];
+            gemm_plan(dw[l], prec, true, so.xhat, so.ldxh, true, si.xhat, si.ldxh, dout, din + 1, B, g, sms);
         } else {
             gemm_plan(dw[l], prec, true, dz[l], ld_act[l + 1], true, acts[l], ld_act[l], dout, din, B, g, sms);
         }
@@ -636,14 +641,16 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
             if (l > 0) gemm_launch(r.da[l], s);
             CUDA_THROW(cudaEventRecord(r.ev_bwd[l], s));  // W_l read; dz[l-1] ready
             if (l > 0) lr_side_chain(r, r.lrl[l - 1].out, r.ev_bwd[l], S(r.lrl[l - 1].out.stream));
-            CUDA_THROW(cudaStreamWaitEvent(S(r.side), r.ev_bwd[l], 0));
-            CUDA_THROW(cudaStreamWaitEvent(S(r.side), r.lrl[l].in.ready, 0));
-            CUDA_THROW(cudaStreamWaitEvent(S(r.side), r.lrl[l].out.ready, 0));
-            lr_layer_update(r, l, S(r.side));
-            r.tmark("dw" + std::to_string(l), S(r.side));
+            // [dW_l | db_l] on the layer's input-side stream: the layers' weight updates are
+            // independent and overlap each other and the remaining chains (a single side
+            // stream made them the step's critical path)
+            cudaStream_t ws = S(r.lrl[l].in.stream);
+            CUDA_THROW(cudaStreamWaitEvent(ws, r.ev_bwd[l], 0));
+            CUDA_THROW(cudaStreamWaitEvent(ws, r.lrl[l].out.ready, 0));
+            lr_layer_update(r, l, ws);
+            r.tmark("dw" + std::to_string(l), ws);
+            CUDA_THROW(cudaEventRecord(r.lrl[l].in.done, ws));
         }
-        CUDA_THROW(cudaEventRecord(r.ev_side, S(r.side)));
-        CUDA_THROW(cudaStreamWaitEvent(s, r.ev_side, 0));
         for (int l = 0; l < L; ++l) {
             CUDA_THROW(cudaStreamWaitEvent(s, r.lrl[l].in.done, 0));
             CUDA_THROW(cudaStreamWaitEvent(s, r.lrl[l].out.done, 0));

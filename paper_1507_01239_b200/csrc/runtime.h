@@ -123,7 +123,7 @@ struct LrSide {
     long D = 0;   // dx (+1 for the ones column)
     int R = 0;
     int ns = 1;  // W operand rows per direction: 1 (fp32 modes), 2 (bf16: W_hi, W_lo)
-    long ldY = 0, ldH = 0, ldx = 0;
+    long ldY = 0, ldH = 0, ldx = 0, ldxh = 0;  // ldx: X's rows; ldxh: xhat's (in side: + the ones column)
     float* YW = nullptr;    // [2R x ldY] fp32: rows [0,R) J = H^T X, rows [R,2R) W (master)
     void* wop = nullptr;    // bf16 operand copy [W_hi; W_lo] [2R x ldY] (fp32 modes: the W rows of YW)
     float* hpart = nullptr; // [S x B x ns*R] split-K partials of H = X W^T
@@ -139,7 +139,7 @@ struct LrSide {
     float* Wn = nullptr;      // [R x ldY] the computed update's W
     void* wopn = nullptr;     // its bf16 [W_hi; W_lo] (bf16 mode)
     float* M = nullptr;       // [R x 2R]: W' = M [J; W]
-    void* xhat = nullptr;     // [B x ldx] preconditioned vectors (operand dtype)
+    void* xhat = nullptr;     // [B x ldxh] preconditioned vectors (operand dtype); in side: column dx = ohat
     const void* X = nullptr;  // [B x ldx] the layer's vectors (acts[l] or dz[l])
     GemmPlan hg, xg, jg, gg;
     int nrb = 0;
