@@ -6,6 +6,7 @@
 #include <string>
 
 #include "gemm.cuh"
+#include "gemm_pick.cuh"
 #include "runtime.h"
 
 namespace pnb {
@@ -48,44 +49,6 @@ CUtensorMap make_tmap(const void* base, bool f32, uint64_t inner, uint64_t outer
     return m;
 }
 
-template <int BN, bool SPLIT>
-constexpr int stages_for() {
-    if (SPLIT) return BN == 256 ? 2 : (BN == 128 ? 3 : 4);
-    return BN == 256 ? 4 : (BN == 128 ? 6 : 8);
-}
-
-using KernelFn = void (*)(CUtensorMap, CUtensorMap, int, int, int, GemmEpi);
-
-template <typename T, int BN, bool AMN, bool BMN, bool SPLIT>
-KernelFn kernel_ptr(int* smem) {
-    constexpr int ST = stages_for<BN, SPLIT>();
-    *smem = GemmSmem<BN, ST, T, SPLIT>::kBytes;
-    auto k = &gemm_tc_kernel<T, BN, ST, AMN, BMN, SPLIT>;
-    static bool configured = false;
-    if (!configured) {
-        CUDA_THROW(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem));
-        configured = true;
-    }
-    return reinterpret_cast<KernelFn>(k);
-}
-
-template <typename T, int BN, bool SPLIT>
-KernelFn pick_major(bool amn, bool bmn, int* smem) {
-    if (!amn && !bmn) return kernel_ptr<T, BN, false, false, SPLIT>(smem);
-    if (amn && bmn) return kernel_ptr<T, BN, true, true, SPLIT>(smem);
-    if (!amn && bmn) return kernel_ptr<T, BN, false, true, SPLIT>(smem);
-    return kernel_ptr<T, BN, true, false, SPLIT>(smem);
-}
-
-template <typename T, bool SPLIT>
-KernelFn pick(int bn, bool amn, bool bmn, int* smem) {
-    switch (bn) {
-        case 256: return pick_major<T, 256, SPLIT>(amn, bmn, smem);
-        case 128: return pick_major<T, 128, SPLIT>(amn, bmn, smem);
-        default: return pick_major<T, 64, SPLIT>(amn, bmn, smem);
-    }
-}
-
 }  // namespace
 
 int choose_bn(int M, int N, int num_sms) {
@@ -119,12 +82,15 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     const long tiles = static_cast<long>((N + bn - 1) / bn) * ((M + 127) / 128) * p.ep.ksplit;
     p.grid = dim3(static_cast<unsigned>(std::min<long>(tiles, num_sms)), 1, 1);  // persistent
     p.tiles = static_cast<int>(tiles);
+    const bool te = gemm_epi_transposed(ep.mode);
+    KernelFn fn;
     if (split)
-        p.fn = reinterpret_cast<void*>(pick<float, true>(bn, a_mn, b_mn, &p.smem));
+        fn = te ? gemm_pick_split_t(bn, a_mn, b_mn, &p.smem) : gemm_pick_split_r(bn, a_mn, b_mn, &p.smem);
     else if (f32)
-        p.fn = reinterpret_cast<void*>(pick<float, false>(bn, a_mn, b_mn, &p.smem));
+        fn = te ? gemm_pick_f32_t(bn, a_mn, b_mn, &p.smem) : gemm_pick_f32_r(bn, a_mn, b_mn, &p.smem);
     else
-        p.fn = reinterpret_cast<void*>(pick<__nv_bfloat16, false>(bn, a_mn, b_mn, &p.smem));
+        fn = te ? gemm_pick_bf16_t(bn, a_mn, b_mn, &p.smem) : gemm_pick_bf16_r(bn, a_mn, b_mn, &p.smem);
+    p.fn = reinterpret_cast<void*>(fn);
     p.bn = bn;
     p.threads = split ? 448 : 320;  // GemmSmem::kThreads
 }

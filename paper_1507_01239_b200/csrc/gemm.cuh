@@ -130,6 +130,260 @@ __device__ __forceinline__ void st_from_float<__nv_bfloat16>(__nv_bfloat16* p, f
     *p = __float2bfloat16_rn(v);
 }
 
+// PP "pieces" of a lane in the transposed epilogue layout: four consecutive
+// values (columns c .. c+3, nvc of them valid) of rows rb, rb+4, ... (valid
+// while < M), at base + row * ld. Whole aligned pieces move as one 16-byte
+// (fp32) / 8-byte (bf16) access; all loads of a call are issued before any of
+// their values is used. Partial pieces (matrix edges) go element-wise.
+template <typename T>
+__device__ __forceinline__ bool pieces_vec(const T* base, long ld, int nvc) {
+    return nvc == 4 && ((reinterpret_cast<uintptr_t>(base) | static_cast<uintptr_t>(ld * sizeof(T))) &
+                        (4 * sizeof(T) - 1)) == 0;
+}
+
+template <typename T, int PP>
+__device__ __forceinline__ void load_pieces(const T* base, long ld, int rb, int M, int nvc, float (&x)[PP][4]) {
+    if (pieces_vec(base, ld, nvc)) {
+        if constexpr (sizeof(T) == 4) {
+            float4 u[PP];
+#pragma unroll
+            for (int i = 0; i < PP; ++i)
+                u[i] = rb + 4 * i < M ? *reinterpret_cast<const float4*>(base + static_cast<long>(rb + 4 * i) * ld)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < PP; ++i) {
+                x[i][0] = u[i].x; x[i][1] = u[i].y; x[i][2] = u[i].z; x[i][3] = u[i].w;
+            }
+        } else {
+            uint2 u[PP];
+#pragma unroll
+            for (int i = 0; i < PP; ++i)
+                u[i] = rb + 4 * i < M ? *reinterpret_cast<const uint2*>(base + static_cast<long>(rb + 4 * i) * ld)
+                                      : make_uint2(0u, 0u);
+#pragma unroll
+            for (int i = 0; i < PP; ++i) {
+                const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[i].x));
+                const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[i].y));
+                x[i][0] = lo.x; x[i][1] = lo.y; x[i][2] = hi.x; x[i][3] = hi.y;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < PP; ++i)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                x[i][e] = (rb + 4 * i < M && e < nvc) ? ld_as_float<T>(base + static_cast<long>(rb + 4 * i) * ld + e)
+                                                      : 0.f;
+    }
+}
+
+template <typename T, int PP>
+__device__ __forceinline__ void store_pieces(T* base, long ld, int rb, int M, int nvc, const float (&x)[PP][4]) {
+    if (pieces_vec(base, ld, nvc)) {
+#pragma unroll
+        for (int i = 0; i < PP; ++i) {
+            if (rb + 4 * i >= M) continue;
+            T* p = base + static_cast<long>(rb + 4 * i) * ld;
+            if constexpr (sizeof(T) == 4) {
+                *reinterpret_cast<float4*>(p) = make_float4(x[i][0], x[i][1], x[i][2], x[i][3]);
+            } else {
+                __nv_bfloat162 lo = __floats2bfloat162_rn(x[i][0], x[i][1]);
+                __nv_bfloat162 hi = __floats2bfloat162_rn(x[i][2], x[i][3]);
+                *reinterpret_cast<uint2*>(p) =
+                    make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < PP; ++i)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (rb + 4 * i < M && e < nvc) st_from_float<T>(base + static_cast<long>(rb + 4 * i) * ld + e, x[i][e]);
+    }
+}
+
+template <int BN, int STAGES, typename T, bool SPLIT = false, bool TE = true>
+struct GemmSmem {
+    static constexpr int kElem = sizeof(T);
+    static constexpr int kBK = 128 / kElem;    // K per stage (one 128-B swizzle row)
+    static constexpr int kUK = 32 / kElem;     // K per tcgen05.mma
+    static constexpr int kAtom = 128 / kElem;  // MN elements per 128-B atom
+    static constexpr int kABytes = 128 * 128;
+    static constexpr int kBBytes = BN * 128;
+    static constexpr int kLoad = kABytes + kBBytes;          // bytes TMA brings per stage
+    static constexpr int kStage = kLoad * (SPLIT ? 2 : 1);   // + low-part copies for 3xTF32
+    static constexpr int kEpiBuf = TE ? 8 * 32 * 32 * 4 : 0; // per epilogue warp: one 32 x 32 fp32 chunk
+    static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 512 /*barriers*/ + kEpiBuf;
+    static constexpr int kThreads = SPLIT ? 448 : 320;       // TMA, MMA, 8 epilogue (+ 4 splitter) warps
+    static constexpr uint32_t kTmemCols = 2 * BN;            // double-buffered accumulator
+};
+
+// Epilogue of one 32 x 32 accumulator chunk: rows r0 .. r0+31 (one TMEM lane
+// quadrant), columns n .. n+31. tcgen05.ld gives one row per lane; the chunk
+// is transposed through the warp's 4 KB buffer (16-byte slots XOR-swizzled by
+// row: conflict-free both ways) so that lane l then owns columns
+// c = n + 4 (l & 7) .. c+3 of rows r0 + 4 i + (l >> 3), i = 0..7. Every global
+// access instruction of the warp then covers 4 rows x 128 B (fp32) / 64 B
+// (bf16) instead of touching 32 rows, and each lane keeps 8 independent
+// accesses in flight (all loads are issued before the first store).
+template <typename T, int PP>
+__device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, const uint32_t (&r)[32], uint4* buf, int lane,
+                                               int r0, int M, int n, int N, float lr, float alpha_eff, int ks,
+                                               float& s_aux, float& s_out) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        buf[lane * 8 + (k ^ (lane & 7))] = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+    __syncwarp();
+    const int kk = lane & 7, rs = lane >> 3;
+    const int c = n + 4 * kk;
+    const int nvc = min(max(N - c, 0), 4);
+    bool bad = false;
+#pragma unroll
+    for (int p0 = 0; p0 < 8; p0 += PP) {  // PP pieces per pass (register budget)
+    float a[PP][4];
+#pragma unroll
+    for (int i = 0; i < PP; ++i) {
+        const int rr = 4 * (p0 + i) + rs;
+        const uint4 u = buf[rr * 8 + (kk ^ (rr & 7))];
+        a[i][0] = __uint_as_float(u.x); a[i][1] = __uint_as_float(u.y);
+        a[i][2] = __uint_as_float(u.z); a[i][3] = __uint_as_float(u.w);
+    }
+    // row of piece i and its valid column count (computed, not kept in registers)
+    const int rb = r0 + rs + 4 * p0;
+
+    switch (ep.mode) {
+        case EPI_PARTIAL: {
+            store_pieces<float, PP>(ep.out32 + ks * ep.split_stride + c, ep.ld_out32, rb, M, nvc, a);
+            break;
+        }
+        case EPI_RESID: {
+            float x[PP][4];
+            load_pieces<T, PP>(static_cast<const T*>(ep.aux) + c, ep.ld_aux, rb, M, nvc, x);
+#pragma unroll
+            for (int i = 0; i < PP; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float v = x[i][e] - a[i][e];
+                    if constexpr (sizeof(T) == 2) v = __bfloat162float(__float2bfloat16_rn(v));  // as stored
+                    a[i][e] = v;
+                    s_aux = fmaf(x[i][e], x[i][e], s_aux);  // invalid elements: x = acc = 0
+                    s_out = fmaf(v, v, s_out);
+                }
+            store_pieces<T, PP>(static_cast<T*>(ep.out) + c, ep.ld_out, rb, M, nvc, a);
+            break;
+        }
+        case EPI_FWD_ACT: {
+            float b[1][4];
+            load_pieces<float, 1>(ep.bias + c, 0, 0, 1, nvc, b);
+#pragma unroll
+            for (int i = 0; i < PP; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) a[i][e] = ep.out_scale * act_fwd(ep.act, a[i][e] + b[0][e]);
+            store_pieces<T, PP>(static_cast<T*>(ep.out) + c, ep.ld_out, rb, M, nvc, a);
+            break;
+        }
+        case EPI_FWD_LINEAR: {
+            float b[1][4];
+            load_pieces<float, 1>(ep.bias + c, 0, 0, 1, nvc, b);
+#pragma unroll
+            for (int i = 0; i < PP; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) a[i][e] += b[0][e];
+            store_pieces<float, PP>(ep.out32 + c, ep.ld_out32, rb, M, nvc, a);
+            break;
+        }
+        case EPI_GRAD: {
+#pragma unroll
+            for (int i = 0; i < PP; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    a[i][e] *= ep.alpha;
+                    bad |= (e < nvc && rb + 4 * i < M) && !isfinite(a[i][e]);
+                }
+            store_pieces<float, PP>(ep.out32 + c, ep.ld_out32, rb, M, nvc, a);
+            break;
+        }
+        case EPI_GRAD_SGD: {
+            const int bj = ep.bias_col - c;  // bias column among this lane's four?
+            const bool has_b = bj >= 0 && bj < nvc;
+            const int nw = has_b ? bj : nvc;
+            float w[PP][4];
+            load_pieces<float, PP>(ep.out32 + c, ep.ld_out32, rb, M, nw, w);
+#pragma unroll
+            for (int i = 0; i < PP; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float g = a[i][e] * alpha_eff;
+                    bad |= (e < nw && rb + 4 * i < M) && !isfinite(g);
+                    w[i][e] -= lr * g;
+                }
+            store_pieces<float, PP>(ep.out32 + c, ep.ld_out32, rb, M, nw, w);
+            if (ep.shadow) store_pieces<__nv_bfloat16, PP>(ep.shadow + c, ep.ld_shadow, rb, M, nw, w);
+            if (has_b) {
+#pragma unroll
+                for (int i = 0; i < PP; ++i) {
+                    if (rb + 4 * i >= M) continue;
+                    float vb = 0.f;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) vb = e == bj ? a[i][e] : vb;  // static register indexing
+                    const float gb = vb * alpha_eff;
+                    if (!isfinite(gb) && ep.flag) atomicOr(ep.flag, 1u << (ep.flag_bit + 1));
+                    ep.bias32[rb + 4 * i] -= lr * gb;
+                }
+            }
+            break;
+        }
+        case EPI_ACTGRAD: {
+            float x[PP][4];
+            load_pieces<T, PP>(static_cast<const T*>(ep.aux) + c, ep.ld_aux, rb, M, nvc, x);
+#pragma unroll
+            for (int i = 0; i < PP; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) a[i][e] *= act_grad(ep.act, x[i][e]);
+            store_pieces<T, PP>(static_cast<T*>(ep.out) + c, ep.ld_out, rb, M, nvc, a);
+            break;
+        }
+        case EPI_EMA: {
+            float o[PP][4];
+            const float beta = ep.coef ? ep.coef[0] : ep.beta;
+            const float alpha = ep.coef ? ep.coef[1] : ep.alpha;
+            if (beta != 0.f) load_pieces<float, PP>(ep.out32 + c, ep.ld_out32, rb, M, nvc, o);
+#pragma unroll
+            for (int i = 0; i < PP; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) o[i][e] = (beta != 0.f ? beta * o[i][e] : 0.f) + alpha * a[i][e];
+            store_pieces<float, PP>(ep.out32 + c, ep.ld_out32, rb, M, nvc, o);
+            break;
+        }
+        case EPI_SUB: {
+            float o[PP][4];
+            load_pieces<float, PP>(ep.out32 + c, ep.ld_out32, rb, M, nvc, o);
+#pragma unroll
+            for (int i = 0; i < PP; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) o[i][e] -= a[i][e];
+            store_pieces<float, PP>(ep.out32 + c, ep.ld_out32, rb, M, nvc, o);
+            break;
+        }
+        case EPI_AXPY: {
+            float w[PP][4];
+            load_pieces<float, PP>(ep.out32 + c, ep.ld_out32, rb, M, nvc, w);
+#pragma unroll
+            for (int i = 0; i < PP; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) w[i][e] += ep.alpha * a[i][e];
+            store_pieces<float, PP>(ep.out32 + c, ep.ld_out32, rb, M, nvc, w);
+            if (ep.shadow) store_pieces<__nv_bfloat16, PP>(ep.shadow + c, ep.ld_shadow, rb, M, nvc, w);
+            break;
+        }
+        default:
+            break;
+    }
+    }  // passes
+    __syncwarp();  // the buffer is free for the next chunk
+    return bad;
+}
+
 // 32 consecutive values of one row -> memory, vectorised when aligned. The
 // ragged path is fully unrolled with predication so v[] stays in registers.
 template <typename T>
@@ -190,24 +444,10 @@ __device__ __forceinline__ void load_row32(const T* src, float (&v)[32], int val
     }
 }
 
-template <int BN, int STAGES, typename T, bool SPLIT = false>
-struct GemmSmem {
-    static constexpr int kElem = sizeof(T);
-    static constexpr int kBK = 128 / kElem;    // K per stage (one 128-B swizzle row)
-    static constexpr int kUK = 32 / kElem;     // K per tcgen05.mma
-    static constexpr int kAtom = 128 / kElem;  // MN elements per 128-B atom
-    static constexpr int kABytes = 128 * 128;
-    static constexpr int kBBytes = BN * 128;
-    static constexpr int kLoad = kABytes + kBBytes;          // bytes TMA brings per stage
-    static constexpr int kStage = kLoad * (SPLIT ? 2 : 1);   // + low-part copies for 3xTF32
-    static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 512 /*barriers*/;
-    static constexpr int kThreads = SPLIT ? 448 : 320;       // TMA, MMA, 8 epilogue (+ 4 splitter) warps
-    static constexpr uint32_t kTmemCols = 2 * BN;            // double-buffered accumulator
-};
-
-// Epilogue of one 32-column chunk of one accumulator row.
+// Row-wise epilogue of one 32-column chunk of one accumulator row (lane = row):
+// bf16-output modes (FWD_ACT, ACTGRAD, RESID), see gemm_epi_transposed().
 template <typename T>
-__device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, float (&v)[32], int row, int n, int valid,
+__device__ __forceinline__ bool epilogue_chunk_rows(const GemmEpi& ep, float (&v)[32], int row, int n, int valid,
                                                float lr, float alpha_eff, int ks, float& s_aux, float& s_out) {
     bool bad = false;
     switch (ep.mode) {
@@ -322,6 +562,15 @@ __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, float (&v)[32]
     return bad;
 }
 
+// Epilogue style per mode. fp32 outputs (the read-modify-write weight updates
+// above all) use the transposed layout: it cuts the L1 wavefronts of a 32 x 32
+// chunk 8x and took the hidden dW GEMM (GRAD_SGD) from 22.9 to 18.6 us. For the
+// bf16-output modes the row-wise form measured faster (and kernels built with
+// the transposed code run their mainloop ~6% slower), so they keep it.
+inline bool gemm_epi_transposed(int mode) {
+    return !(mode == EPI_FWD_ACT || mode == EPI_ACTGRAD || mode == EPI_RESID);
+}
+
 // Persistent, warp-specialised tcgen05 GEMM. grid <= #tiles; CTA c handles
 // tiles c, c + grid, ... (m fastest). Roles:
 //   warp 0      TMA producer (one elected lane), STAGES-deep smem ring
@@ -336,11 +585,11 @@ __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, float (&v)[32]
 // operand x as hi = x with the low 13 mantissa bits cleared (exact TF32, in
 // place) and lo = x - hi (exact in fp32) next to it; the MMA warp then
 // accumulates hi*hi + hi*lo + lo*hi: relative error ~2^-21 instead of 2^-11.
-template <typename T, int BN, int STAGES, bool A_MN, bool B_MN, bool SPLIT>
-__global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
+template <typename T, int BN, int STAGES, bool A_MN, bool B_MN, bool SPLIT, bool TE>
+__global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, GemmEpi ep) {
-    using S = GemmSmem<BN, STAGES, T, SPLIT>;
+    using S = GemmSmem<BN, STAGES, T, SPLIT, TE>;
     constexpr bool kTf32 = OpTraits<T>::kTf32;
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
     static_assert(!SPLIT || kTf32, "3xTF32 split needs fp32 operands");
@@ -479,6 +728,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
         // per-row work of each thread
         const int quad = warp & 3;
         const int eset = (warp - 2) >> 2;
+        uint4* ebuf = reinterpret_cast<uint4*>(smem + STAGES * S::kStage + 512) + (warp - 2) * 256;
         float lr = 0.f, alpha_eff = ep.alpha;
         if (ep.mode == EPI_GRAD_SGD) {
             lr = ep.lr[ep.step ? *ep.step : 0];
@@ -510,21 +760,26 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT>::kThreads, 1)
                 }
                 for (long o = 0; o < bytes; o += 128) prefetch_l2(src + o);
             }
-            mbar_wait(&tfull[acc], (local >> 1) & 1);
+            mbar_wait_sleep(&tfull[acc], (local >> 1) & 1);
             if (warp == 2 && lane == 0) PNB_TRACE(4);
             tc_fence_after();
 #pragma unroll 1
             for (int c = eset; c < BN / 32; c += 2) {
                 const int n = n0 + c * 32;
                 if (n >= N) break;  // warp-uniform
+                if (m0 + quad * 32 >= M) break;  // warp-uniform: no rows of this quadrant
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c * 32, r);
                 tmem_ld_wait();
-                if (!row_ok) continue;
-                float v[32];
+                if constexpr (TE) {
+                    bad |= epilogue_chunk<T, SPLIT ? 4 : 8>(ep, r, ebuf, lane, m0 + quad * 32, M, n, N, lr, alpha_eff,
+                                                            ks, s_aux, s_out);
+                } else if (row_ok) {
+                    float v[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                bad |= epilogue_chunk<T>(ep, v, row, n, min(32, N - n), lr, alpha_eff, ks, s_aux, s_out);
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                    bad |= epilogue_chunk_rows<T>(ep, v, row, n, min(32, N - n), lr, alpha_eff, ks, s_aux, s_out);
+                }
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);

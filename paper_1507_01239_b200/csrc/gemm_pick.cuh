@@ -1,0 +1,68 @@
+// Kernel instantiation + launch-attribute setup for one operand type /
+// epilogue style. The GEMM kernels are instantiated in six translation units
+// (gemm_k_*.cu: {bf16, tf32, 3xTF32} x {row-wise, transposed epilogue}) so
+// they compile in parallel; gemm.cu picks among them at plan time.
+#pragma once
+#include <stdexcept>
+
+#include "gemm.cuh"
+#include "runtime.h"
+
+namespace pnb {
+
+using KernelFn = void (*)(CUtensorMap, CUtensorMap, int, int, int, GemmEpi);
+
+namespace gemm_pick_detail {
+
+template <int BN, bool SPLIT>
+constexpr int stages_for() {
+    if (SPLIT) return BN == 256 ? 2 : (BN == 128 ? 3 : 4);
+    return BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+}
+
+template <typename T, int BN, bool AMN, bool BMN, bool SPLIT, bool TE>
+KernelFn kernel_ptr(int* smem) {
+    constexpr int ST = stages_for<BN, SPLIT>();
+    *smem = GemmSmem<BN, ST, T, SPLIT, TE>::kBytes;
+    auto k = &gemm_tc_kernel<T, BN, ST, AMN, BMN, SPLIT, TE>;
+    static bool configured = false;
+    if (!configured) {
+        CUDA_THROW(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem));
+        configured = true;
+    }
+    return reinterpret_cast<KernelFn>(k);
+}
+
+template <typename T, int BN, bool SPLIT, bool TE>
+KernelFn pick_major(bool amn, bool bmn, int* smem) {
+    if (!amn && !bmn) return kernel_ptr<T, BN, false, false, SPLIT, TE>(smem);
+    if (amn && bmn) return kernel_ptr<T, BN, true, true, SPLIT, TE>(smem);
+    if (!amn && bmn) return kernel_ptr<T, BN, false, true, SPLIT, TE>(smem);
+    return kernel_ptr<T, BN, true, false, SPLIT, TE>(smem);
+}
+
+template <typename T, bool SPLIT, bool TE>
+KernelFn pick(int bn, bool amn, bool bmn, int* smem) {
+    switch (bn) {
+        case 256: return pick_major<T, 256, SPLIT, TE>(amn, bmn, smem);
+        case 128: return pick_major<T, 128, SPLIT, TE>(amn, bmn, smem);
+        default: return pick_major<T, 64, SPLIT, TE>(amn, bmn, smem);
+    }
+}
+
+}  // namespace gemm_pick_detail
+
+// one per gemm_k_*.cu
+KernelFn gemm_pick_bf16_r(int bn, bool amn, bool bmn, int* smem);
+KernelFn gemm_pick_bf16_t(int bn, bool amn, bool bmn, int* smem);
+KernelFn gemm_pick_f32_r(int bn, bool amn, bool bmn, int* smem);
+KernelFn gemm_pick_f32_t(int bn, bool amn, bool bmn, int* smem);
+KernelFn gemm_pick_split_r(int bn, bool amn, bool bmn, int* smem);
+KernelFn gemm_pick_split_t(int bn, bool amn, bool bmn, int* smem);
+
+#define PNB_GEMM_PICK(name, T, SPLIT, TE)                                     \
+    KernelFn gemm_pick_##name(int bn, bool amn, bool bmn, int* smem) {        \
+        return gemm_pick_detail::pick<T, SPLIT, TE>(bn, amn, bmn, smem);      \
+    }
+
+}  // namespace pnb

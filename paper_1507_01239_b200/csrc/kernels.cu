@@ -163,26 +163,50 @@ __global__ void ce_reduce_kernel(const float* __restrict__ ce_rows, long B, doub
 
 // db = colsum(dz)/B (network.cpp:203-208); finite check (optimizer.cpp:26-28);
 // SGD b -= lr*db (optimizer.cpp:32-34) when bias != null; db stored when gb != null.
+// Column sums of dz (B x C): one block per 2 x 16-byte column vectors, 128 row lanes
+// each keeping several 16-byte loads in flight, a fixed shuffle + shared-memory tree
+// (deterministic). g = sum / B; SGD: bias -= lr g; NG: gb = g.
 template <typename T>
-__global__ void bias_grad_kernel(const T* __restrict__ dz, long lddz, long B, long C, float* __restrict__ bias,
-                                 float* __restrict__ gb, const float* __restrict__ lr, const int* __restrict__ step,
-                                 unsigned* __restrict__ flags, unsigned bit) {
-    __shared__ float sh[32][33];
-    const long j = blockIdx.x * 32 + threadIdx.x;
-    float acc = 0.f;
-    if (j < C) {
-#pragma unroll 8
-        for (long b = threadIdx.y; b < B; b += 32) acc += to_f<T>(dz[b * lddz + j]);
+__global__ void __launch_bounds__(256) bias_grad_kernel(const T* __restrict__ dz, long lddz, long B, long C,
+                                                        float* __restrict__ bias, float* __restrict__ gb,
+                                                        const float* __restrict__ lr, const int* __restrict__ step,
+                                                        unsigned* __restrict__ flags, unsigned bit) {
+    constexpr int VE = 16 / sizeof(T);
+    __shared__ float red[8][2 * VE];
+    const int t = threadIdx.x, cv = t & 1, rl = t >> 1;
+    const long c0 = (blockIdx.x * 2L + cv) * VE;
+    float acc[VE];
+#pragma unroll
+    for (int e = 0; e < VE; ++e) acc[e] = 0.f;
+    if (c0 < C) {
+        const T* p = dz + c0;
+#pragma unroll 4
+        for (long b = rl; b < B; b += 128) {
+            const uint4 u = *reinterpret_cast<const uint4*>(p + b * lddz);
+            const T* v = reinterpret_cast<const T*>(&u);
+#pragma unroll
+            for (int e = 0; e < VE; ++e) acc[e] += to_f<T>(v[e]);
+        }
     }
-    sh[threadIdx.y][threadIdx.x] = acc;
+#pragma unroll
+    for (int o = 2; o < 32; o <<= 1)
+#pragma unroll
+        for (int e = 0; e < VE; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    if ((t & 31) < 2)
+#pragma unroll
+        for (int e = 0; e < VE; ++e) red[t >> 5][cv * VE + e] = acc[e];
     __syncthreads();
-    if (threadIdx.y == 0 && j < C) {
-        float s = 0.f;
-        for (int r = 0; r < 32; ++r) s += sh[r][threadIdx.x];
-        const float g = s * (1.f / static_cast<float>(B));
-        if (!isfinite(g) && flags) atomicOr(flags, 1u << bit);
-        if (gb) gb[j] = g;
-        if (bias) bias[j] -= lr[step ? *step : 0] * g;
+    if (t < 2 * VE) {
+        const long j = blockIdx.x * 2L * VE + t;
+        if (j < C) {
+            float s = 0.f;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) s += red[w][t];
+            const float g = s * (1.f / static_cast<float>(B));
+            if (!isfinite(g) && flags) atomicOr(flags, 1u << bit);
+            if (gb) gb[j] = g;
+            if (bias) bias[j] -= lr[step ? *step : 0] * g;
+        }
     }
 }
 
@@ -255,7 +279,8 @@ void launch_ce_reduce(const float* ce_rows, long B, double* d_ce, int* step, int
 
 void launch_bias_grad(const void* dz, long lddz, long B, long C, bool f32, float* bias, float* gb, const float* lr,
                       const int* step, unsigned* flags, unsigned bit, cudaStream_t s) {
-    dim3 grid((C + 31) / 32), block(32, 32);
+    const long cpb = 2 * (f32 ? 4 : 8);  // columns per block
+    dim3 grid(static_cast<unsigned>((C + cpb - 1) / cpb)), block(256);
     if (f32)
         bias_grad_kernel<float><<<grid, block, 0, s>>>(static_cast<const float*>(dz), lddz, B, C, bias, gb, lr, step,
                                                        flags, bit);

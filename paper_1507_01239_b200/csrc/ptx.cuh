@@ -45,6 +45,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Long waits (the epilogue warps idle through a whole mainloop): the thread
+// is suspended in try_wait until the phase completes (or the hint, in ns,
+// elapses) instead of spinning against the TMA / MMA warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(addr),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }

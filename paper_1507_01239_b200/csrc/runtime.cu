@@ -694,11 +694,12 @@ void Replica::enqueue_step(cudaStream_t s) {
         tmark("fwd", s);
         if (ng) ng_coeff_kernel<<<1, 1, 0, s>>>(tdev, ng_decay, 1.0 / static_cast<double>(B), coef);
         for (int l = L - 1; l >= 0; --l) {
-            launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
-                             ng ? grads + b_off[l] : nullptr, d_lr, d_step, d_flags, 2 * l + 1, s);
             if (l > 0) gemm_launch(da[l], s);
             CUDA_THROW(cudaEventRecord(ev_bwd[l], s));
             CUDA_THROW(cudaStreamWaitEvent(side, ev_bwd[l], 0));
+            // the bias gradient is off the dz chain: side stream, before dW_l
+            launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
+                             ng ? grads + b_off[l] : nullptr, d_lr, d_step, d_flags, 2 * l + 1, side);
             gemm_launch(dw[l], side);
             tmark("dw" + std::to_string(l), side);
             if (ng) {

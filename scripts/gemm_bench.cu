@@ -1,24 +1,31 @@
 // GEMM microbenchmark (warm L2, CUDA events, 20 reps) over the trainer's shapes.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1507_01239_b200/csrc -I include \
-//   scripts/gemm_bench.cu -o scripts/gemm_bench.bin -Lpaper_1507_01239_b200 -lparnn_b200 -Xlinker -rpath ...
+//   scripts/gemm_bench.cu -o scripts/gemm_bench.bin
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
-#include "runtime.h"
+#include "../paper_1507_01239_b200/csrc/gemm.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_bf16_r.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_bf16_t.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_f32_r.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_f32_t.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_split_r.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_split_t.cu"
 using namespace pnb;
 int main(int argc, char** argv) {
     int bnf = argc > 1 ? atoi(argv[1]) : 0;
-    struct Case { const char* name; int prec; bool amn, bmn; int M, N, K; };
+    struct Case { const char* name; int prec; bool amn, bmn; int M, N, K; int mode; };
     std::vector<Case> cases = {
-        {"fwd hidden 1024x2048x2048", 0, false, false, 1024, 2048, 2048},
-        {"fwd out    1024x8806x2048", 0, false, false, 1024, 8806, 2048},
-        {"dW hidden  2048x2048x1024", 0, true, true, 2048, 2048, 1024},
-        {"dW out     8806x2048x1024", 0, true, true, 8806, 2048, 1024},
-        {"dA hidden  1024x2048x2048", 0, false, true, 1024, 2048, 2048},
-        {"dA out     1024x2048x8806", 0, false, true, 1024, 2048, 8806},
-        {"big        8192x8192x8192", 0, false, false, 8192, 8192, 8192},
-        {"f32 trsm   8678x2049x128 ", 2, false, true, 8678, 2049, 128},
-        {"f32 trail  8678x8678x128 ", 2, false, false, 8678, 8678, 128},
+        {"fwd hidden 1024x2048x2048 ACT ", 0, false, false, 1024, 2048, 2048, EPI_FWD_ACT},
+        {"fwd out    1024x8806x2048 LIN ", 0, false, false, 1024, 8806, 2048, EPI_FWD_LINEAR},
+        {"dW hidden  2048x2048x1024 SGD ", 0, true, true, 2048, 2048, 1024, EPI_GRAD_SGD},
+        {"dW out     8806x2048x1024 SGD ", 0, true, true, 8806, 2048, 1024, EPI_GRAD_SGD},
+        {"dA hidden  1024x2048x2048 AGR ", 0, false, true, 1024, 2048, 2048, EPI_ACTGRAD},
+        {"dA out     1024x2048x8806 AGR ", 0, false, true, 1024, 2048, 8806, EPI_ACTGRAD},
+        {"dW hidden  2048x2048x1024 GRAD", 0, true, true, 2048, 2048, 1024, EPI_GRAD},
+        {"big        8192x8192x8192 GRAD", 0, false, false, 8192, 8192, 8192, EPI_GRAD},
+        {"f32 trsm   8678x2049x128  SUB ", 2, false, true, 8678, 2049, 128, EPI_SUB},
+        {"f32 trail  8678x8678x128  SUB ", 2, false, false, 8678, 8678, 128, EPI_SUB},
     };
     void *A, *B;
     float* C;
@@ -26,15 +33,33 @@ int main(int argc, char** argv) {
     cudaMalloc(&A, maxe * 4);
     cudaMalloc(&B, maxe * 4);
     cudaMalloc(&C, maxe * 4);
+    void *C2, *C3;
+    float* bias;
+    cudaMalloc(&C2, maxe * 4);
+    cudaMalloc(&C3, maxe * 4);
+    cudaMalloc(&bias, 65536 * 4);
+    cudaMemset(C, 0, maxe * 4);
+    cudaMemset(C2, 0, maxe * 4);
+    cudaMemset(C3, 0, maxe * 4);
+    cudaMemset(bias, 0, 65536 * 4);
     cudaMemset(A, 0, maxe * 4);
     cudaMemset(B, 0, maxe * 4);
     int sms = 148;
     for (auto& c : cases) {
         GemmPlan p;
         GemmEpi e;
-        e.mode = EPI_GRAD;
+        e.mode = c.mode;
         e.out32 = C;
         e.ld_out32 = (c.N + 31) / 32 * 32;
+        e.out = C2;
+        e.ld_out = e.ld_out32;
+        e.aux = C3;
+        e.ld_aux = e.ld_out32;
+        e.bias = bias;
+        e.shadow = static_cast<__nv_bfloat16*>(C2);
+        e.ld_shadow = e.ld_out32;
+        e.lr = bias;
+        e.step = nullptr;
         long lda = c.amn ? (c.M + 31) / 32 * 32 : (c.K + 31) / 32 * 32;
         long ldb = c.bmn ? (c.N + 31) / 32 * 32 : (c.K + 31) / 32 * 32;
         gemm_plan(p, c.prec, c.amn, A, lda, c.bmn, B, ldb, c.M, c.N, c.K, e, sms, bnf);

@@ -7,6 +7,12 @@
 #include <vector>
 
 #include "../paper_1507_01239_b200/csrc/gemm.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_bf16_r.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_bf16_t.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_f32_r.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_f32_t.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_split_r.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_split_t.cu"
 
 using namespace pnb;
 
@@ -40,26 +46,27 @@ int main() {
                                {"dA   1024x2048x2048 ACTGRAD", false, true, 1024, 2048, 2048, EPI_ACTGRAD},
                                {"dW   2048x2048x1024 GRAD_SGD", true, true, 2048, 2048, 1024, EPI_GRAD_SGD},
                                {"dW   2048x2048x1024 GRAD", true, true, 2048, 2048, 1024, EPI_GRAD},
-                               {"dW128 2048x2048x1024 GRAD_SGD", true, true, 2048, 2048, 1024, 100 + EPI_GRAD_SGD}};
+                               {"dW128 2048x2048x1024 GRAD_SGD", true, true, 2048, 2048, 1024, 100 + EPI_GRAD_SGD},
+                               {"dAout 1024x2048x8806 ACTGRAD", false, true, 1024, 2048, 8806, EPI_ACTGRAD}};
     for (auto& c : cases) {
         GemmEpi e;
         const int force_bn = c.mode >= 100 ? 128 : 0;
         e.mode = c.mode % 100;
         e.act = 0;
         e.out = out;
-        e.ld_out = c.N;
+        e.ld_out = (c.N + 31) / 32 * 32;
         e.bias = bias;
         e.aux = A;
-        e.ld_aux = c.N;
+        e.ld_aux = (c.N + 31) / 32 * 32;
         e.out32 = w32;
-        e.ld_out32 = c.N;
+        e.ld_out32 = (c.N + 31) / 32 * 32;
         e.shadow = static_cast<__nv_bfloat16*>(out);
-        e.ld_shadow = c.N;
+        e.ld_shadow = (c.N + 31) / 32 * 32;
         e.lr = lr;
         e.step = step;
         e.alpha = 1e-3f;
         GemmPlan p;
-        long lda = c.amn ? c.M : c.K, ldb = c.bmn ? c.N : c.K;
+        long lda = ((c.amn ? c.M : c.K) + 31) / 32 * 32, ldb = ((c.bmn ? c.N : c.K) + 31) / 32 * 32;
         gemm_plan(p, 0, c.amn, A, lda, c.bmn, Bm, ldb, c.M, c.N, c.K, e, 148, force_bn);
         for (int cold = 0; cold < 2; ++cold) {
             for (int rep = 0; rep < 3; ++rep) {
