@@ -655,9 +655,13 @@ void side_plans(Replica& r, LrSide& sd, const void* X) {
         const int NR = sd.ns * R;  // bf16: [W_hi; W_lo]
         const int bn = NR <= 64 ? 64 : (NR <= 128 ? 128 : 256);
         const int tiles = static_cast<int>((B + 127) / 128);
-        e.ksplit = std::max(1, sms / tiles);
         const int bk = r.f32() ? 32 : 64;
         const int nk = static_cast<int>((sd.dx + bk - 1) / bk);
+        // ~kKbPerSplit k-blocks per CTA: enough work per CTA to amortise its prologue and
+        // partial-tile write, few CTAs so the chain does not crowd the concurrent GEMMs
+        int kb_per = 32;
+        if (const char* v = std::getenv("PARNN_LR_HKB")) kb_per = std::max(1, std::atoi(v));  // tuning aid
+        e.ksplit = std::max(1, std::min(sms / tiles, (nk + kb_per - 1) / kb_per));
         const int per = (nk + e.ksplit - 1) / e.ksplit;
         const int S = (nk + per - 1) / per;
         if (sd.hpart) cudaFree(sd.hpart);
@@ -789,6 +793,7 @@ void lr_precondition_side(Replica& r, LrSide& sd, cudaStream_t s) {
                                                          static_cast<bf16*>(sd.xhat), sd.ldxh);
     CUDA_THROW(cudaGetLastError());
     gemm_launch(sd.xg, s);
+    // (folding this into the residual GEMM's last CTA measured ~5 us/step slower)
     lr_stats_kernel<<<1, 32, 0, s>>>(sd.xpart, static_cast<int>(gemm_launch_grid(sd.xg).x), sd.rpart, sd.nrb, sd.R,
                                      sd.in, r.B, sd.st);
     CUDA_THROW(cudaGetLastError());

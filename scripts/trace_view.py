@@ -29,7 +29,7 @@ def demangle(n):
 
 
 def short(n):
-    n = demangle(n)
+    n = demangle(n).replace("(anonymous namespace)::", "")
     n = re.sub(r"\(.*", "", n)
     n = n.replace("void ", "").replace("pnb::", "").replace("(anonymous namespace)::", "")
     m = re.match(r"gemm_tc_kernel<(.*)>", n)
