@@ -444,122 +444,79 @@ __device__ __forceinline__ void load_row32(const T* src, float (&v)[32], int val
     }
 }
 
-// Row-wise epilogue of one 32-column chunk of one accumulator row (lane = row):
-// bf16-output modes (FWD_ACT, ACTGRAD, RESID), see gemm_epi_transposed().
+// Row-wise epilogue (lane = row) for the bf16-output modes FWD_ACT, ACTGRAD
+// and RESID, see gemm_epi_transposed(). Their second operand x (the bias of
+// FWD_ACT, the activations of ACTGRAD, X of RESID) does not depend on the
+// accumulator, so its 32 values per chunk are loaded into raw registers before
+// the accumulator is ready (for a tile's first chunk: before the mainloop ends)
+// and converted only when used.
 template <typename T>
-__device__ __forceinline__ bool epilogue_chunk_rows(const GemmEpi& ep, float (&v)[32], int row, int n, int valid,
-                                               float lr, float alpha_eff, int ks, float& s_aux, float& s_out) {
-    bool bad = false;
-    switch (ep.mode) {
-        case EPI_PARTIAL: {
-            store_row32<float>(ep.out32 + ks * ep.split_stride + row * ep.ld_out32 + n, v, valid);
-            break;
-        }
-        case EPI_RESID: {
-            float a[32];
-            load_row32<T>(static_cast<const T*>(ep.aux) + row * ep.ld_aux + n, a, valid);
+__device__ __forceinline__ bool rows_x_fetch(const GemmEpi& ep, int row, int n, int valid, uint4 (&raw)[8]) {
+    const bool fp = ep.mode == EPI_FWD_ACT;  // fp32 bias; else T-typed aux row
+    const char* src = fp ? reinterpret_cast<const char*>(ep.bias + n)
+                         : static_cast<const char*>(ep.aux) + (row * ep.ld_aux + n) * static_cast<long>(sizeof(T));
+    const bool ok = valid == 32 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    if (ok) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        if (fp || sizeof(T) == 4) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                v[j] = a[j] - v[j];
-                if constexpr (sizeof(T) == 2) v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));  // as stored
-                s_aux = fmaf(a[j], a[j], s_aux);
-                s_out = fmaf(v[j], v[j], s_out);  // padding columns: a = acc = 0
-            }
-            store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
-            break;
-        }
-        case EPI_FWD_ACT: {
-            float b[32];
-            load_row32<float>(ep.bias + n, b, valid);  // 8 vector loads, broadcast across the warp
+            for (int i = 0; i < 8; ++i) raw[i] = s4[i];
+        } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = ep.out_scale * act_fwd(ep.act, v[j] + b[j]);
-            store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
-            break;
+            for (int i = 0; i < 4; ++i) raw[i] = s4[i];
         }
-        case EPI_FWD_LINEAR: {
-            float b[32];
-            load_row32<float>(ep.bias + n, b, valid);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += b[j];
-            store_row32<float>(ep.out32 + row * ep.ld_out32 + n, v, valid);
-            break;
-        }
-        case EPI_GRAD: {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                v[j] *= ep.alpha;
-                bad |= (j < valid) && !isfinite(v[j]);
-            }
-            store_row32<float>(ep.out32 + row * ep.ld_out32 + n, v, valid);
-            break;
-        }
-        case EPI_GRAD_SGD: {
-            float w[32];
-            float* wp = ep.out32 + row * ep.ld_out32 + n;
-            const int bj = ep.bias_col - n;  // bias column inside this chunk?
-            const int wvalid = (bj >= 0 && bj < valid) ? bj : valid;
-            load_row32<float>(wp, w, wvalid);
-            const float alpha = alpha_eff;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const float g = v[j] * alpha;
-                bad |= (j < wvalid) && !isfinite(g);
-                w[j] -= lr * g;
-            }
-            store_row32<float>(wp, w, wvalid);
-            if (ep.shadow) store_row32<__nv_bfloat16>(ep.shadow + row * ep.ld_shadow + n, w, wvalid);
-            if (bj >= 0 && bj < valid) {
-                float vb = 0.f;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) vb = j == bj ? v[j] : vb;  // static register indexing
-                const float gb = vb * alpha;
-                if (!isfinite(gb) && ep.flag) atomicOr(ep.flag, 1u << (ep.flag_bit + 1));
-                ep.bias32[row] -= lr * gb;
-            }
-            break;
-        }
-        case EPI_ACTGRAD: {
-            float a[32];
-            load_row32<T>(static_cast<const T*>(ep.aux) + row * ep.ld_aux + n, a, valid);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] *= act_grad(ep.act, a[j]);
-            store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
-            break;
-        }
-        case EPI_EMA: {
-            float o[32];
-            float* op = ep.out32 + row * ep.ld_out32 + n;
-            const float beta = ep.coef ? ep.coef[0] : ep.beta;
-            const float alpha = ep.coef ? ep.coef[1] : ep.alpha;
-            if (beta != 0.f) load_row32<float>(op, o, valid);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) o[j] = (beta != 0.f ? beta * o[j] : 0.f) + alpha * v[j];
-            store_row32<float>(op, o, valid);
-            break;
-        }
-        case EPI_SUB: {
-            float o[32];
-            float* op = ep.out32 + row * ep.ld_out32 + n;
-            load_row32<float>(op, o, valid);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) o[j] -= v[j];
-            store_row32<float>(op, o, valid);
-            break;
-        }
-        case EPI_AXPY: {
-            float w[32];
-            float* wp = ep.out32 + row * ep.ld_out32 + n;
-            load_row32<float>(wp, w, valid);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) w[j] += ep.alpha * v[j];
-            store_row32<float>(wp, w, valid);
-            if (ep.shadow) store_row32<__nv_bfloat16>(ep.shadow + row * ep.ld_shadow + n, w, valid);
-            break;
-        }
-        default:
-            break;
     }
-    return bad;
+    return ok;
+}
+
+template <typename S>
+__device__ __forceinline__ void rows_x_convert(const uint4 (&raw)[8], float (&x)[32]) {
+    if constexpr (sizeof(S) == 4) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            x[4 * i] = __uint_as_float(raw[i].x); x[4 * i + 1] = __uint_as_float(raw[i].y);
+            x[4 * i + 2] = __uint_as_float(raw[i].z); x[4 * i + 3] = __uint_as_float(raw[i].w);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t w[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+                x[8 * i + 2 * j] = f.x;
+                x[8 * i + 2 * j + 1] = f.y;
+            }
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void epilogue_chunk_rows(const GemmEpi& ep, float (&v)[32], int row, int n, int valid,
+                                                    const uint4 (&raw)[8], bool have, float& s_aux, float& s_out) {
+    float x[32];
+    if (ep.mode == EPI_FWD_ACT) {
+        if (have) rows_x_convert<float>(raw, x);
+        else load_row32<float>(ep.bias + n, x, valid);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = ep.out_scale * act_fwd(ep.act, v[j] + x[j]);
+    } else {
+        if (have) rows_x_convert<T>(raw, x);
+        else load_row32<T>(static_cast<const T*>(ep.aux) + row * ep.ld_aux + n, x, valid);
+        if (ep.mode == EPI_ACTGRAD) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= act_grad(ep.act, x[j]);
+        } else {  // EPI_RESID
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                v[j] = x[j] - v[j];
+                if constexpr (sizeof(T) == 2) v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));  // as stored
+                s_aux = fmaf(x[j], x[j], s_aux);
+                s_out = fmaf(v[j], v[j], s_out);  // padding columns: x = acc = 0
+            }
+        }
+    }
+    store_row32<T>(static_cast<T*>(ep.out) + row * ep.ld_out + n, v, valid);
 }
 
 // Epilogue style per mode. fp32 outputs (the read-modify-write weight updates
@@ -760,6 +717,13 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                 }
                 for (long o = 0; o < bytes; o += 128) prefetch_l2(src + o);
             }
+            // row-wise modes: the first chunk's x operand is fetched before the accumulator is ready
+            uint4 xraw[8];
+            bool xhave = false;
+            if constexpr (!TE) {
+                const int n = n0 + eset * 32;
+                if (row_ok && n < N) xhave = rows_x_fetch<T>(ep, row, n, min(32, N - n), xraw);
+            }
             mbar_wait_sleep(&tfull[acc], (local >> 1) & 1);
             if (warp == 2 && lane == 0) PNB_TRACE(4);
             tc_fence_after();
@@ -778,7 +742,10 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     float v[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                    bad |= epilogue_chunk_rows<T>(ep, v, row, n, min(32, N - n), lr, alpha_eff, ks, s_aux, s_out);
+                    epilogue_chunk_rows<T>(ep, v, row, n, min(32, N - n), xraw, xhave, s_aux, s_out);
+                    // next chunk of this warp: its x loads overlap the next TMEM load
+                    const int nn = n + 64;
+                    xhave = nn < N && rows_x_fetch<T>(ep, row, nn, min(32, N - nn), xraw);
                 }
             }
             tc_fence_before();
