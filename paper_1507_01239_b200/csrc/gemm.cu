@@ -1,6 +1,7 @@
 // Host side of the tcgen05 GEMM: TMA tensor-map construction, tile-shape
 // selection and launch. See gemm.cuh for the kernel.
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -67,24 +68,43 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     const int bn = force_bn ? force_bn : choose_bn(M, N, num_sms);
     const uint32_t atom = f32 ? 32 : 64;  // elements per 128-B row
     const uint32_t bk = atom;
+    // split-K: round the factor so that every split owns >= 1 k-block
+    const int nk = static_cast<int>((K + bk - 1) / bk);
+    const int per = (nk + std::max(ep.ksplit, 1) - 1) / std::max(ep.ksplit, 1);
+    const int ksplit = (nk + per - 1) / per;
+    if (ksplit > 1 && ep.mode != EPI_PARTIAL) throw std::runtime_error("gemm: split-K needs EPI_PARTIAL");
+    const int tiles_m = (M + 127) / 128, tiles_n = (N + bn - 1) / bn;
+    // CTA pairs with 2-SM MMAs (256 x BN pair tiles, each SM loads its A rows and half
+    // of B): opt-in (PARNN_GEMM_PAIRS=1). Measured on the trainer's shapes it is no
+    // faster than single-CTA tiles (the mainloop is bound by MMA consumption, not by
+    // operand delivery), so the default stays 1-SM.
+    static const bool pairs_on = [] {
+        const char* v = std::getenv("PARNN_GEMM_PAIRS");
+        return v && v[0] == '1';
+    }();
+    p.mc = (!f32 && pairs_on && ksplit == 1 && !ep.lower && bn >= 128 && tiles_m >= 2) ? 2 : 1;
     // A(m,k): K-major buffer [M x K] or MN-major buffer [K x M].
     p.ta = a_mn ? make_tmap(A, f32, M, K, lda, atom, bk, true) : make_tmap(A, f32, K, M, lda, bk, 128);
-    p.tb = b_mn ? make_tmap(B, f32, N, K, ldb, atom, bk, true) : make_tmap(B, f32, K, N, ldb, bk, bn);
+    p.tb = b_mn ? make_tmap(B, f32, N, K, ldb, atom, bk, true) : make_tmap(B, f32, K, N, ldb, bk, bn / p.mc);
     p.M = M;
     p.N = N;
     p.K = K;
     p.ep = ep;
-    // split-K: round the factor so that every split owns >= 1 k-block
-    const int nk = static_cast<int>((K + bk - 1) / bk);
-    const int per = (nk + std::max(ep.ksplit, 1) - 1) / std::max(ep.ksplit, 1);
-    p.ep.ksplit = (nk + per - 1) / per;
-    if (p.ep.ksplit > 1 && ep.mode != EPI_PARTIAL) throw std::runtime_error("gemm: split-K needs EPI_PARTIAL");
-    const long tiles = static_cast<long>((N + bn - 1) / bn) * ((M + 127) / 128) * p.ep.ksplit;
-    p.grid = dim3(static_cast<unsigned>(std::min<long>(tiles, num_sms)), 1, 1);  // persistent
-    p.tiles = static_cast<int>(tiles);
+    p.ep.ksplit = ksplit;
+    if (p.mc == 2) {
+        const long pairs = static_cast<long>((tiles_m + 1) / 2) * tiles_n;
+        p.grid = dim3(static_cast<unsigned>(2 * std::min<long>(pairs, num_sms / 2)), 1, 1);
+        p.tiles = static_cast<int>(2 * pairs);
+    } else {
+        const long tiles = static_cast<long>(tiles_n) * tiles_m * ksplit;
+        p.grid = dim3(static_cast<unsigned>(std::min<long>(tiles, num_sms)), 1, 1);  // persistent
+        p.tiles = static_cast<int>(tiles);
+    }
     const bool te = gemm_epi_transposed(ep.mode);
     KernelFn fn;
-    if (split)
+    if (p.mc == 2)
+        fn = te ? gemm_pick_bf16_t_mc(bn, a_mn, b_mn, &p.smem) : gemm_pick_bf16_r_mc(bn, a_mn, b_mn, &p.smem);
+    else if (split)
         fn = te ? gemm_pick_split_t(bn, a_mn, b_mn, &p.smem) : gemm_pick_split_r(bn, a_mn, b_mn, &p.smem);
     else if (f32)
         fn = te ? gemm_pick_f32_t(bn, a_mn, b_mn, &p.smem) : gemm_pick_f32_r(bn, a_mn, b_mn, &p.smem);
@@ -102,14 +122,32 @@ thread_local int g_grid_cap = 0;
 void gemm_set_grid_cap(int cap) { g_grid_cap = cap; }
 
 dim3 gemm_launch_grid(const GemmPlan& p) {
-    // the persistent kernel covers every tile with any grid (tile = blockIdx + k * gridDim)
-    if (g_grid_cap > 0 && static_cast<int>(p.grid.x) > g_grid_cap) return dim3(g_grid_cap, 1, 1);
+    // the persistent kernel covers every tile with any grid (tile = blockIdx + k * gridDim;
+    // CTA pairs: pair = blockIdx / 2 + k * gridDim / 2, so the grid stays even)
+    if (g_grid_cap > 0 && static_cast<int>(p.grid.x) > g_grid_cap)
+        return dim3(p.mc == 2 ? std::max(2, g_grid_cap & ~1) : g_grid_cap, 1, 1);
     return p.grid;
 }
 
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {
     auto fn = reinterpret_cast<KernelFn>(p.fn);
-    fn<<<gemm_launch_grid(p), p.threads, p.smem, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.ep);
+    if (p.mc == 1) {
+        fn<<<gemm_launch_grid(p), p.threads, p.smem, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.ep);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = gemm_launch_grid(p);
+        cfg.blockDim = dim3(p.threads, 1, 1);
+        cfg.dynamicSmemBytes = p.smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_THROW(cudaLaunchKernelEx(&cfg, fn, p.ta, p.tb, p.M, p.N, p.K, p.ep));
+    }
     CUDA_THROW(cudaGetLastError());
 }
 

@@ -542,7 +542,7 @@ inline bool gemm_epi_transposed(int mode) {
 // operand x as hi = x with the low 13 mantissa bits cleared (exact TF32, in
 // place) and lo = x - hi (exact in fp32) next to it; the MMA warp then
 // accumulates hi*hi + hi*lo + lo*hi: relative error ~2^-21 instead of 2^-11.
-template <typename T, int BN, int STAGES, bool A_MN, bool B_MN, bool SPLIT, bool TE>
+template <typename T, int BN, int STAGES, bool A_MN, bool B_MN, bool SPLIT, bool TE, int MC>
 __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, GemmEpi ep) {
@@ -550,6 +550,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     constexpr bool kTf32 = OpTraits<T>::kTf32;
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
     static_assert(!SPLIT || kTf32, "3xTF32 split needs fp32 operands");
+    static_assert(MC == 1 || (MC == 2 && !SPLIT && !kTf32 && BN >= 128), "CTA pairs: bf16, BN >= 128");
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -564,7 +565,25 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     const int lane = threadIdx.x & 31;
     const int tiles_m = (M + 127) / 128;
     const int tiles_mn = tiles_m * ((N + BN - 1) / BN);
-    const int tiles = tiles_mn * ep.ksplit;  // split-K: tile = mn + tiles_mn * ks
+    // MC == 1: work item = tile (split-K: tile = mn + tiles_mn * ks), CTA b takes
+    // b, b + grid, ... MC == 2 (CTA pairs, 2-SM MMA): work item = a 256 x BN
+    // pair tile, pair p takes p, p + grid/2, ...; CTA rank r of the pair holds
+    // rows 128 r .. 128 r + 127 of it (A rows and accumulator) and half of the
+    // B tile (columns r BN/2 .. ); the leader (rank 0) issues the M = 256 MMAs.
+    const int tmp = (tiles_m + 1) / 2;
+    const int tiles = MC == 1 ? tiles_mn * ep.ksplit : tmp * ((N + BN - 1) / BN);
+    const int w0 = MC == 1 ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x) / 2;
+    const int wstep = MC == 1 ? static_cast<int>(gridDim.x) : static_cast<int>(gridDim.x) / 2;
+    const int rank = MC == 1 ? 0 : static_cast<int>(cluster_ctarank());
+    auto tile_mn = [&](int w, int& m0, int& n0) {
+        if (MC == 1) {
+            m0 = (w % tiles_m) * 128;
+            n0 = ((w % tiles_mn) / tiles_m) * BN;
+        } else {
+            m0 = (2 * (w % tmp) + rank) * 128;
+            n0 = (w / tmp) * BN;
+        }
+    };
     const int nk_all = (K + S::kBK - 1) / S::kBK;
     const int nk_per = (nk_all + ep.ksplit - 1) / ep.ksplit;
     auto tile_skipped = [&](int m0, int n0) { return ep.lower && n0 > m0 + 127; };
@@ -585,15 +604,21 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 256);
+            mbar_init(&tempty[i], MC == 1 ? 256 : 16);  // pairs: one arrive per epilogue warp of both CTAs
         }
         fence_barrier_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
     }
-    if (warp == 1) tmem_alloc<S::kTmemCols>(tslot);
+    if (warp == 1) {
+        if constexpr (MC == 2)
+            tmem_alloc2<S::kTmemCols>(tslot);
+        else
+            tmem_alloc<S::kTmemCols>(tslot);
+    }
     tc_fence_before();
     __syncthreads();
+    if constexpr (MC == 2) cluster_sync_all();  // the leader's barriers exist before the peer's loads / arrives
     tc_fence_after();
     const uint32_t tmem = *tslot;
     if (threadIdx.x == 0) PNB_TRACE(1);
@@ -602,8 +627,9 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
         // ---------------- TMA producer ----------------
         if (lane == 0) {
             int it = 0;  // global k-block counter (ring position)
-            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-                const int m0 = (tile % tiles_m) * 128, n0 = ((tile % tiles_mn) / tiles_m) * BN;
+            for (int tile = w0; tile < tiles; tile += wstep) {
+                int m0, n0;
+                tile_mn(tile, m0, n0);
                 if (tile_skipped(m0, n0)) continue;
                 int kb0, kb1;
                 krange(tile, kb0, kb1);
@@ -612,8 +638,29 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
                     uint8_t* sa = smem + s * S::kStage;
                     uint8_t* sb = sa + S::kABytes;
-                    mbar_arrive_expect_tx(&full[s], S::kLoad);
                     const int k0 = kb * S::kBK;
+                    if constexpr (MC == 2) {
+                        // own A rows + own half of B, bytes counted on the leader's full barrier
+                        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (S::kABytes + S::kBBytes / 2));
+                        const uint32_t fb = mapa_cluster(&full[s], 0);
+                        if constexpr (!A_MN) {
+                            tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
+                        } else {
+#pragma unroll
+                            for (int a = 0; a < 128 / S::kAtom; ++a)
+                                tma_load_2d_cg2(sa + a * (S::kBK * 128), &tmA, fb, m0 + a * S::kAtom, k0);
+                        }
+                        if constexpr (!B_MN) {
+                            tma_load_2d_cg2(sb, &tmB, fb, k0, n0 + rank * (BN / 2));
+                        } else {
+                            constexpr int nb = BN / 2 / S::kAtom;
+#pragma unroll
+                            for (int a = 0; a < nb; ++a)
+                                tma_load_2d_cg2(sb + a * (S::kBK * 128), &tmB, fb, n0 + (rank * nb + a) * S::kAtom, k0);
+                        }
+                        continue;
+                    }
+                    mbar_arrive_expect_tx(&full[s], S::kLoad);
                     if constexpr (!A_MN) {
                         tma_load_2d(sa, &tmA, &full[s], k0, m0);
                     } else {
@@ -630,11 +677,17 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     }
                 }
             }
+            if constexpr (MC == 2) {
+                // drain: every stage's last phase released by the leader's MMAs, so
+                // no remote arrive targets this CTA once it passes the exit barrier
+                for (int j = (it > STAGES ? it - STAGES : 0); j < it; ++j)
+                    mbar_wait(&empty[j % STAGES], (j / STAGES) & 1);
+            }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer ----------------
-        if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc(OpTraits<T>::kFmt, A_MN ? 1 : 0, B_MN ? 1 : 0, 128, BN);
+        // ---------------- MMA issuer (pairs: the leader only) ----------------
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = make_idesc(OpTraits<T>::kFmt, A_MN ? 1 : 0, B_MN ? 1 : 0, 128 * MC, BN);
             constexpr uint32_t kMnLayout = kTf32 ? 1 : 2;  // BASE32B for TF32 MN-major
             constexpr uint32_t kMnSbo = kTf32 ? 512 : 1024;
             auto desc_a = [&](uint32_t base, int k) {
@@ -646,8 +699,9 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                             : smem_desc_sw128(base + k * 32, 16, 1024);
             };
             int it = 0, local = 0;
-            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-                const int m0 = (tile % tiles_m) * 128, n0 = ((tile % tiles_mn) / tiles_m) * BN;
+            for (int tile = w0; tile < tiles; tile += wstep) {
+                int m0, n0;
+                tile_mn(tile, m0, n0);
                 if (tile_skipped(m0, n0)) continue;
                 const int acc = local & 1;
                 if (local >= 2) mbar_wait(&tempty[acc], ((local >> 1) - 1) & 1);
@@ -664,6 +718,10 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     const uint32_t sb = sa + S::kABytes;
 #pragma unroll
                     for (int k = 0; k < S::kBK / S::kUK; ++k) {
+                        if constexpr (MC == 2) {
+                            umma2_bf16(d, desc_a(sa, k), desc_b(sb, k), idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                            continue;
+                        }
                         umma<kTf32>(d, desc_a(sa, k), desc_b(sb, k), idesc, (kb != kb0 || k != 0) ? 1u : 0u);
                         if constexpr (SPLIT) {
                             const uint32_t sal = sa + S::kLoad, sbl = sb + S::kLoad;
@@ -671,9 +729,15 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                             umma<kTf32>(d, desc_a(sal, k), desc_b(sb, k), idesc, 1u);
                         }
                     }
-                    umma_commit(&empty[s]);
+                    if constexpr (MC == 2)
+                        umma_commit2_mc(&empty[s], 3);  // both CTAs' stage s is free again
+                    else
+                        umma_commit(&empty[s]);
                 }
-                umma_commit(&tfull[acc]);
+                if constexpr (MC == 2)
+                    umma_commit2_mc(&tfull[acc], 3);  // both CTAs' accumulator rows are ready
+                else
+                    umma_commit(&tfull[acc]);
                 PNB_TRACE(3);
                 ++local;
             }
@@ -695,8 +759,9 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
         bool bad = false;
         float s_aux = 0.f, s_out = 0.f;  // RESID sums (per thread, this CTA's tiles)
         int local = 0;
-        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-            const int m0 = (tile % tiles_m) * 128, n0 = ((tile % tiles_mn) / tiles_m) * BN;
+        for (int tile = w0; tile < tiles; tile += wstep) {
+            int m0, n0;
+            tile_mn(tile, m0, n0);
             if (tile_skipped(m0, n0)) continue;
             const int ks = tile / tiles_mn;
             const int acc = local & 1;
@@ -749,7 +814,12 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            if constexpr (MC == 2) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(mapa_cluster(&tempty[acc], 0));  // the leader's MMA reuses it
+            } else {
+                mbar_arrive(&tempty[acc]);
+            }
             if (warp == 2 && lane == 0) PNB_TRACE(5);
             ++local;
         }
@@ -781,8 +851,9 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
         // ---------------- 3xTF32 splitters (warps 10-13) ----------------
         const int t = threadIdx.x - 320;
         int it = 0;
-        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-            const int m0 = (tile % tiles_m) * 128, n0 = ((tile % tiles_mn) / tiles_m) * BN;
+        for (int tile = w0; tile < tiles; tile += wstep) {
+            int m0, n0;
+            tile_mn(tile, m0, n0);
             if (tile_skipped(m0, n0)) continue;
             int kb0, kb1;
             krange(tile, kb0, kb1);
@@ -809,7 +880,12 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc<S::kTmemCols>(tmem);
+    if constexpr (MC == 2) {
+        cluster_sync_all();
+        if (warp == 1) tmem_dealloc2<S::kTmemCols>(tmem);
+    } else {
+        if (warp == 1) tmem_dealloc<S::kTmemCols>(tmem);
+    }
     if (threadIdx.x == 0) PNB_TRACE(6);
 }
 

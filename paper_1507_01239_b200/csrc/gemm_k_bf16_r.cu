@@ -2,5 +2,5 @@
 #include "gemm_pick.cuh"
 
 namespace pnb {
-PNB_GEMM_PICK(bf16_r, __nv_bfloat16, false, false)
+PNB_GEMM_PICK(bf16_r, __nv_bfloat16, false, false, 1)
 }  // namespace pnb

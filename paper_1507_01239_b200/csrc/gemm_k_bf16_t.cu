@@ -2,5 +2,5 @@
 #include "gemm_pick.cuh"
 
 namespace pnb {
-PNB_GEMM_PICK(bf16_t, __nv_bfloat16, false, true)
+PNB_GEMM_PICK(bf16_t, __nv_bfloat16, false, true, 1)
 }  // namespace pnb

@@ -2,5 +2,5 @@
 #include "gemm_pick.cuh"
 
 namespace pnb {
-PNB_GEMM_PICK(f32_r, float, false, false)
+PNB_GEMM_PICK(f32_r, float, false, false, 1)
 }  // namespace pnb

@@ -2,5 +2,5 @@
 #include "gemm_pick.cuh"
 
 namespace pnb {
-PNB_GEMM_PICK(f32_t, float, false, true)
+PNB_GEMM_PICK(f32_t, float, false, true, 1)
 }  // namespace pnb

@@ -2,5 +2,5 @@
 #include "gemm_pick.cuh"
 
 namespace pnb {
-PNB_GEMM_PICK(split_r, float, true, false)
+PNB_GEMM_PICK(split_r, float, true, false, 1)
 }  // namespace pnb

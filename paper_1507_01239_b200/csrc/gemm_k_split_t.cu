@@ -2,5 +2,5 @@
 #include "gemm_pick.cuh"
 
 namespace pnb {
-PNB_GEMM_PICK(split_t, float, true, true)
+PNB_GEMM_PICK(split_t, float, true, true, 1)
 }  // namespace pnb

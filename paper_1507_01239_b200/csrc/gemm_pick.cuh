@@ -1,6 +1,7 @@
 // Kernel instantiation + launch-attribute setup for one operand type /
 // epilogue style. The GEMM kernels are instantiated in six translation units
-// (gemm_k_*.cu: {bf16, tf32, 3xTF32} x {row-wise, transposed epilogue}) so
+// (gemm_k_*.cu: {bf16, tf32, 3xTF32} x {row-wise, transposed epilogue}, plus
+// the bf16 CTA-pair kernels with 2-SM MMAs) so
 // they compile in parallel; gemm.cu picks among them at plan time.
 #pragma once
 #include <stdexcept>
@@ -20,11 +21,11 @@ constexpr int stages_for() {
     return BN == 256 ? 4 : (BN == 128 ? 6 : 8);
 }
 
-template <typename T, int BN, bool AMN, bool BMN, bool SPLIT, bool TE>
+template <typename T, int BN, bool AMN, bool BMN, bool SPLIT, bool TE, int MC>
 KernelFn kernel_ptr(int* smem) {
     constexpr int ST = stages_for<BN, SPLIT>();
     *smem = GemmSmem<BN, ST, T, SPLIT, TE>::kBytes;
-    auto k = &gemm_tc_kernel<T, BN, ST, AMN, BMN, SPLIT, TE>;
+    auto k = &gemm_tc_kernel<T, BN, ST, AMN, BMN, SPLIT, TE, MC>;
     static bool configured = false;
     if (!configured) {
         CUDA_THROW(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem));
@@ -33,20 +34,26 @@ KernelFn kernel_ptr(int* smem) {
     return reinterpret_cast<KernelFn>(k);
 }
 
-template <typename T, int BN, bool SPLIT, bool TE>
+template <typename T, int BN, bool SPLIT, bool TE, int MC>
 KernelFn pick_major(bool amn, bool bmn, int* smem) {
-    if (!amn && !bmn) return kernel_ptr<T, BN, false, false, SPLIT, TE>(smem);
-    if (amn && bmn) return kernel_ptr<T, BN, true, true, SPLIT, TE>(smem);
-    if (!amn && bmn) return kernel_ptr<T, BN, false, true, SPLIT, TE>(smem);
-    return kernel_ptr<T, BN, true, false, SPLIT, TE>(smem);
+    if (!amn && !bmn) return kernel_ptr<T, BN, false, false, SPLIT, TE, MC>(smem);
+    if (amn && bmn) return kernel_ptr<T, BN, true, true, SPLIT, TE, MC>(smem);
+    if (!amn && bmn) return kernel_ptr<T, BN, false, true, SPLIT, TE, MC>(smem);
+    return kernel_ptr<T, BN, true, false, SPLIT, TE, MC>(smem);
 }
 
-template <typename T, bool SPLIT, bool TE>
+template <typename T, bool SPLIT, bool TE, int MC>
 KernelFn pick(int bn, bool amn, bool bmn, int* smem) {
-    switch (bn) {
-        case 256: return pick_major<T, 256, SPLIT, TE>(amn, bmn, smem);
-        case 128: return pick_major<T, 128, SPLIT, TE>(amn, bmn, smem);
-        default: return pick_major<T, 64, SPLIT, TE>(amn, bmn, smem);
+    if constexpr (MC == 2) {
+        if (bn == 256) return pick_major<T, 256, SPLIT, TE, MC>(amn, bmn, smem);
+        if (bn == 128) return pick_major<T, 128, SPLIT, TE, MC>(amn, bmn, smem);
+        throw std::runtime_error("gemm: CTA-pair tiles need BN >= 128");
+    } else {
+        switch (bn) {
+            case 256: return pick_major<T, 256, SPLIT, TE, MC>(amn, bmn, smem);
+            case 128: return pick_major<T, 128, SPLIT, TE, MC>(amn, bmn, smem);
+            default: return pick_major<T, 64, SPLIT, TE, MC>(amn, bmn, smem);
+        }
     }
 }
 
@@ -59,10 +66,12 @@ KernelFn gemm_pick_f32_r(int bn, bool amn, bool bmn, int* smem);
 KernelFn gemm_pick_f32_t(int bn, bool amn, bool bmn, int* smem);
 KernelFn gemm_pick_split_r(int bn, bool amn, bool bmn, int* smem);
 KernelFn gemm_pick_split_t(int bn, bool amn, bool bmn, int* smem);
+KernelFn gemm_pick_bf16_r_mc(int bn, bool amn, bool bmn, int* smem);  // CTA pairs, 2-SM MMA
+KernelFn gemm_pick_bf16_t_mc(int bn, bool amn, bool bmn, int* smem);
 
-#define PNB_GEMM_PICK(name, T, SPLIT, TE)                                     \
+#define PNB_GEMM_PICK(name, T, SPLIT, TE, MC)                                 \
     KernelFn gemm_pick_##name(int bn, bool amn, bool bmn, int* smem) {        \
-        return gemm_pick_detail::pick<T, SPLIT, TE>(bn, amn, bmn, smem);      \
+        return gemm_pick_detail::pick<T, SPLIT, TE, MC>(bn, amn, bmn, smem);  \
     }
 
 }  // namespace pnb

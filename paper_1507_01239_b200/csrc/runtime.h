@@ -29,6 +29,7 @@ struct GemmPlan {
     CUtensorMap ta, tb;
     dim3 grid;
     int smem = 0, M = 0, N = 0, K = 0, bn = 0, threads = 128, tiles = 0;
+    int mc = 1;  // 2: CTA pairs (clusters of 2) computing 256 x BN tiles with 2-SM MMAs
     GemmEpi ep;
     void* fn = nullptr;
 };

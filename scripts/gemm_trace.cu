@@ -13,6 +13,8 @@
 #include "../paper_1507_01239_b200/csrc/gemm_k_f32_t.cu"
 #include "../paper_1507_01239_b200/csrc/gemm_k_split_r.cu"
 #include "../paper_1507_01239_b200/csrc/gemm_k_split_t.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_bf16_r_mc.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_bf16_t_mc.cu"
 
 using namespace pnb;
 
