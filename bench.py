@@ -212,15 +212,23 @@ def run_ours(args, rank, world, local_rank):
     g_fl = sum(by_kind[k][1] for k in gemm_kinds)
     peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     achieved = (d_fl / d_n) / (d_ms / d_n / 1e3) / 1e12 if d_fl > 0 else None
-    traffic = None
+    # DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    # capture (dram__bytes_read.sum + dram__bytes_write.sum, profiles/)
+    # algorithmic bytes of one dW launch (avg over layers): fp32 W read + write, bf16 shadow
+    # write, and the two bf16 operands (B x dout, B x (din + 1))
+    dw_bytes = sum(10.0 * o * (i + 1) + 2.0 * B * (o + i + 1) for i, o in zip(DIMS[:-1], DIMS[1:])) / (len(DIMS) - 1)
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "dominant_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom)
+            t = json.load(open(tpath)).get(dom) or {}
+            traffic, traffic_src = t.get("bytes_per_launch"), t.get("source")
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
                 "frac": (achieved / peak_t) if achieved else None, "traffic": traffic,
+                "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": dw_bytes,
                 "peak_source": f"{how} bf16_tflops_sustained (MEASURED_PEAKS.json)",
                 "launches_per_step": d_n, "ms_per_step": d_ms,
                 "note": ("tcgen05 GEMM region, algorithmic flops (2MNK per launch) / CUDA-event time of the region "
