@@ -83,15 +83,37 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
         return v && v[0] == '1';
     }();
     p.mc = (!f32 && pairs_on && ksplit == 1 && !ep.lower && bn >= 128 && tiles_m >= 2) ? 2 : 1;
+    // Split-K CTA pairs (mc = 3): a GEMM whose 128 x 256 tiles number at most half the
+    // SMs runs each tile on a cluster of two CTAs, one per half of K, exchanging the
+    // partial tiles through distributed shared memory. N = 256 MMAs run at ~95% of
+    // the tensor peak where the N = 128 tiles that would otherwise fill the GPU
+    // reach ~66%.
+    static const bool sk_off = [] {
+        const char* v = std::getenv("PARNN_GEMM_SK2");
+        return v && v[0] == '0';
+    }();
+    int bn_eff = bn;
+    if (p.mc == 1 && !f32 && !sk_off && !force_bn && ksplit == 1 && !ep.lower && nk >= 8) {
+        const long t256 = static_cast<long>(tiles_m) * ((N + 255) / 256);
+        if (2 * t256 <= num_sms && 2 * t256 >= num_sms / 2) {
+            p.mc = 3;
+            bn_eff = 256;
+        }
+    }
     // A(m,k): K-major buffer [M x K] or MN-major buffer [K x M].
     p.ta = a_mn ? make_tmap(A, f32, M, K, lda, atom, bk, true) : make_tmap(A, f32, K, M, lda, bk, 128);
-    p.tb = b_mn ? make_tmap(B, f32, N, K, ldb, atom, bk, true) : make_tmap(B, f32, K, N, ldb, bk, bn / p.mc);
+    p.tb = b_mn ? make_tmap(B, f32, N, K, ldb, atom, bk, true)
+                : make_tmap(B, f32, K, N, ldb, bk, p.mc == 2 ? bn_eff / 2 : bn_eff);
     p.M = M;
     p.N = N;
     p.K = K;
     p.ep = ep;
     p.ep.ksplit = ksplit;
-    if (p.mc == 2) {
+    if (p.mc == 3) {
+        const long t = static_cast<long>(tiles_m) * ((N + bn_eff - 1) / bn_eff);
+        p.grid = dim3(static_cast<unsigned>(2 * t), 1, 1);  // one tile per cluster (the ring holds the exchange)
+        p.tiles = static_cast<int>(t);
+    } else if (p.mc == 2) {
         const long pairs = static_cast<long>((tiles_m + 1) / 2) * tiles_n;
         p.grid = dim3(static_cast<unsigned>(2 * std::min<long>(pairs, num_sms / 2)), 1, 1);
         p.tiles = static_cast<int>(2 * pairs);
@@ -102,7 +124,9 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     }
     const bool te = gemm_epi_transposed(ep.mode);
     KernelFn fn;
-    if (p.mc == 2)
+    if (p.mc == 3)
+        fn = te ? gemm_pick_bf16_t_sk(bn_eff, a_mn, b_mn, &p.smem) : gemm_pick_bf16_r_sk(bn_eff, a_mn, b_mn, &p.smem);
+    else if (p.mc == 2)
         fn = te ? gemm_pick_bf16_t_mc(bn, a_mn, b_mn, &p.smem) : gemm_pick_bf16_r_mc(bn, a_mn, b_mn, &p.smem);
     else if (split)
         fn = te ? gemm_pick_split_t(bn, a_mn, b_mn, &p.smem) : gemm_pick_split_r(bn, a_mn, b_mn, &p.smem);
@@ -111,7 +135,7 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     else
         fn = te ? gemm_pick_bf16_t(bn, a_mn, b_mn, &p.smem) : gemm_pick_bf16_r(bn, a_mn, b_mn, &p.smem);
     p.fn = reinterpret_cast<void*>(fn);
-    p.bn = bn;
+    p.bn = bn_eff;
     p.threads = split ? 448 : 320;  // GemmSmem::kThreads
 }
 
@@ -124,6 +148,7 @@ void gemm_set_grid_cap(int cap) { g_grid_cap = cap; }
 dim3 gemm_launch_grid(const GemmPlan& p) {
     // the persistent kernel covers every tile with any grid (tile = blockIdx + k * gridDim;
     // CTA pairs: pair = blockIdx / 2 + k * gridDim / 2, so the grid stays even)
+    if (p.mc == 3) return p.grid;  // one tile per cluster: the grid cannot shrink
     if (g_grid_cap > 0 && static_cast<int>(p.grid.x) > g_grid_cap)
         return dim3(p.mc == 2 ? std::max(2, g_grid_cap & ~1) : g_grid_cap, 1, 1);
     return p.grid;

@@ -550,7 +550,8 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     constexpr bool kTf32 = OpTraits<T>::kTf32;
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
     static_assert(!SPLIT || kTf32, "3xTF32 split needs fp32 operands");
-    static_assert(MC == 1 || (MC == 2 && !SPLIT && !kTf32 && BN >= 128), "CTA pairs: bf16, BN >= 128");
+    static_assert(MC == 1 || ((MC == 2 || MC == 3) && !SPLIT && !kTf32 && BN >= 128), "CTA pairs: bf16, BN >= 128");
+    static_assert(MC != 3 || STAGES * S::kStage >= 2 * 128 * (BN / 2) * 4, "split-K pair: receive + send buffers in the ring");
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -559,7 +560,8 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     uint64_t* split_done = empty + STAGES;
     uint64_t* tfull = split_done + STAGES;  // [2] accumulator ready for the epilogue
     uint64_t* tempty = tfull + 2;           // [2] accumulator drained by the epilogue
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* xbar = tempty + 2;            // MC == 3: [0] both CTAs' MMAs done, [1] peer's partial half received
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(xbar + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -570,13 +572,16 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     // pair tile, pair p takes p, p + grid/2, ...; CTA rank r of the pair holds
     // rows 128 r .. 128 r + 127 of it (A rows and accumulator) and half of the
     // B tile (columns r BN/2 .. ); the leader (rank 0) issues the M = 256 MMAs.
+    // MC == 3 (split-K pairs): one 128 x BN tile per cluster (grid = 2 x tiles),
+    // CTA rank r runs the k-blocks of half r; the partial tiles are exchanged
+    // through distributed shared memory and rank r finalises columns r BN/2 ...
     const int tmp = (tiles_m + 1) / 2;
-    const int tiles = MC == 1 ? tiles_mn * ep.ksplit : tmp * ((N + BN - 1) / BN);
+    const int tiles = MC == 1 ? tiles_mn * ep.ksplit : (MC == 3 ? tiles_mn : tmp * ((N + BN - 1) / BN));
     const int w0 = MC == 1 ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x) / 2;
     const int wstep = MC == 1 ? static_cast<int>(gridDim.x) : static_cast<int>(gridDim.x) / 2;
     const int rank = MC == 1 ? 0 : static_cast<int>(cluster_ctarank());
     auto tile_mn = [&](int w, int& m0, int& n0) {
-        if (MC == 1) {
+        if (MC != 2) {
             m0 = (w % tiles_m) * 128;
             n0 = ((w % tiles_mn) / tiles_m) * BN;
         } else {
@@ -589,6 +594,12 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     auto tile_skipped = [&](int m0, int n0) { return ep.lower && n0 > m0 + 127; };
     // k-block range [kb0, kb1) of split ks (gemm_plan guarantees it is non-empty)
     auto krange = [&](int tile, int& kb0, int& kb1) {
+        if (MC == 3) {
+            const int half = (nk_all + 1) / 2;
+            kb0 = rank * half;
+            kb1 = min(nk_all, kb0 + half);
+            return 0;
+        }
         const int ks = tile / tiles_mn;
         kb0 = ks * nk_per;
         kb1 = min(nk_all, kb0 + nk_per);
@@ -604,8 +615,10 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], MC == 1 ? 256 : 16);  // pairs: one arrive per epilogue warp of both CTAs
+            mbar_init(&tempty[i], MC == 2 ? 16 : 256);  // pairs: one arrive per epilogue warp of both CTAs
         }
+        mbar_init(&xbar[0], 2);  // MC == 3: each CTA's MMA completion, multicast to both
+        mbar_init(&xbar[1], 1);  // MC == 3: own expect_tx + the peer's bulk copy bytes
         fence_barrier_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
@@ -618,7 +631,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     }
     tc_fence_before();
     __syncthreads();
-    if constexpr (MC == 2) cluster_sync_all();  // the leader's barriers exist before the peer's loads / arrives
+    if constexpr (MC != 1) cluster_sync_all();  // the peer's barriers exist before any remote arrive
     tc_fence_after();
     const uint32_t tmem = *tslot;
     if (threadIdx.x == 0) PNB_TRACE(1);
@@ -686,8 +699,8 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (pairs: the leader only) ----------------
-        if (lane == 0 && rank == 0) {
-            constexpr uint32_t idesc = make_idesc(OpTraits<T>::kFmt, A_MN ? 1 : 0, B_MN ? 1 : 0, 128 * MC, BN);
+        if (lane == 0 && (MC != 2 || rank == 0)) {
+            constexpr uint32_t idesc = make_idesc(OpTraits<T>::kFmt, A_MN ? 1 : 0, B_MN ? 1 : 0, MC == 2 ? 256 : 128, BN);
             constexpr uint32_t kMnLayout = kTf32 ? 1 : 2;  // BASE32B for TF32 MN-major
             constexpr uint32_t kMnSbo = kTf32 ? 512 : 1024;
             auto desc_a = [&](uint32_t base, int k) {
@@ -738,6 +751,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     umma_commit2_mc(&tfull[acc], 3);  // both CTAs' accumulator rows are ready
                 else
                     umma_commit(&tfull[acc]);
+                if constexpr (MC == 3) umma_commit_mc(&xbar[0], 3);  // my ring is free for the peer's partial
                 PNB_TRACE(3);
                 ++local;
             }
@@ -782,24 +796,71 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                 }
                 for (long o = 0; o < bytes; o += 128) prefetch_l2(src + o);
             }
+            // MC == 3: this CTA finalises the chunks of its half of the columns
+            constexpr int kHalfChunks = BN / 64;
+            const int c_begin = (MC == 3 ? rank * kHalfChunks : 0) + eset;
+            const int c_end = MC == 3 ? (rank + 1) * kHalfChunks : BN / 32;
             // row-wise modes: the first chunk's x operand is fetched before the accumulator is ready
             uint4 xraw[8];
             bool xhave = false;
             if constexpr (!TE) {
-                const int n = n0 + eset * 32;
+                const int n = n0 + c_begin * 32;
                 if (row_ok && n < N) xhave = rows_x_fetch<T>(ep, row, n, min(32, N - n), xraw);
             }
             mbar_wait_sleep(&tfull[acc], (local >> 1) & 1);
             if (warp == 2 && lane == 0) PNB_TRACE(4);
             tc_fence_after();
+            // receive buffer (the idle ring): [128 rows][BN/2 cols] fp32, 16-byte slots
+            // XOR-swizzled by row inside each 32-column chunk (conflict-free both ways)
+            uint4* xrecv = reinterpret_cast<uint4*>(smem);
+            const int rl = quad * 32 + lane;  // tile row of this thread
+            if constexpr (MC == 3) {
+                // stage the partial of the peer's half in my ring (behind my receive
+                // buffer; my MMAs are done), then one bulk copy into the peer's ring
+                constexpr uint32_t kHalfBytes = 128u * (BN / 2) * 4u;
+                uint4* xsend = xrecv + kHalfBytes / 16;
 #pragma unroll 1
-            for (int c = eset; c < BN / 32; c += 2) {
+                for (int c = (rank ^ 1) * kHalfChunks + eset; c < ((rank ^ 1) + 1) * kHalfChunks; c += 2) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c * 32, r);
+                    tmem_ld_wait();
+                    const int cl = c - (rank ^ 1) * kHalfChunks;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        xsend[(rl * kHalfChunks + cl) * 8 + (k ^ (rl & 7))] =
+                            make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+                }
+                fence_proxy_async_smem();  // generic writes -> visible to the bulk copy
+                asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
+                if (warp == 2 && lane == 0) {
+                    mbar_arrive_expect_tx(&xbar[1], kHalfBytes);  // the peer's copy into my ring
+                    mbar_wait(&xbar[0], 0);                       // both MMAs done: the peer's ring is free
+                    bulk_copy_to_peer(mapa_cluster(xrecv, rank ^ 1), xsend, kHalfBytes,
+                                      mapa_cluster(&xbar[1], rank ^ 1));
+                    PNB_TRACE(7);
+                }
+                mbar_wait_cluster(&xbar[1], 0);  // the peer's partial of my half has landed
+            }
+#pragma unroll 1
+            for (int c = c_begin; c < c_end; c += 2) {
                 const int n = n0 + c * 32;
                 if (n >= N) break;  // warp-uniform
                 if (m0 + quad * 32 >= M) break;  // warp-uniform: no rows of this quadrant
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c * 32, r);
                 tmem_ld_wait();
+                if constexpr (MC == 3) {
+                    const int cl = c - rank * kHalfChunks;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint4 u = xrecv[(rl * kHalfChunks + cl) * 8 + (k ^ (rl & 7))];
+                        // own + peer partial (fp32 addition commutes: both CTAs' halves round alike)
+                        r[4 * k] = __float_as_uint(__uint_as_float(r[4 * k]) + __uint_as_float(u.x));
+                        r[4 * k + 1] = __float_as_uint(__uint_as_float(r[4 * k + 1]) + __uint_as_float(u.y));
+                        r[4 * k + 2] = __float_as_uint(__uint_as_float(r[4 * k + 2]) + __uint_as_float(u.z));
+                        r[4 * k + 3] = __float_as_uint(__uint_as_float(r[4 * k + 3]) + __uint_as_float(u.w));
+                    }
+                }
                 if constexpr (TE) {
                     bad |= epilogue_chunk<T, SPLIT ? 4 : 8>(ep, r, ebuf, lane, m0 + quad * 32, M, n, N, lr, alpha_eff,
                                                             ks, s_aux, s_out);
@@ -810,7 +871,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     epilogue_chunk_rows<T>(ep, v, row, n, min(32, N - n), xraw, xhave, s_aux, s_out);
                     // next chunk of this warp: its x loads overlap the next TMEM load
                     const int nn = n + 64;
-                    xhave = nn < N && rows_x_fetch<T>(ep, row, nn, min(32, N - nn), xraw);
+                    xhave = nn < N && c + 2 < c_end && rows_x_fetch<T>(ep, row, nn, min(32, N - nn), xraw);
                 }
             }
             tc_fence_before();
@@ -883,6 +944,9 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     if constexpr (MC == 2) {
         cluster_sync_all();
         if (warp == 1) tmem_dealloc2<S::kTmemCols>(tmem);
+    } else if constexpr (MC == 3) {
+        cluster_sync_all();  // no CTA leaves while the peer may still read or write its smem
+        if (warp == 1) tmem_dealloc<S::kTmemCols>(tmem);
     } else {
         if (warp == 1) tmem_dealloc<S::kTmemCols>(tmem);
     }

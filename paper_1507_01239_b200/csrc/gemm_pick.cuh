@@ -44,7 +44,7 @@ KernelFn pick_major(bool amn, bool bmn, int* smem) {
 
 template <typename T, bool SPLIT, bool TE, int MC>
 KernelFn pick(int bn, bool amn, bool bmn, int* smem) {
-    if constexpr (MC == 2) {
+    if constexpr (MC != 1) {
         if (bn == 256) return pick_major<T, 256, SPLIT, TE, MC>(amn, bmn, smem);
         if (bn == 128) return pick_major<T, 128, SPLIT, TE, MC>(amn, bmn, smem);
         throw std::runtime_error("gemm: CTA-pair tiles need BN >= 128");
@@ -68,6 +68,8 @@ KernelFn gemm_pick_split_r(int bn, bool amn, bool bmn, int* smem);
 KernelFn gemm_pick_split_t(int bn, bool amn, bool bmn, int* smem);
 KernelFn gemm_pick_bf16_r_mc(int bn, bool amn, bool bmn, int* smem);  // CTA pairs, 2-SM MMA
 KernelFn gemm_pick_bf16_t_mc(int bn, bool amn, bool bmn, int* smem);
+KernelFn gemm_pick_bf16_r_sk(int bn, bool amn, bool bmn, int* smem);  // split-K CTA pairs (DSMEM exchange)
+KernelFn gemm_pick_bf16_t_sk(int bn, bool amn, bool bmn, int* smem);
 
 #define PNB_GEMM_PICK(name, T, SPLIT, TE, MC)                                 \
     KernelFn gemm_pick_##name(int bn, bool amn, bool bmn, int* smem) {        \

@@ -13,6 +13,8 @@
 #include "../paper_1507_01239_b200/csrc/gemm_k_split_t.cu"
 #include "../paper_1507_01239_b200/csrc/gemm_k_bf16_r_mc.cu"
 #include "../paper_1507_01239_b200/csrc/gemm_k_bf16_t_mc.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_bf16_r_sk.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_bf16_t_sk.cu"
 using namespace pnb;
 int main(int argc, char** argv) {
     int bnf = argc > 1 ? atoi(argv[1]) : 0;

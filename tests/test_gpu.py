@@ -280,40 +280,46 @@ def test_reference_adapter_dropin():
     assert "train_parallel: avg_frequency must be >= 1" in err["error"]
 
 
-_PAIRS_SCRIPT = r"""
+_PATH_SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[1])
 from paper_1507_01239_b200 import parnn as P
 ctx = P.Context(0)
 dims = [440, 2048, 2048, 1101]
-x = np.random.default_rng(0).standard_normal((2048, 440))
-y = np.random.default_rng(1).integers(0, 1101, 2048).astype(np.int32)
+x = np.random.default_rng(0).standard_normal((4096, 440))
+y = np.random.default_rng(1).integers(0, 1101, 4096).astype(np.int32)
 ds = P.DeviceDataset(ctx, P.Dataset(x, y, 1101))
-r = P.Replica(ctx, dims, precision=P.Precision.bf16, optimizer=P.OptimizerKind.sgd, minibatch=512, max_steps=3)
+r = P.Replica(ctx, dims, precision=P.Precision.bf16, optimizer=P.OptimizerKind.sgd, minibatch=1024, max_steps=3)
 r.set_params(P.init_random(dims, seed=1).params)
 r.bind(ds)
-r.upload_epoch(np.random.default_rng(2).integers(0, 2048, 3 * 512), [0.05] * 3)
+r.upload_epoch(np.random.default_rng(2).integers(0, 4096, 3 * 1024), [0.05] * 3)
 r.step(3)
 r.sync()
 np.save(sys.argv[2], r.get_params())
 """
 
 
-def test_cta_pair_gemm_path_matches(tmp_path):
-    """The opt-in 2-SM (cta_group::2) GEMM path (PARNN_GEMM_PAIRS=1, read once per
-    process) trains to the same parameters as the default 1-SM tiles (bf16 mode:
-    identical products, fp32 accumulation order differs only inside the MMA)."""
+@pytest.mark.parametrize("var,alt", [("PARNN_GEMM_PAIRS", "1"), ("PARNN_GEMM_SK2", "0")])
+def test_gemm_cluster_paths_match(tmp_path, var, alt):
+    """The GEMM's cluster paths train to the same parameters as the plain 1-SM
+    tiles (bf16 mode: the products are identical, only the fp32 accumulation
+    order differs): the opt-in 2-SM cta_group::2 pairs (PARNN_GEMM_PAIRS=1) and
+    the default split-K pairs with the DSMEM partial-tile exchange, which the
+    1024 x 2048 hidden GEMMs take (PARNN_GEMM_SK2=0 turns them off). The
+    switches are read once per process, so each run is a subprocess."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
-    for pairs in ("0", "1"):
-        env = dict(os.environ, PARNN_GEMM_PAIRS=pairs)
-        f = tmp_path / f"p{pairs}.npy"
-        subprocess.run([sys.executable, "-c", _PAIRS_SCRIPT, root, str(f)], env=env, check=True, timeout=300)
-        out[pairs] = np.load(f)
-    d = np.linalg.norm(out["1"] - out["0"]) / np.linalg.norm(out["0"])
+    for v in ("default", alt):
+        env = dict(os.environ)
+        env.pop(var, None)
+        if v != "default":
+            env[var] = v
+        f = tmp_path / f"p_{v}.npy"
+        subprocess.run([sys.executable, "-c", _PATH_SCRIPT, root, str(f)], env=env, check=True, timeout=300)
+        out[v] = np.load(f)
+    d = np.linalg.norm(out[alt] - out["default"]) / np.linalg.norm(out["default"])
     assert d < 1e-4, d
-
