@@ -560,8 +560,8 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     uint64_t* split_done = empty + STAGES;
     uint64_t* tfull = split_done + STAGES;  // [2] accumulator ready for the epilogue
     uint64_t* tempty = tfull + 2;           // [2] accumulator drained by the epilogue
-    uint64_t* xbar = tempty + 2;            // MC == 3: [0] both CTAs' MMAs done, [1] peer's partial half received
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(xbar + 2);
+    uint64_t* xbar = tempty + 2;  // MC == 3: [0] both CTAs' MMAs done, [1 + w] epilogue warp w's partial received
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(xbar + 9);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
             mbar_init(&tempty[i], MC == 2 ? 16 : 256);  // pairs: one arrive per epilogue warp of both CTAs
         }
         mbar_init(&xbar[0], 2);  // MC == 3: each CTA's MMA completion, multicast to both
-        mbar_init(&xbar[1], 1);  // MC == 3: own expect_tx + the peer's bulk copy bytes
+        for (int w = 1; w <= 8; ++w) mbar_init(&xbar[w], 1);  // MC == 3: own expect_tx + the peer warp's copy
         fence_barrier_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
@@ -631,7 +631,9 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     }
     tc_fence_before();
     __syncthreads();
-    if constexpr (MC != 1) cluster_sync_all();  // the peer's barriers exist before any remote arrive
+    if constexpr (MC == 2) cluster_sync_all();  // the peer's barriers exist before any remote arrive
+    // MC == 3: arrive now, wait right before each role's first remote operation
+    if constexpr (MC == 3) cluster_arrive_relaxed();
     tc_fence_after();
     const uint32_t tmem = *tslot;
     if (threadIdx.x == 0) PNB_TRACE(1);
@@ -697,6 +699,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     mbar_wait(&empty[j % STAGES], (j / STAGES) & 1);
             }
         }
+        if constexpr (MC == 3) cluster_wait();
     } else if (warp == 1) {
         // ---------------- MMA issuer (pairs: the leader only) ----------------
         if (lane == 0 && (MC != 2 || rank == 0)) {
@@ -751,10 +754,14 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     umma_commit2_mc(&tfull[acc], 3);  // both CTAs' accumulator rows are ready
                 else
                     umma_commit(&tfull[acc]);
-                if constexpr (MC == 3) umma_commit_mc(&xbar[0], 3);  // my ring is free for the peer's partial
+
                 PNB_TRACE(3);
                 ++local;
             }
+        }
+        if constexpr (MC == 3) {
+            cluster_wait();  // the peer's barriers are initialised
+            if (lane == 0) umma_commit_mc(&xbar[0], 3);  // after my MMAs: my ring is free for the peer's partial
         }
     } else if (warp < 10) {
         // ---------------- epilogue (8 warps: 2 sets x 128 TMEM lanes) ----------------
@@ -810,36 +817,37 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
             mbar_wait_sleep(&tfull[acc], (local >> 1) & 1);
             if (warp == 2 && lane == 0) PNB_TRACE(4);
             tc_fence_after();
-            // receive buffer (the idle ring): [128 rows][BN/2 cols] fp32, 16-byte slots
-            // XOR-swizzled by row inside each 32-column chunk (conflict-free both ways)
-            uint4* xrecv = reinterpret_cast<uint4*>(smem);
-            const int rl = quad * 32 + lane;  // tile row of this thread
+            // Exchange buffers in the idle ring, one contiguous region per epilogue warp
+            // (quad, set): its 32 rows x the kJ chunks it finalises, 16-byte slots
+            // XOR-swizzled by row (conflict-free both ways). Warp (quad, set) of one CTA
+            // sends exactly what warp (quad, set) of the peer finalises.
+            constexpr int kJ = BN / 128;  // chunks per warp per half
+            uint4* xrecv = reinterpret_cast<uint4*>(smem) + ((warp - 2) * 32 + lane) * (kJ * 8);
             if constexpr (MC == 3) {
-                // stage the partial of the peer's half in my ring (behind my receive
-                // buffer; my MMAs are done), then one bulk copy into the peer's ring
+                cluster_wait();  // the peer's barriers are initialised
+                constexpr uint32_t kWarpBytes = 32u * kJ * 32u * 4u;
                 constexpr uint32_t kHalfBytes = 128u * (BN / 2) * 4u;
                 uint4* xsend = xrecv + kHalfBytes / 16;
-#pragma unroll 1
-                for (int c = (rank ^ 1) * kHalfChunks + eset; c < ((rank ^ 1) + 1) * kHalfChunks; c += 2) {
+#pragma unroll
+                for (int j = 0; j < kJ; ++j) {
+                    const int c = (rank ^ 1) * kHalfChunks + eset + 2 * j;
                     uint32_t r[32];
                     tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c * 32, r);
                     tmem_ld_wait();
-                    const int cl = c - (rank ^ 1) * kHalfChunks;
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
-                        xsend[(rl * kHalfChunks + cl) * 8 + (k ^ (rl & 7))] =
-                            make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+                        xsend[j * 8 + (k ^ (lane & 7))] = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
                 }
                 fence_proxy_async_smem();  // generic writes -> visible to the bulk copy
-                asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
-                if (warp == 2 && lane == 0) {
-                    mbar_arrive_expect_tx(&xbar[1], kHalfBytes);  // the peer's copy into my ring
-                    mbar_wait(&xbar[0], 0);                       // both MMAs done: the peer's ring is free
-                    bulk_copy_to_peer(mapa_cluster(xrecv, rank ^ 1), xsend, kHalfBytes,
-                                      mapa_cluster(&xbar[1], rank ^ 1));
-                    PNB_TRACE(7);
+                __syncwarp();
+                uint64_t* wbar = &xbar[1 + (warp - 2)];
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(wbar, kWarpBytes);  // the peer warp's copy into my ring
+                    mbar_wait(&xbar[0], 0);                   // both MMAs done: the peer's ring is free
+                    bulk_copy_to_peer(mapa_cluster(xrecv, rank ^ 1), xsend, kWarpBytes, mapa_cluster(wbar, rank ^ 1));
+                    if (warp == 2) PNB_TRACE(7);
                 }
-                mbar_wait_cluster(&xbar[1], 0);  // the peer's partial of my half has landed
+                mbar_wait(wbar, 0);  // the peer's partial of my chunks has landed (bulk copy, like TMA)
             }
 #pragma unroll 1
             for (int c = c_begin; c < c_end; c += 2) {
@@ -850,10 +858,10 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                 tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c * 32, r);
                 tmem_ld_wait();
                 if constexpr (MC == 3) {
-                    const int cl = c - rank * kHalfChunks;
+                    const int j = (c - rank * kHalfChunks - eset) / 2;
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        const uint4 u = xrecv[(rl * kHalfChunks + cl) * 8 + (k ^ (rl & 7))];
+                        const uint4 u = xrecv[j * 8 + (k ^ (lane & 7))];
                         // own + peer partial (fp32 addition commutes: both CTAs' halves round alike)
                         r[4 * k] = __float_as_uint(__uint_as_float(r[4 * k]) + __uint_as_float(u.x));
                         r[4 * k + 1] = __float_as_uint(__uint_as_float(r[4 * k + 1]) + __uint_as_float(u.y));
@@ -945,7 +953,10 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
         cluster_sync_all();
         if (warp == 1) tmem_dealloc2<S::kTmemCols>(tmem);
     } else if constexpr (MC == 3) {
-        cluster_sync_all();  // no CTA leaves while the peer may still read or write its smem
+        // no CTA leaves while its outgoing copy may still read its smem (the peer
+        // arrives only after receiving it)
+        cluster_arrive_relaxed();
+        cluster_wait();
         if (warp == 1) tmem_dealloc<S::kTmemCols>(tmem);
     } else {
         if (warp == 1) tmem_dealloc<S::kTmemCols>(tmem);
