@@ -641,11 +641,15 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
             if (l > 0) gemm_launch(r.da[l], s);
             CUDA_THROW(cudaEventRecord(r.ev_bwd[l], s));  // W_l read; dz[l-1] ready
             if (l > 0) lr_side_chain(r, r.lrl[l - 1].out, r.ev_bwd[l], S(r.lrl[l - 1].out.stream));
+        }
+        for (int l = L - 1; l >= 0; --l) {
             // [dW_l | db_l] on the layer's input-side stream: the layers' weight updates are
             // independent and overlap each other and the remaining chains (a single side
-            // stream made them the step's critical path)
+            // stream made them the step's critical path). They start after the whole dz
+            // chain: a persistent dW grid launched beside it held the SMs the next dA
+            // needed (the output layer's 75 us dW delayed dA_1 by ~60 us).
             cudaStream_t ws = S(r.lrl[l].in.stream);
-            CUDA_THROW(cudaStreamWaitEvent(ws, r.ev_bwd[l], 0));
+            CUDA_THROW(cudaStreamWaitEvent(ws, r.ev_bwd[0], 0));
             CUDA_THROW(cudaStreamWaitEvent(ws, r.lrl[l].out.ready, 0));
             lr_layer_update(r, l, ws);
             r.tmark("dw" + std::to_string(l), ws);
