@@ -95,7 +95,11 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     int bn_eff = bn;
     if (p.mc == 1 && !f32 && !sk_off && !force_bn && ksplit == 1 && !ep.lower && nk >= 8) {
         const long t256 = static_cast<long>(tiles_m) * ((N + 255) / 256);
-        if (2 * t256 <= num_sms && 2 * t256 >= num_sms / 2) {
+        static const int min_frac = [] {  // tuning aid: pairs must fill >= 1/x of the SMs
+            const char* v = std::getenv("PARNN_GEMM_SK2_FRAC");
+            return v ? std::max(1, std::atoi(v)) : 2;
+        }();
+        if (2 * t256 <= num_sms && 2 * t256 >= num_sms / min_frac) {
             p.mc = 3;
             bn_eff = 256;
         }

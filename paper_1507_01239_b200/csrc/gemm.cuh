@@ -232,7 +232,7 @@ __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, const uint32_t
                                                float& s_aux, float& s_out) {
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-        buf[lane * 8 + (k ^ (lane & 7))] = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+        sts128(buf + lane * 8 + (k ^ (lane & 7)), make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
     __syncwarp();
     const int kk = lane & 7, rs = lane >> 3;
     const int c = n + 4 * kk;
@@ -244,7 +244,7 @@ __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, const uint32_t
 #pragma unroll
     for (int i = 0; i < PP; ++i) {
         const int rr = 4 * (p0 + i) + rs;
-        const uint4 u = buf[rr * 8 + (kk ^ (rr & 7))];
+        const uint4 u = lds128(buf + rr * 8 + (kk ^ (rr & 7)));
         a[i][0] = __uint_as_float(u.x); a[i][1] = __uint_as_float(u.y);
         a[i][2] = __uint_as_float(u.z); a[i][3] = __uint_as_float(u.w);
     }
@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     tmem_ld_wait();
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
-                        xsend[j * 8 + (k ^ (lane & 7))] = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+                        sts128(xsend + j * 8 + (k ^ (lane & 7)), make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
                 }
                 fence_proxy_async_smem();  // generic writes -> visible to the bulk copy
                 __syncwarp();
@@ -861,7 +861,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     const int j = (c - rank * kHalfChunks - eset) / 2;
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        const uint4 u = xrecv[j * 8 + (k ^ (lane & 7))];
+                        const uint4 u = lds128(xrecv + j * 8 + (k ^ (lane & 7)));
                         // own + peer partial (fp32 addition commutes: both CTAs' halves round alike)
                         r[4 * k] = __float_as_uint(__uint_as_float(r[4 * k]) + __uint_as_float(u.x));
                         r[4 * k + 1] = __float_as_uint(__uint_as_float(r[4 * k + 1]) + __uint_as_float(u.y));

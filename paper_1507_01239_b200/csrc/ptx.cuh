@@ -220,6 +220,22 @@ __device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint4 v) {
                  : "memory");
 }
 
+// Explicit shared-space 16-byte accesses: pointers derived from the aligned
+// dynamic-smem base lose their address space, and the generic LD/ST the
+// compiler then emits measured as the top stall of the transposed epilogue.
+__device__ __forceinline__ void sts128(const void* p, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p))
+                 : "memory");
+    return v;
+}
+
 // Bulk copy of `bytes` from this CTA's smem to shared::cluster address dst_cl
 // (a peer CTA's smem); the bytes complete on the mbarrier at bar_cl there.
 __device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cl, const void* src, uint32_t bytes, uint32_t bar_cl) {

@@ -624,18 +624,24 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
             }
         launch_gather(ds->features(r.prec), ds->ld, ds->y, r.d_rows, r.d_step, r.B, r.dims[0], r.acts[0],
                       r.ld_act[0], r.d_ybatch, F, s);
+        static const int in_late = [] {  // tuning aid: input-side chains 0 = beside the forward, 1 = from the loss on
+            const char* v = std::getenv("PARNN_LR_IN_LATE");
+            return v ? std::atoi(v) : 0;
+        }();
         CUDA_THROW(cudaEventRecord(r.ev_act[0], s));
-        lr_side_chain(r, r.lrl[0].in, r.ev_act[0], S(r.lrl[0].in.stream));
+        if (!in_late) lr_side_chain(r, r.lrl[0].in, r.ev_act[0], S(r.lrl[0].in.stream));
         for (int l = 0; l < L; ++l) {
             gemm_launch(r.fwd[l], s);
             if (l + 1 < L) {
                 CUDA_THROW(cudaEventRecord(r.ev_act[l + 1], s));
-                lr_side_chain(r, r.lrl[l + 1].in, r.ev_act[l + 1], S(r.lrl[l + 1].in.stream));
+                if (!in_late) lr_side_chain(r, r.lrl[l + 1].in, r.ev_act[l + 1], S(r.lrl[l + 1].in.stream));
             }
         }
         launch_softmax_ce(r.zout, r.ld_act[L], r.B, r.dims[L], r.d_ybatch, r.dz[L - 1], r.ld_act[L], r.ce_rows, F, s);
         r.tmark("fwd", s);
         CUDA_THROW(cudaEventRecord(r.ev_dw[L - 1], s));  // dz[L-1] ready
+        if (in_late)
+            for (int l = L - 1; l >= 0; --l) lr_side_chain(r, r.lrl[l].in, r.ev_dw[L - 1], S(r.lrl[l].in.stream));
         lr_side_chain(r, r.lrl[L - 1].out, r.ev_dw[L - 1], S(r.lrl[L - 1].out.stream));
         for (int l = L - 1; l >= 0; --l) {
             if (l > 0) gemm_launch(r.da[l], s);
