@@ -23,6 +23,12 @@ namespace b200 {
 struct Options {
     int device = 0;
     int precision = PARNN_BF16;  // PARNN_FP32 for the fp32 parity mode
+    // OptimizerKind::ngsgd runs the reference's kron-full NG-SGD by default; with
+    // lowrank_ng it runs the online low-rank NG-SGD (rank-R Fisher projection and
+    // subspace update; alpha = opts.ng_smoothing). 0 = the defaults (20, 80, 4, 2000, 3).
+    bool lowrank_ng = false;
+    int ng_rank_in = 0, ng_rank_out = 0, ng_update_period = 0, ng_update_lag = 0;
+    double ng_history = 0.0;
 };
 
 namespace detail {
@@ -65,7 +71,13 @@ inline TrainResult run(const ParallelPlan& plan, const MlpModel& model0, const D
     cfg.avg_frequency = plan.avg_frequency;
     cfg.minibatch = plan.minibatch;
     cfg.base_seed = plan.base_seed;
-    cfg.optimizer = opts.optimizer == OptimizerKind::ngsgd ? PARNN_NGSGD : PARNN_SGD;
+    cfg.optimizer = opts.optimizer != OptimizerKind::ngsgd ? PARNN_SGD
+                    : (o.lowrank_ng ? PARNN_NGSGD_LOWRANK : PARNN_NGSGD);
+    cfg.ng_rank_in = o.ng_rank_in;
+    cfg.ng_rank_out = o.ng_rank_out;
+    cfg.ng_update_period = o.ng_update_period;
+    cfg.ng_history = o.ng_history;
+    cfg.ng_update_lag = o.ng_update_lag;
     cfg.lr_schedule = opts.lr_schedule == LrVariant::newbob ? PARNN_NEWBOB : PARNN_EXPONENTIAL;
     cfg.lr_init = opts.lr_init;
     cfg.epochs = opts.epochs;
