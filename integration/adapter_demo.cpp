@@ -41,6 +41,12 @@ int main() {
                 "\"avg_events\": [%zu, %zu]}\n",
                 ref.metrics.size(), ours.metrics.size(), ref.metrics.back().train_ce, ours.metrics.back().train_ce,
                 std::sqrt(num / den), ref.metrics.back().avg_events, ours.metrics.back().avg_events);
+    // the north star's low-rank NG-SGD through the same adapter call
+    b200::Options lo = o;
+    lo.lowrank_ng = true;
+    const TrainResult low = b200::train_parallel(plan, m0, tr, cv, opts, lo);
+    std::printf("{\"lowrank_epochs\": %zu, \"ce_lowrank\": %.9f, \"ce_ref\": %.9f}\n", low.metrics.size(),
+                low.metrics.back().train_ce, ref.metrics.back().train_ce);
     try {
         ParallelPlan bad = plan;
         bad.avg_frequency = 0;

@@ -273,10 +273,13 @@ def test_reference_adapter_dropin():
         pytest.skip("integration/_build/adapter_demo not built (needs the reference headers at build time)")
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
-    res, err = [json.loads(l) for l in out.stdout.strip().splitlines()]
+    res, low, err = [json.loads(l) for l in out.stdout.strip().splitlines()]
     assert res["epochs"][0] == res["epochs"][1] and res["avg_events"][0] == res["avg_events"][1]
     assert abs(res["ce_ref"] - res["ce_b200"]) <= 0.01 * res["ce_ref"]
     assert res["theta_rel_l2"] < 2e-3
+    # the low-rank NG-SGD selected through the same adapter trains as well as the reference's NG
+    assert low["lowrank_epochs"] == res["epochs"][0]
+    assert np.isfinite(low["ce_lowrank"]) and low["ce_lowrank"] <= 1.05 * low["ce_ref"]
     assert "train_parallel: avg_frequency must be >= 1" in err["error"]
 
 
