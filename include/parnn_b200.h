@@ -189,12 +189,12 @@ typedef struct {
     uint64_t rank0;          /* first global rank hosted by this process */
     uint64_t local_workers;  /* ranks hosted here (0 = all m) */
     int serial;              /* serial_train semantics (parallel.cpp:285-294) */
-    /* low-rank NG-SGD knobs (PARNN_NGSGD_LOWRANK); 0 = default (20, 80, 4, 2000, lag 3) */
+    /* low-rank NG-SGD knobs (PARNN_NGSGD_LOWRANK); 0 = default (20, 80, 4, 2000, lag 4) */
     int ng_rank_in;
     int ng_rank_out;
     int ng_update_period;
     double ng_history;
-    int ng_update_lag;       /* 0 = default (3) */
+    int ng_update_lag;       /* 0 = default (4 = the update period) */
 } parnn_train_config;
 
 /* train_parallel / serial_train (parallel.cpp:163-294). metrics_out holds up

@@ -23,7 +23,8 @@ Preconditioning (X F~^-1 up to scale, F~ = F + alpha tr(F)/D I):
     H = X W^T,  X^ = X - H W,  gamma = sqrt(tr(X X^T) / tr(X^ X^T)).
 Subspace update every `update_period` calls (eta = 1 - exp(-N P / S)), in
 effect update_lag calls later (1 = the next call, as in the paper; the default
-here is 3, which lets the device overlap the eigensolve with two steps):
+here is 4 = the update period, which lets the device overlap the eigensolve
+with the three steps in between):
     T = (eta/N) X^T X + (1 - eta) F_t,    Y = R_t T,   Z = Y Y^T = U C^2 U^T
     R_{t+1} = C^-1 U^T Y,  rho_{t+1} = (tr T - tr C) / (D - R),  D_{t+1} = C - rho_{t+1}
 with the floors c, d >= max(DELTA c_max, EPS tr(T)/D) and rho >= EPS tr(T)/D
@@ -61,7 +62,7 @@ class LowRankConfig:
     num_samples_history: float = 2000.0
     alpha: float = 4.0
     init_iters: int = 3
-    update_lag: int = 3  # steps until an update computed at step t takes effect (1 = t+1 as in Kaldi; <= P)
+    update_lag: int = 4  # steps until an update computed at step t takes effect (1 = t+1 as in Kaldi; <= P)
 
 
 def basis_seed(layer: int, side: int) -> int:

@@ -115,7 +115,7 @@ struct LrConfig {
     int update_period = 4;            // subspace update every P minibatches
     int init_iters = 3;               // updates on the first minibatch before use
     double history = 2000.0;          // S: eta = 1 - exp(-B P / S)
-    int update_lag = 3;               // steps until an update takes effect (1 = next step; <= P)
+    int update_lag = 4;               // steps until an update takes effect (1 = next step; <= P)
     double alpha = 4.0;               // smoothing (the reference's ng_smoothing)
 };
 struct LrSide {

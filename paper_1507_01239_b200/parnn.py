@@ -104,7 +104,7 @@ class TrainOptions:
     ng_rank_out: int = 80
     ng_update_period: int = 4
     ng_history: float = 2000.0
-    ng_update_lag: int = 3
+    ng_update_lag: int = 4
 
 
 @dataclass
@@ -368,7 +368,7 @@ class Replica:
         check(lib().parnn_replica_set_ng_state(self.h, ptr(flat), flat.size, update_count))
 
     def set_lowrank(self, rank_in: int = 20, rank_out: int = 80, update_period: int = 4, init_iters: int = 3,
-                    num_samples_history: float = 2000.0, update_lag: int = 3):
+                    num_samples_history: float = 2000.0, update_lag: int = 4):
         check(lib().parnn_replica_set_lowrank(self.h, rank_in, rank_out, update_period, init_iters,
                                               num_samples_history, update_lag))
 

@@ -125,7 +125,7 @@ def _oracle_run(p0, dims, x, y, batches, lrs, cfg):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("lag,period", [(1, 2), (2, 2), (3, 3)])
+@pytest.mark.parametrize("lag,period", [(1, 2), (2, 2), (3, 3), (4, 4)])
 @pytest.mark.parametrize("prec,dtol", [("fp32", 2e-3), ("tf32", 3e-2), ("bf16", 8e-2)])
 def test_lowrank_step_parity(ctx, prec, dtol, lag, period):
     from paper_1507_01239_b200 import parnn as P
