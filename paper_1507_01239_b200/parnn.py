@@ -499,10 +499,13 @@ class Comm:
 # ------------------------------------------------------------ training
 def _train(plan: ParallelPlan, model0: MlpModel, train: Dataset, cv: Dataset, opts: TrainOptions, serial: bool,
            device: int = 0, comm: Comm | None = None, rank0: int = 0, local_workers: int = 0,
-           ctx: Context | None = None) -> TrainResult:
+           ctx: Context | None = None, device_data: tuple | None = None) -> TrainResult:
     ctx = ctx or Context(device)
-    tr = DeviceDataset(ctx, train)
-    cvd = DeviceDataset(ctx, cv) if cv is not None and cv.size() > 0 else None
+    if device_data is not None:  # (train, cv) already resident on ctx's device (repeated runs, sweeps)
+        tr, cvd = device_data
+    else:
+        tr = DeviceDataset(ctx, train)
+        cvd = DeviceDataset(ctx, cv) if cv is not None and cv.size() > 0 else None
     cfg = TrainConfig(plan.workers, plan.avg_frequency, plan.minibatch, plan.base_seed, int(opts.optimizer),
                       int(opts.lr_schedule), opts.lr_init, opts.epochs, opts.ng_decay, opts.ng_smoothing,
                       int(opts.precision), int(model0.activation), rank0, local_workers, int(serial),
@@ -521,7 +524,9 @@ def _train(plan: ParallelPlan, model0: MlpModel, train: Dataset, cv: Dataset, op
 def train_parallel(plan: ParallelPlan, model0: MlpModel, train: Dataset, cv: Dataset, opts: TrainOptions,
                    **placement) -> TrainResult:
     """train_parallel (parallel.hpp:73-75). ``placement`` (device, comm, rank0,
-    local_workers) spreads the m workers over processes/GPUs."""
+    local_workers) spreads the m workers over processes/GPUs; ``ctx`` and
+    ``device_data`` (DeviceDataset train / cv uploaded once) let repeated runs
+    share a context and the resident data set."""
     return _train(plan, model0, train, cv, opts, False, **placement)
 
 

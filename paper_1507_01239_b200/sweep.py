@@ -96,22 +96,46 @@ class RunConfig:
 
 
 _data_cache: dict = {}
+_device_cache: dict = {}
+
+
+def _key(cfg: RunConfig):
+    return (cfg.dims[-1], cfg.dims[0], cfg.per_class, cfg.separation, cfg.data_seed, cfg.cv_fraction, cfg.split_seed)
 
 
 def _data(cfg: RunConfig):
-    key = (cfg.dims[-1], cfg.dims[0], cfg.per_class, cfg.separation, cfg.data_seed, cfg.cv_fraction, cfg.split_seed)
+    key = _key(cfg)
     if key not in _data_cache:
         _data_cache.clear()
+        _device_cache.clear()
         _data_cache[key] = P.make_data(*key, True)
     return _data_cache[key]
 
 
-def run(cfg: RunConfig, ctx: P.Context | None = None) -> P.TrainResult:
-    """SPEC.md:526-532 ``run`` minus file plumbing: serial when workers == 1
-    and avg_frequency == 1 is not forced; ``train_parallel`` otherwise."""
+def _device_data(cfg: RunConfig, ctx: P.Context):
+    """The run's train / CV sets uploaded once per (data recipe, context)."""
     train, cv = _data(cfg)
-    model0 = P.init_random(list(cfg.dims), seed=cfg.init_seed)
-    return P.train_parallel(cfg.plan, model0, train, cv, cfg.opts, ctx=ctx)
+    key = (_key(cfg), id(ctx))
+    if key not in _device_cache:
+        _device_cache.clear()
+        _device_cache[key] = (ctx, P.DeviceDataset(ctx, train), P.DeviceDataset(ctx, cv) if cv.size() else None)
+    return _device_cache[key][1:]
+
+
+_models: dict = {}
+
+
+def run(cfg: RunConfig, ctx: P.Context | None = None) -> P.TrainResult:
+    """SPEC.md:526-532 ``run`` minus file plumbing: ``train_parallel`` of
+    the config from ``init_random(dims, init_seed)``. With a context the data
+    set stays resident across runs."""
+    train, cv = _data(cfg)
+    mkey = (tuple(cfg.dims), cfg.init_seed)
+    if mkey not in _models:
+        _models.clear()
+        _models[mkey] = P.init_random(list(cfg.dims), seed=cfg.init_seed)
+    dd = _device_data(cfg, ctx) if ctx is not None else None
+    return P.train_parallel(cfg.plan, _models[mkey], train, cv, cfg.opts, ctx=ctx, device_data=dd)
 
 
 @dataclass
