@@ -10,6 +10,8 @@
 //    its bf16 operand copy.
 #include <nccl.h>
 
+#include <utility>
+
 #include "parallel.h"
 
 namespace pnb {
@@ -42,6 +44,68 @@ __global__ void tree_avg_kernel(const float* const* src, int m, long n, float sc
             if (shadow[k]) shadow[k][i] = __float2bfloat16_rn(v);
         }
     }
+}
+
+// Vectorised form for m <= 32 local replicas: each thread loads the m float4s
+// of its 4 elements into registers, then adds them in the same midpoint tree,
+// unrolled at compile time (bitwise equal to tree_sum_at), so all m loads are
+// in flight at once. Elements past the last whole float4 go through the scalar
+// tree in block 0.
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float add4(float a, float b) { return a + b; }
+
+template <int LO, int HI, typename V>
+__device__ __forceinline__ V tree_reg(const V* x) {
+    if constexpr (HI - LO == 1) {
+        return x[LO];
+    } else {
+        constexpr int MID = LO + (HI - LO) / 2;
+        return add4(tree_reg<LO, MID>(x), tree_reg<MID, HI>(x));
+    }
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) tree_avg4_kernel(const float* const* src, long n, float scale, int apply_scale,
+                                                        float* const* dst, bf16* const* shadow, int ndst) {
+    const long n4 = n / 4;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+        float4 x[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) x[k] = reinterpret_cast<const float4*>(src[k])[i];  // warp-uniform pointer loads
+        float4 v = tree_reg<0, M>(x);
+        if (apply_scale) v = make_float4(v.x * scale, v.y * scale, v.z * scale, v.w * scale);
+        for (int k = 0; k < ndst; ++k) {
+            reinterpret_cast<float4*>(dst[k])[i] = v;
+            if (shadow[k]) {
+                const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+                reinterpret_cast<uint2*>(shadow[k])[i] =
+                    make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+            }
+        }
+    }
+    const long t = 4 * n4 + threadIdx.x;
+    if (blockIdx.x == 0 && t < n) {
+        float x[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) x[k] = src[k][t];
+        float v = tree_reg<0, M>(x);
+        if (apply_scale) v *= scale;
+        for (int k = 0; k < ndst; ++k) {
+            dst[k][t] = v;
+            if (shadow[k]) shadow[k][t] = __float2bfloat16_rn(v);
+        }
+    }
+}
+
+using AvgFn = void (*)(const float* const*, long, float, int, float* const*, bf16* const*, int);
+
+template <int... Ms>
+AvgFn avg4_pick(int m, std::integer_sequence<int, Ms...>) {
+    AvgFn fn = nullptr;
+    ((m == Ms + 1 ? (fn = &tree_avg4_kernel<Ms + 1>, 0) : 0), ...);
+    return fn;
 }
 
 __global__ void bf16_copy_kernel(const float* __restrict__ src, long n, bf16* __restrict__ dst) {
@@ -130,9 +194,19 @@ void Averager::run() {
     }
     const float inv = static_cast<float>(1.0 / static_cast<double>(m_total));
     const int grid = ctx->num_sms * 8;
+    // float4 params / 8-byte bf16 shadows (cudaMalloc'd replica buffers always are)
+    bool vec_ok = true;
+    for (Replica* r : reps)
+        vec_ok = vec_ok && (reinterpret_cast<uintptr_t>(r->params) & 15) == 0 &&
+                 (reinterpret_cast<uintptr_t>(r->wshadow) & 7) == 0;
+    if (scratch) vec_ok = vec_ok && (reinterpret_cast<uintptr_t>(scratch) & 15) == 0;
     if (!comm) {
-        if (k > 1)
-            tree_avg_kernel<<<grid, 256, 0, s>>>(d_src, k, n, inv, 1, d_src, d_shadow, k);
+        if (k > 1) {
+            if (AvgFn f = vec_ok ? avg4_pick(k, std::make_integer_sequence<int, 32>{}) : nullptr)
+                f<<<grid, 256, 0, s>>>(d_src, n, inv, 1, d_src, d_shadow, k);
+            else
+                tree_avg_kernel<<<grid, 256, 0, s>>>(d_src, k, n, inv, 1, d_src, d_shadow, k);
+        }
         else if (m_total != 1)
             throw std::runtime_error("allreduce_average: got 1 contributions for m = " + std::to_string(m_total));
         // m == 1: x * 1.0 is the identity (parallel.cpp:56-57), nothing to do.
@@ -146,7 +220,10 @@ void Averager::run() {
         if (reps[0]->wshadow) bf16_copy_kernel<<<grid, 256, 0, s>>>(reps[0]->params, n, reps[0]->wshadow);
     } else {
         // local subtree sum -> NCCL sum over GPUs -> x 1/m into every local replica
-        tree_avg_kernel<<<grid, 256, 0, s>>>(d_src, k, n, 1.f, 0, d_scratch_ptr, d_shadow, 0);
+        if (AvgFn f = vec_ok ? avg4_pick(k, std::make_integer_sequence<int, 32>{}) : nullptr)
+            f<<<grid, 256, 0, s>>>(d_src, n, 1.f, 0, d_scratch_ptr, d_shadow, 0);
+        else
+            tree_avg_kernel<<<grid, 256, 0, s>>>(d_src, k, n, 1.f, 0, d_scratch_ptr, d_shadow, 0);
         NCCL_THROW(ncclAllReduce(scratch, scratch, n, ncclFloat, ncclSum, static_cast<ncclComm_t>(comm->comm), s));
         tree_avg_kernel<<<grid, 256, 0, s>>>(d_scratch_ptr, 1, n, inv, 1, d_src, d_shadow, k);
     }

@@ -145,7 +145,7 @@ def test_serial_equals_parallel_m1_and_is_deterministic(ctx, golden):
     assert np.array_equal(b.model.params, c.model.params)
 
 
-@pytest.mark.parametrize("m", [2, 3, 4, 8])
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 8, 16, 32])
 def test_device_average_matches_tree(ctx, m):
     dims = [20, 33, 7]
     x = np.random.default_rng(0).standard_normal((40, 20))
@@ -164,7 +164,7 @@ def test_device_average_matches_tree(ctx, m):
     for o in out:
         assert np.array_equal(o, out[0])  # every worker sees the identical vector
     assert np.abs(out[0] - ref).max() < 1e-6 * max(1.0, np.abs(ref).max())
-    if m in (2, 4, 8):  # power of two: fp32 tree sum of fp32 inputs, exact scale
+    if m in (2, 4, 8, 16, 32):  # power of two: fp32 tree sum of fp32 inputs, exact scale
         t = O.tree_sum([v.astype(np.float32) for v in vecs], 0, m) * np.float32(1.0 / m)
         assert np.array_equal(out[0].astype(np.float32), t.astype(np.float32))
 
