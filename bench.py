@@ -1,29 +1,41 @@
 #!/usr/bin/env python
 """Benchmark of the model-averaging DNN trainer path (BASELINE.json).
 
-Workload (N=1): config 2 of BASELINE.json — Switchboard-shaped DNN
-440-2048x6-8806 sigmoid, NG-SGD, minibatch 1024, synthetic frames from the
-reference's own generate_synthetic recipe. NG-SGD is the north star's online
-low-rank preconditioner by default (--optimizer ngsgd_lowrank); the
-reference's kron-full NG-SGD is timed on the same data in the same run
-("ngsgd_kron_full") and is selectable with --optimizer ngsgd. N>1 (torchrun): config 3 — one replica per GPU,
-model averaging every 4 minibatches over NCCL (weak scaling: each GPU does
-the same per-step work).
+Workload: config 2 of BASELINE.json at N=1 -- Switchboard-shaped DNN
+440-2048x6-8806 sigmoid, NG-SGD, minibatch 1024 -- and config 3 at N>1 (one
+replica per GPU, model averaging every 4 minibatches over NCCL; weak scaling:
+every GPU does the same per-step work). Synthetic frames come from the
+reference's own generate_synthetic + split_cv + standardize recipe.
+
+NG-SGD is the north star's online low-rank preconditioner (--optimizer
+ngsgd_lowrank, the default); the reference's own kron-full NG-SGD runs on the
+same data in the same process ("ngsgd_kron_full") and is selectable with
+--optimizer ngsgd.
 
 One "step" = one minibatch update on every replica (gather -> forward ->
-softmax-CE -> backward -> NG precondition (+ subspace update) -> SGD), plus the
-averaging event every --avg-frequency steps.
+softmax-CE -> backward -> NG precondition (+ subspace update) -> SGD), plus
+the averaging event every --avg-frequency steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Rank 0 prints ONE JSON line (metric/value/unit/... + roofline, cpu_baseline,
-e2e, clocks, gpu_launches).
+With --gpus N > 1 and no torchrun environment, the script relaunches itself
+under torch.distributed.run with N ranks (127.0.0.1). Rank 0 prints ONE JSON
+line (metric/value/unit/... + roofline, cpu_baseline, e2e, clocks,
+gpu_launches).
+
+--impl reference times the UNMODIFIED reference (oracle/_ref, compiled from
+its sources): one true-width config-2 minibatch with its own kron-full NG-SGD
+on all host cores. One such step takes minutes of CPU time, so the reference
+line reports steps = 1, warmup = 0 (nothing is extrapolated).
 """
 import argparse
 import json
+import math
 import os
+import socket
 import subprocess
 import sys
+import threading
 import time
 
 import numpy as np
@@ -32,10 +44,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 DIMS = [440] + [2048] * 6 + [8806]
-OPT_DESC = {"ngsgd_lowrank": "NG-SGD (online low-rank Fisher, rank 20/80, update every 4)",
-            "ngsgd": "NG-SGD (the reference's kron-full Fisher)", "sgd": "plain SGD"}
+OPT_DESC = {"ngsgd_lowrank": "ngsgd_lowrank: online low-rank Fisher NG-SGD (north star; rank 20/80, subspace "
+                             "update every 4 steps)",
+            "ngsgd": "ngsgd: the reference's kron-full Kronecker-factored NG-SGD (optimizer.cpp:44-157)",
+            "sgd": "sgd: plain SGD"}
 METRIC = "training frames/sec (440-2048x6-8806 NG-SGD, minibatch 1024)"
 UNIT = "frames/s"
+SEPARATION = 8.0
 
 
 def flops_per_frame(dims):
@@ -45,92 +60,113 @@ def flops_per_frame(dims):
 
 def peaks():
     try:
-        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+        return ({"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0},
+                "fallback (B200_PROFILING.md)")
+
+
+def workload_config(args, world):
+    """The workload both arms run (identical dict in both JSON lines)."""
+    n = DIMS[-1] * args.per_class
+    n_train = n - math.ceil(0.10 * n)  # split_cv takes ceil(f N) to CV (data.cpp:178-179)
+    reps = "1 replica" if world == 1 else f"{world} replicas (one per GPU), averaging every {args.avg_frequency}"
+    return {
+        "workload": f"config {2 if world == 1 else 3}: 440-2048x6-8806 sigmoid NG-SGD, minibatch "
+                    f"{args.minibatch}, {reps}",
+        "global_batch": args.minibatch * world,
+        "parallelism": f"dp{world} model-averaging",
+        "avg_frequency": args.avg_frequency,
+        "data": (f"generate_synthetic({DIMS[-1]} classes x {args.per_class}, {DIMS[0]}-dim, s={SEPARATION:g}, "
+                 f"seed 1) -> split_cv(0.1, seed 2) -> standardize: {n_train} train frames"),
+        "l2": "inputs larger than L2: the resident training set is %.0f MB (bf16) and each step streams 160 MB of "
+              "fp32 parameters" % (n_train * 440 * 2 / 1e6),
+    }
 
 
 # ------------------------------------------------------------ CPU reference
-def reference_sample(steps, threads=1):
-    """Time the UNMODIFIED reference (oracle/_ref) on a bounded sample of the
-    config-2 step: the same network with every layer width scaled by 1/8
-    (55-256x6-1101), batch 1024. Per-phase times are extrapolated exactly by
-    the cost model of the reference loops: forward/backward/ng_update/sgd are
-    degree-2 in the widths (x64), ng_precondition (Cholesky + triangular
-    solves) is degree-3 (x512)."""
+def reference_step(per_class, threads=None):
+    """One TRUE-WIDTH config-2 minibatch of the UNMODIFIED reference
+    (oracle/_ref): worker_epoch's body (parallel.cpp:117-130) with the
+    reference's own kron-full NG-SGD, at 440-2048x6-8806, batch 1024, on the
+    same synthetic frames as our arm, built from the reference's public
+    functions and spread over all host cores (ref_time_step_threaded; equal to
+    the single-threaded reference step up to fp64 summation order). Nothing is
+    extrapolated: the value is 1024 frames / the measured wall time."""
     from oracle.ref_lib import RefLib, available
     if not available():
         raise RuntimeError("oracle/_ref/libparnn_ref.so missing (make -C oracle)")
+    from paper_1507_01239_b200 import parnn as P
     R = RefLib()
-    s = 8
-    dims = [max(1, d // s) for d in DIMS]
-    rng = np.random.default_rng(0)
-    n = 4096
-    x = rng.standard_normal((n, dims[0]))
-    y = rng.integers(0, dims[-1], n).astype(np.int32)
-    p0 = R.init_random(dims, 1)
-    t0 = time.perf_counter()
-    fps_s, ph = R.time_steps(dims, p0, x, y, 1024, steps, True, threads)
-    wall = time.perf_counter() - t0
-    per_step = ph / steps
-    est = (per_step[0] + per_step[1] + per_step[2] + per_step[4]) * s ** 2 + per_step[3] * s ** 3
+    threads = threads or os.cpu_count() or 1
+    train, _ = P.make_data(DIMS[-1], DIMS[0], per_class, SEPARATION, 1, 0.10, 2, True)
+    order = P.minibatch_rows(train.size(), 1024, int(P.rng_u64(0, 1)[0]))[0].astype(np.int64)
+    x, y = train.features[order], train.labels[order]
+    p0 = R.init_random(DIMS, 7)
+    wall, ph, _, ce = R.time_step_threaded(DIMS, p0, x, y, True, threads)
+    names = ["forward+ce", "backward", "ng_moments", "ng_factor+solve1+bias", "ng_solve2", "ng_gamma", "sgd"]
     return {
-        "value": 1024.0 * threads / est,
-        "unit": UNIT,
-        "cores": threads,
-        "kind": "reference",
-        "sample": (f"{steps} reference step(s) of 55-256x6-1101 NG-SGD at minibatch 1024 "
-                   f"({wall:.1f} s CPU); fwd/bwd/ng_update/sgd x64 and ng_precondition x512 "
-                   f"(width^2 / width^3 cost of the reference loops) -> {est:.1f} s per config-2 step"),
-        "phase_seconds_extrapolated": {"forward+ce": per_step[0] * 64, "backward": per_step[1] * 64,
-                                       "ng_update_state": per_step[2] * 64, "ng_precondition": per_step[3] * 512,
-                                       "sgd": per_step[4] * 64},
+        "value": 1024.0 / wall, "unit": UNIT, "cores": threads, "kind": "reference",
+        "sample": ("one full config-2 minibatch (440-2048x6-8806, batch 1024, kron-full NG-SGD, fp64) of the "
+                   "unmodified reference's own functions on %d host threads: %.1f s wall, no extrapolation"
+                   % (threads, wall)),
+        "phase_seconds": {n: round(float(t), 3) for n, t in zip(names, ph)},
+        "batch_ce": ce, "wall_seconds": wall,
     }
 
 
 # -------------------------------------------------------------- clocks
 class ClockSampler:
-    def __init__(self, path):
-        self.path = path
-        self.proc = None
+    """NVML polling thread (~1 ms) over the timed region: SM clock, max clock
+    and the throttle reasons seen while the GPU is busy."""
+    BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+            0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device):
+        self.device, self.samples, self.reasons, self.max_mhz = device, [], set(), None
+        self.err = None
 
     def __enter__(self):
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self.stop = threading.Event()
         try:
-            self.f = open(self.path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        util = pynvml.nvmlDeviceGetUtilizationRates(h).gpu
+                        mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    except Exception as e:  # noqa: BLE001
+                        self.err = str(e)
+                        return
+                    self.samples.append((float(mhz), int(util)))
+                    for bit, name in self.BITS.items():
+                        if rs & bit:
+                            self.reasons.add(name)
+                    time.sleep(0.001)
+
+            self.th = threading.Thread(target=poll, daemon=True)
+            self.th.start()
+        except Exception as e:  # noqa: BLE001
+            self.err, self.th = str(e), None
         return self
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            self.proc.wait()
-            self.f.close()
+        self.stop.set()
+        if getattr(self, "th", None):
+            self.th.join()
 
-    def summary(self, device=0):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            f = [v.strip() for v in line.split(",")]
-            if len(f) < 9 or f[0] != str(device):
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0,
+                    "note": self.err or "no samples"}
+        busy = [m for m, u in self.samples if u > 0] or [m for m, _ in self.samples]
+        return {"sm_mhz": float(np.median(busy)), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "samples_busy": len(busy), "source": "NVML, ~1 ms polling"}
 
 
 # -------------------------------------------------------------- our arm
@@ -153,9 +189,17 @@ def run_ours(args, rank, world, local_rank):
         dist.broadcast_object_list(uid, src=0)
         comm = P.Comm(ctx, uid[0], world, rank)
 
-    # synthetic Switchboard-shaped frames (generate_synthetic + split + standardize, data.cpp:124-242)
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # synthetic Switchboard-shaped frames (generate_synthetic + split + standardize, data.cpp:124-242);
+    # worker r trains on shard r of partition_data (parallel.cpp:61-77)
     t0 = time.perf_counter()
-    train, _ = P.make_data(DIMS[-1], DIMS[0], args.per_class, 8.0, 1, 0.10, 2, True)
+    train, _ = P.make_data(DIMS[-1], DIMS[0], args.per_class, SEPARATION, 1, 0.10, 2, True)
     shards = P.partition_rows(train.size(), world, 0)
     ds = P.DeviceDataset(ctx, train)
     gen_s = time.perf_counter() - t0
@@ -170,25 +214,86 @@ def run_ours(args, rank, world, local_rank):
     rows = np.resize(rows, need * B)
     lrs = np.full(need, 1e-3, np.float32)
     rep.upload_epoch(rows, lrs)
-    rep.step(W)
+    if W:
+        P.run_steps([rep], W, args.avg_frequency, comm=comm, m_total=world)  # warm-up, averaging included
     rep.sync()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    clk = ClockSampler(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else ".",
-                                    f"clocks_rank{rank}.csv"))
-    with clk:
-        ms = P.run_steps([rep], K, args.avg_frequency, comm=comm, m_total=world)
+    with ClockSampler(local_rank) as clk:
+        ms = P.run_steps([rep], K, args.avg_frequency, comm=comm, m_total=world)  # CUDA events, this rank
     rep.sync()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms)
     ms_per_step = ms / K
     value = world * B * K / (ms / 1e3)
     ce = rep.ce(W + K)
+
+    # ---- averaging alone: NVLink bus bandwidth (N > 1)
+    avg = None
+    if world > 1:
+        a_ms, a_bytes = P.time_average([rep], comm=comm, m_total=world, iters=10)
+        a_ms = max_over_ranks(a_ms)
+        avg = {"ms_per_event": a_ms, "bytes_per_event": a_bytes, "events_per_step": 1.0 / args.avg_frequency,
+               "bus_gbs": 2.0 * (world - 1) / world * a_bytes / (a_ms / 1e3) / 1e9,
+               "how": "per-layer ncclAllReduce(ncclAvg) buckets + bf16 copy, 10 back-to-back events, CUDA events, "
+                      "max over ranks; bus GB/s = 2(n-1)/n * bytes / time"}
+
+    # ---- end-to-end through the C ABI with host buffers (every rank): per step, host
+    # batch assembly into pinned staging (double buffered), H2D (parnn_dataset_write_f32),
+    # the step, the averaging event every avg_frequency steps (parnn_averager_run), and the
+    # D2H read of a step's loss (parnn_replica_step_ce, one step behind, so copies and
+    # host work overlap the GPU). Wall clock, max over ranks.
+    e2e = None
+    if not args.no_e2e:
+        E = args.e2e_steps
+        pins = [torch.empty((B, DIMS[0]), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        pinys = [torch.empty((B,), dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        stage = P.DeviceDataset(ctx, P.Dataset(train.features[:2 * B], train.labels[:2 * B], DIMS[-1]))
+        rep_e = P.Replica(ctx, DIMS, precision=prec, optimizer=opt, minibatch=B, max_steps=E + 4)
+        rep_e.set_params(m0.params)
+        rep_e.bind(stage)
+        rep_e.upload_epoch(np.concatenate([np.arange(B) + (i % 2) * B for i in range(E + 4)]),
+                           np.full(E + 4, 1e-3, np.float32))
+        avg_e = P.Averager([rep_e], comm=comm, m_total=world)
+        src = torch.from_numpy(shards[rank][np.random.default_rng(3 + rank).integers(0, S, (E + 4, B))].astype(np.int64))
+        # host-resident training frames in the device dataset's element type (fp32),
+        # converted once like the upload in parnn_dataset_create; the per-step row
+        # gather runs on the host's threads straight into the pinned staging buffer
+        host_x = torch.from_numpy(np.ascontiguousarray(train.features, dtype=np.float32))
+        host_y = torch.from_numpy(np.ascontiguousarray(train.labels, dtype=np.int32))
+
+        def stage_step(i):
+            torch.index_select(host_x, 0, src[i], out=pins[i % 2])  # host-side batch assembly
+            torch.index_select(host_y, 0, src[i], out=pinys[i % 2])
+            stage.write_rows(pins[i % 2].numpy(), pinys[i % 2].numpy(), row0=(i % 2) * B)  # H2D of this step's inputs
+            rep_e.step(1)
+            if (i + 1) % args.avg_frequency == 0:
+                avg_e.run()
+
+        stage_step(0)
+        stage_step(1)
+        rep_e.step_ce(1)  # warm (includes the low-rank init step)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(2, 2 + E):
+            stage_step(i)
+            ce_e = rep_e.step_ce(i - 1)  # D2H of the previous step's loss
+        ce_e = rep_e.step_ce(1 + E)
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": world * B * E / e2e_s, "unit": UNIT, "h2d_bytes_per_step": B * DIMS[0] * 4 + B * 4,
+               "d2h_bytes_per_step": 8, "steps": E,
+               "path": "host batch assembly (fp32 host frames, threaded row gather) -> pinned staging -> "
+                       "parnn_dataset_write_f32 (H2D) + parnn_replica_step (+ parnn_averager_run every "
+                       f"{args.avg_frequency}) + parnn_replica_step_ce (D2H loss, one step behind); wall clock, "
+                       "max over ranks",
+               "last_ce": float(ce_e)}
+        avg_e.close()
+        rep_e.close()
+
     out = {"_rank": rank}
     if rank != 0:
         return out
@@ -210,13 +315,13 @@ def run_ours(args, rank, world, local_rank):
     gemm_kinds = [k for k in by_kind if k.startswith("gemm_") and k != "gemm_ng_moments"]
     g_ms = sum(by_kind[k][0] for k in gemm_kinds)
     g_fl = sum(by_kind[k][1] for k in gemm_kinds)
-    peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    burst = pk["bf16_tflops"]
+    sustained = pk.get("bf16_tflops_sustained", burst)
     achieved = (d_fl / d_n) / (d_ms / d_n / 1e3) / 1e12 if d_fl > 0 else None
-    # DRAM bytes per launch of the dominant kernel from the committed ncu --set full
-    # capture (dram__bytes_read.sum + dram__bytes_write.sum, profiles/)
     # algorithmic bytes of one dW launch (avg over layers): fp32 W read + write, bf16 shadow
     # write, and the two bf16 operands (B x dout, B x (din + 1))
     dw_bytes = sum(10.0 * o * (i + 1) + 2.0 * B * (o + i + 1) for i, o in zip(DIMS[:-1], DIMS[1:])) / (len(DIMS) - 1)
+    # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "dominant_traffic.json")
     if os.path.exists(tpath):
@@ -225,69 +330,30 @@ def run_ours(args, rank, world, local_rank):
             traffic, traffic_src = t.get("bytes_per_launch"), t.get("source")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
-                "frac": (achieved / peak_t) if achieved else None, "traffic": traffic,
-                "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
+    step_flops = flops_per_frame(DIMS) * B
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
+                "frac": (achieved / burst) if achieved else None, "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": dw_bytes,
-                "peak_source": f"{how} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+                "peak_source": f"{how} bf16_tflops (burst: each launch is timed alone in the eager profile)",
                 "launches_per_step": d_n, "ms_per_step": d_ms,
                 "note": ("tcgen05 GEMM region, algorithmic flops (2MNK per launch) / CUDA-event time of the region "
-                         "in an eager serial profile of %d steps (one low-rank update period)" % args.profile_steps)}
-    model_gemm = {"achieved": g_fl / (g_ms / 1e3) / 1e12, "peak": peak_t, "unit": "TFLOP/s",
-                  "frac": g_fl / (g_ms / 1e3) / 1e12 / peak_t, "ms_per_step": g_ms,
+                         "in an eager serial profile of %d steps (one low-rank update period)" % args.profile_steps),
+                "step": {"achieved": step_flops / (ms_per_step / 1e3) / 1e12, "peak": sustained,
+                         "frac": step_flops / (ms_per_step / 1e3) / 1e12 / sustained,
+                         "note": "whole step: model GEMM flops per minibatch (2.376e8 x B) / the timed ms_per_step, "
+                                 "against bf16_tflops_sustained (a long back-to-back run)"}}
+    model_gemm = {"achieved": g_fl / (g_ms / 1e3) / 1e12, "peak": burst, "unit": "TFLOP/s",
+                  "frac": g_fl / (g_ms / 1e3) / 1e12 / burst, "ms_per_step": g_ms,
                   "flops_per_step": g_fl, "kinds": gemm_kinds}
-
-    # ---- end-to-end through the C ABI with host buffers: per step, host batch
-    # assembly into pinned staging (double buffered), H2D (parnn_dataset_write_f32),
-    # the step, and the D2H read of a step's loss (parnn_replica_step_ce). The loss
-    # of step i is read after step i+1 has been queued, so the copies and the host
-    # work overlap the GPU instead of serialising with it.
-    e2e = None
-    if not args.no_e2e:
-        E = args.e2e_steps
-        pins = [torch.empty((B, DIMS[0]), dtype=torch.float32, pin_memory=True) for _ in range(2)]
-        pinys = [torch.empty((B,), dtype=torch.int32, pin_memory=True) for _ in range(2)]
-        stage = P.DeviceDataset(ctx, P.Dataset(train.features[:2 * B], train.labels[:2 * B], DIMS[-1]))
-        rep_e = P.Replica(ctx, DIMS, precision=prec, optimizer=opt, minibatch=B, max_steps=E + 4)
-        rep_e.set_params(m0.params)
-        rep_e.bind(stage)
-        rep_e.upload_epoch(np.concatenate([np.arange(B) + (i % 2) * B for i in range(E + 4)]),
-                           np.full(E + 4, 1e-3, np.float32))
-        src = torch.from_numpy(np.random.default_rng(3).integers(0, train.size(), (E + 4, B)))
-        # host-resident training frames in the device dataset's element type (fp32),
-        # converted once like the upload in parnn_dataset_create; the per-step row
-        # gather runs on the host's threads straight into the pinned staging buffer
-        host_x = torch.from_numpy(np.ascontiguousarray(train.features, dtype=np.float32))
-        host_y = torch.from_numpy(np.ascontiguousarray(train.labels, dtype=np.int32))
-
-        def stage_step(i):
-            torch.index_select(host_x, 0, src[i], out=pins[i % 2])  # host-side batch assembly
-            torch.index_select(host_y, 0, src[i], out=pinys[i % 2])
-            stage.write_rows(pins[i % 2].numpy(), pinys[i % 2].numpy(), row0=(i % 2) * B)  # H2D of this step's inputs
-            rep_e.step(1)
-
-        stage_step(0)
-        stage_step(1)
-        rep_e.step_ce(1)  # warm (includes the low-rank init step)
-        t0 = time.perf_counter()
-        for i in range(2, 2 + E):
-            stage_step(i)
-            ce_e = rep_e.step_ce(i - 1)  # D2H of the previous step's loss
-        ce_e = rep_e.step_ce(1 + E)
-        e2e_s = time.perf_counter() - t0
-        e2e = {"value": B * E / e2e_s, "unit": UNIT, "h2d_bytes_per_step": B * DIMS[0] * 4 + B * 4,
-               "d2h_bytes_per_step": 8, "steps": E,
-               "path": "host batch assembly (fp32 host frames, threaded row gather) -> pinned staging -> parnn_dataset_write_f32 (H2D) + parnn_replica_step "
-                       "+ parnn_replica_step_ce (D2H loss, one step behind), wall clock",
-               "last_ce": float(ce_e)}
-        rep_e.close()
 
     cpu = None
     if world == 1 and not args.no_cpu:
         try:
-            cpu = reference_sample(1)
+            cpu = reference_step(args.per_class)
         except Exception as e:  # reported, not fatal
-            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
 
     # ---- the reference's own NG variant (kron-full) on the same data, same clock
     kron = None
@@ -299,62 +365,73 @@ def run_ours(args, rank, world, local_rank):
         rk.step(2)
         rk.sync()
         kms = rk.time_steps(4) / 4
-        kron = {"optimizer": "ngsgd (kron-full, the reference's NG-SGD)", "value": B / (kms / 1e3), "unit": UNIT,
+        kron = {"optimizer": OPT_DESC["ngsgd"], "value": B / (kms / 1e3), "unit": UNIT,
                 "ms_per_step": kms, "kernels_per_step": rk.kernels_per_step(), "steps": 4,
-                "timing": "CUDA events on the replica stream, graph launches"}
+                "timing": "CUDA events on the replica stream, graph launches",
+                "vs_cpu_reference": (B / (kms / 1e3)) / cpu["value"] if cpu and cpu.get("value") else None,
+                "note": "like-for-like: the same NG-SGD algorithm as the reference arm (bf16 operands here)"}
         rk.close()
 
     kps = rep.kernels_per_step()
+    events = -(-K // args.avg_frequency)
+    avg_kernels = 0 if world == 1 else (len(DIMS) - 1) * (2 if prec == P.Precision.bf16 else 1)
     out.update({
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": args.precision, "data": f"synthetic (generate_synthetic 8806x{args.per_class}, 440-dim, s=8)",
-        "config": {"workload": f"config 2: 440-2048x6-8806 sigmoid {OPT_DESC[args.optimizer]}, "
-                               f"minibatch {B}, {'1 replica' if world == 1 else f'{world} replicas, averaging every {args.avg_frequency}'}",
-                   "global_batch": B * world, "parallelism": f"dp{world} model-averaging",
-                   "precision": f"{args.precision} operands, fp32 accumulate, fp32 NG solves",
-                   "l2": "inputs larger than L2 (dataset %.0f MB + 160 MB fp32 params + NG factors per step)"
-                         % (train.size() * 440 * (2 if prec == P.Precision.bf16 else 4) / 1e6),
-                   "data_gen_seconds": gen_s},
-        "clocks": clk.summary(local_rank),
-        "gpu_launches": int(kps * K + (K // args.avg_frequency) * (0 if world == 1 else 2)),
+        "dtype": args.precision, "data": "synthetic",
+        "optimizer": OPT_DESC[args.optimizer],
+        "precision": f"{args.precision} operands, fp32 accumulate, fp32 master weights and NG solves",
+        "config": workload_config(args, world),
+        "clocks": clk.summary(),
+        "gpu_launches": int(kps * K + events * avg_kernels),
         "kernels_per_step": kps,
         "roofline": roofline,
         "model_gemm_roofline": model_gemm,
         "model_flops_per_frame": flops_per_frame(DIMS),
+        "averaging": avg,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "ngsgd_kron_full": kron,
         "final_ce": float(ce[-1]),
+        "data_gen_seconds": gen_s,
         "regions_ms": {k: round(v[0], 4) for k, v in sorted(by_kind.items(), key=lambda kv: -kv[1][0])},
     })
     return out
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the unmodified reference (oracle/_ref) on this box's
+    host cores, on the same workload dict as our arm. Rank 0 alone runs it.
+    One true-width step; at N > 1 the host's cores are already saturated by one
+    replica's step (N replicas take N times as long on the same cores), so the
+    frames/s of the whole job is the same as at N = 1 and one step is timed."""
     if rank != 0:
         return None
-    t0 = time.perf_counter()
-    samples = []
     try:
-        for _ in range(args.warmup_ref):
-            reference_sample(1)
-        for _ in range(args.steps_ref):
-            samples.append(reference_sample(1))
+        s = reference_step(args.per_class)
     except Exception as e:
         return {"impl": "reference", "unavailable": str(e).splitlines()[0]}
-    v = float(np.mean([s["value"] for s in samples]))
-    cpu = dict(samples[-1])
-    cpu["value"] = v
-    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": len(samples),
-            "warmup": args.warmup_ref, "ms_per_step": 1024.0 / v * 1e3, "higher_is_better": True, "scaling": "weak",
+    v = s["value"]
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": 1,
+            "warmup": 0, "ms_per_step": s["wall_seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config 2: 440-2048x6-8806 sigmoid ngsgd (kron-full NG), minibatch 1024, "
-                                   "reference CPU trainer (1 worker = 1 thread)", "global_batch": 1024,
-                       "parallelism": "1 worker"},
-            "cpu_baseline": cpu,
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "wall_seconds": time.perf_counter() - t0}
+            "optimizer": OPT_DESC["ngsgd"],
+            "precision": "fp64 (the reference's only arithmetic)",
+            "config": workload_config(args, world),
+            "cpu_baseline": s,
+            "replicas_timed": 1,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def spawn(args_list, n):
+    """--gpus N without a torchrun environment: relaunch under torch.distributed.run."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + args_list
+    return subprocess.call(cmd)
 
 
 def main():
@@ -376,12 +453,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(sys.argv[1:], args.gpus))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
-        args.warmup_ref = 0
-        args.steps_ref = max(1, min(args.steps, 3))
         out = run_reference(args, rank, world)
         if out is not None:
             print(json.dumps(out), flush=True)

@@ -126,6 +126,24 @@ int parnn_replica_lowrank_diag(parnn_replica* r, int layer, int side, double out
  * and M (R x 2R, W' = M [J; W]). */
 int parnn_debug_lowrank_eig(int rank, uint64_t dim, double eta, double a, double alpha, const double* state_in,
                             const float* gram, double* state_out, float* m_out, int* sweeps);
+/* Test hook: ONE production tcgen05 GEMM (the trainer's gemm_plan tile / cluster
+ * selection, kernels and fused epilogues) on host fp32 data:
+ *   D[m, n] = sum_k A(m, k) B(n, k),  A given as [M x K] (a_mn = 0) or [K x M]
+ *   (a_mn = 1), B as [N x K] (b_mn = 0) or [K x N] (b_mn = 1), operands rounded
+ *   to the precision's type, fp32 accumulation, then epilogue `mode`
+ *   (gemm.cuh EpiMode: 0 act(D + bias[n]), 1 D + bias[n], 2 alpha D,
+ *   3 out -= lr alpha D (+ bias column `bias_col` -> bias[m]), 4 D * act'(aux),
+ *   5 beta out + alpha D, 6 out += alpha D, 7 out -= D, 8 split-K partials
+ *   (summed into out), 9 aux - D (+ sums {aux^2, out^2})).
+ * out (M x N) is read for the read-modify-write modes and receives the result;
+ * out2 receives the bf16 operand copy (modes 3, 6 in bf16) or the updated bias
+ * (mode 3 with bias_col >= 0). force_mc: 0 auto, 1 single-CTA tiles, 2 CTA
+ * pairs with 2-SM MMAs, 3 split-K CTA pairs. info[6] = {cluster mode, BN,
+ * split-K factor, non-finite flag bits, grid, threads}. */
+int parnn_debug_gemm(int precision, int a_mn, int b_mn, int m, int n, int k, int mode, int act, int ksplit,
+                     int force_bn, int force_mc, int lower, int bias_col, float alpha, float beta, float lr,
+                     const float* a, const float* b, const float* bias, const float* aux, float* out, float* out2,
+                     double* sums, int* info);
 /* Build the step's GEMM plans + CUDA graph against a training dataset. */
 int parnn_replica_bind(parnn_replica* r, parnn_dataset* train);
 /* Upload one epoch: steps*minibatch dataset row ids (Dataset::select order) and per-step lr. */
@@ -165,6 +183,19 @@ int parnn_comm_destroy(parnn_comm* c);
 /* allreduce_average (parallel.cpp:40-59) over the local replicas (+ comm):
  * every replica is replaced by the mean over m_total workers. */
 int parnn_average(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_t m_total);
+/* A persistent averaging group over the local replicas (+ comm): run() enqueues
+ * one averaging event (per-layer buckets, event-gated into each replica's next
+ * forward) without blocking the host, as train_parallel's loop does. */
+typedef struct parnn_averager parnn_averager;
+int parnn_averager_create(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_t m_total,
+                          parnn_averager** out);
+int parnn_averager_run(parnn_averager* a);
+int parnn_averager_destroy(parnn_averager* a);
+/* Device time (CUDA events on the averaging stream) of `iters` back-to-back
+ * averaging events: ms per event, and the fp32 bytes one event reduces per GPU
+ * (bus bandwidth = 2 (n-1)/n * bytes / time over n GPUs). */
+int parnn_time_average(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_t m_total, uint64_t iters,
+                       double* ms_per_event, double* bytes);
 /* worker_epoch's inner loop (parallel.cpp:106-137) for benchmarking: `steps`
  * minibatch updates on every local replica with an averaging event every
  * avg_frequency updates (and one closing the window); device time in ms. */
@@ -226,6 +257,18 @@ int parnn_rbm_reconstruction_error(parnn_rbm* r, const double* x, uint64_t n, do
 int parnn_greedy_pretrain(parnn_ctx* ctx, const uint64_t* dims, int ndims, const double* data, uint64_t n,
                           uint64_t epochs, double lr_gaussian, double lr_bernoulli, uint64_t batch, uint64_t seed,
                           int precision, double* params_out);
+
+/* greedy_pretrain (pretrain.hpp:74-76) on the CALLER's Rng: rng_state /
+ * rng_spare / rng_has_spare hold the xoshiro256** state words and the polar
+ * gaussian cache of the caller's parnn::Rng (rng.hpp) and are updated in place
+ * to the state the reference leaves (rbm_init, per-epoch shuffles and the
+ * Bernoulli draws consumed exactly as pretrain.cpp:162-207 does; the output
+ * layer's Glorot init is bit-identical). `activation` is the model's
+ * (network.hpp:16); RBM layers are sigmoid as in the reference. */
+int parnn_greedy_pretrain_rng(parnn_ctx* ctx, const uint64_t* dims, int ndims, const double* data, uint64_t n,
+                              uint64_t epochs, double lr_gaussian, double lr_bernoulli, uint64_t batch,
+                              int activation, uint64_t rng_state[4], double* rng_spare, int* rng_has_spare,
+                              int precision, double* params_out);
 
 #ifdef __cplusplus
 }

@@ -7,7 +7,9 @@
 // the reference's message text.
 #pragma once
 #include <cstdint>
+#include <cstring>
 #include <memory>
+#include <type_traits>
 #include <vector>
 
 #include "parnn/data.hpp"
@@ -15,6 +17,7 @@
 #include "parnn/network.hpp"
 #include "parnn/parallel.hpp"
 #include "parnn/pretrain.hpp"
+#include "parnn/rng.hpp"
 #include "parnn_b200.h"
 
 namespace parnn {
@@ -22,7 +25,9 @@ namespace b200 {
 
 struct Options {
     int device = 0;
-    int precision = PARNN_BF16;  // PARNN_FP32 for the fp32 parity mode
+    // PARNN_FP32 (3xTF32 operands, fp32 everything else) is the default: the
+    // closest to the reference's fp64 results. PARNN_BF16 is the fast mode.
+    int precision = PARNN_FP32;
     // OptimizerKind::ngsgd runs the reference's kron-full NG-SGD by default; with
     // lowrank_ng it runs the online low-rank NG-SGD (rank-R Fisher projection and
     // subspace update; alpha = opts.ng_smoothing). 0 = the defaults (20, 80, 4, 2000, 3).
@@ -129,6 +134,50 @@ inline TrainResult serial_train(const MlpModel& model0, const Dataset& train, co
     p.minibatch = minibatch;
     p.base_seed = base_seed;
     return detail::run(p, model0, train, cv, opts, true, o);
+}
+
+// pretrain.hpp:74-76. The caller's Rng is advanced exactly as the reference's
+// greedy_pretrain advances it (rbm_init, the per-epoch shuffles, the Bernoulli
+// draws it would consume, the output-layer init); its state crosses the C ABI
+// as the object's own words. parnn::Rng is a standard-layout, trivially
+// copyable class {uint64_t state_[4]; double spare_; bool has_spare_;}
+// (rng.hpp), so its bytes are read and written with memcpy.
+inline MlpModel greedy_pretrain(const std::vector<std::size_t>& dims, const Matrix& data,
+                                const PretrainOptions& opts, Activation activation, Rng& rng,
+                                const Options& o = {}) {
+    static_assert(std::is_trivially_copyable_v<Rng> && std::is_standard_layout_v<Rng>, "Rng layout");
+    static_assert(sizeof(Rng) == 48, "Rng = {uint64_t[4], double, bool}");
+    if (dims.size() < 2) fail("greedy_pretrain: need at least 2 dims");
+    if (data.cols() != dims.front())
+        fail("greedy_pretrain: data has ", data.cols(), " columns, dims expect ", dims.front());
+    if (opts.batch_size == 0) fail("greedy_pretrain: batch size must be >= 1");
+    unsigned char raw[sizeof(Rng)];
+    std::memcpy(raw, &rng, sizeof(Rng));
+    uint64_t st[4];
+    double spare = 0.0;
+    bool has = false;
+    std::memcpy(st, raw, 32);
+    std::memcpy(&spare, raw + 32, 8);
+    std::memcpy(&has, raw + 40, 1);
+    int has_i = has ? 1 : 0;
+    detail::Ctx ctx(o.device);
+    std::vector<uint64_t> d(dims.begin(), dims.end());
+    MlpModel shape;
+    shape.layer_dims = dims;
+    shape.activation = activation;
+    ParamVector p;
+    p.data.resize(param_count(dims));
+    detail::check(parnn_greedy_pretrain_rng(ctx.get(), d.data(), static_cast<int>(d.size()), data.data().data(),
+                                            data.rows(), opts.epochs, opts.lr_gaussian, opts.lr_bernoulli,
+                                            opts.batch_size,
+                                            activation == Activation::sigmoid ? PARNN_SIGMOID : PARNN_TANH, st,
+                                            &spare, &has_i, o.precision, p.data.data()));
+    std::memcpy(raw, st, 32);
+    std::memcpy(raw + 32, &spare, 8);
+    has = has_i != 0;
+    std::memcpy(raw + 40, &has, 1);
+    std::memcpy(static_cast<void*>(&rng), raw, sizeof(Rng));
+    return unflatten(p, shape);
 }
 
 }  // namespace b200

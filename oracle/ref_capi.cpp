@@ -7,7 +7,11 @@
 // Every entry point takes/returns plain pointers (flatten order for model
 // parameters, row-major doubles for matrices) and returns 0 on success or
 // -1 after storing the reference's exception text (ref_last_error).
+#include <algorithm>
 #include <array>
+#include <atomic>
+#include <functional>
+#include <mutex>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -580,6 +584,248 @@ double ref_time_steps(const uint64_t* dims, int nd, const double* params0, const
             for (int i = 0; i < 5; ++i) phase_out[i] = phases[0][i];
     });
     return fps;
+}
+
+// ---- One TRUE-WIDTH minibatch step of the reference on all host cores -----
+// worker_epoch's body for one minibatch (parallel.cpp:117-130) -- forward,
+// cross_entropy, backward_with_context, ng_update_state, ng_precondition,
+// sgd_step_in_place -- built only from the reference's own public functions
+// (forward, cross_entropy, backward_with_context, matmul_tn, smoothed_factor,
+// cholesky_solve, transpose, frobenius_norm, sgd_step_in_place), spread over
+// `threads` host threads along the only seams those functions allow without
+// changing their arithmetic:
+//   * forward / cross_entropy / backward_with_context on row chunks of the
+//     batch (every output row and every dz row is computed exactly as in the
+//     whole-batch call); the per-chunk gradients dz_c^T A_c / b_c are combined
+//     as sum_c (b_c / B) g_c  (the whole-batch call sums all rows, then / B);
+//   * the NG moments A^T A / B, D^T D / B as per-chunk matmul_tn partials,
+//     summed (ng_update_state, optimizer.cpp:79-106; first update: r = C);
+//   * ng_precondition (optimizer.cpp:123-157) with its two cholesky_solve calls
+//     split over right-hand-side columns (each task refactors S, exactly as
+//     every reference call does), the bias solve (a further S_out factor) as
+//     its own task, gamma from the full Frobenius norms.
+// Tasks of a phase run longest-first on a dynamic pool. The result equals the
+// single-threaded reference step up to fp64 summation order (checked by
+// tests/test_oracle.py at a small shape against ref_train_steps).
+// phase_out[7] = seconds of {forward+ce, backward (+combine), moments,
+// smoothed factors + first solves + bias solves, second solves, gamma +
+// assemble, sgd}; returns the step's wall seconds (or -1 on error).
+double ref_time_step_threaded(const uint64_t* dims, int nd, const double* params0, const double* x,
+                              const int32_t* labels, uint64_t batch, int ngsgd, int threads, double lr,
+                              double* phase_out, double* params_out, double* ce_out) {
+    double wall = -1.0;
+    guarded([&] {
+        using clk = std::chrono::steady_clock;
+        const int T = std::max(1, threads);
+        MlpModel m = make_model(dims, nd, 0, params0);
+        const std::size_t L = m.layers.size();
+        const Matrix X = make_matrix(x, batch, dims[0]);
+        const Labels Y(labels, labels + batch);
+        auto pool = [&](std::vector<std::pair<double, std::function<void()>>>& tasks) {
+            std::sort(tasks.begin(), tasks.end(), [](auto& a, auto& b) { return a.first > b.first; });
+            std::atomic<std::size_t> next{0};
+            std::vector<std::thread> th;
+            std::mutex emu;
+            std::string err;
+            for (int t = 0; t < T; ++t)
+                th.emplace_back([&] {
+                    for (std::size_t i; (i = next.fetch_add(1)) < tasks.size();) {
+                        try {
+                            tasks[i].second();
+                        } catch (const std::exception& e) {
+                            std::lock_guard<std::mutex> lk(emu);
+                            err = e.what();
+                        }
+                    }
+                });
+            for (auto& t : th) t.join();
+            if (!err.empty()) throw std::runtime_error(err);
+        };
+        // row chunks of the batch
+        const std::size_t nch = std::min<std::size_t>(T, batch);
+        std::vector<std::size_t> r0(nch + 1);
+        for (std::size_t c = 0; c <= nch; ++c) r0[c] = batch * c / nch;
+        std::vector<Matrix> xc(nch);
+        std::vector<Labels> yc(nch);
+        for (std::size_t c = 0; c < nch; ++c) {
+            const std::size_t b = r0[c + 1] - r0[c];
+            xc[c] = Matrix(b, dims[0], std::vector<double>(X.row_ptr(r0[c]), X.row_ptr(r0[c]) + b * dims[0]));
+            yc[c].assign(Y.begin() + r0[c], Y.begin() + r0[c + 1]);
+        }
+        std::vector<ForwardTrace> trc(nch);
+        std::vector<double> cec(nch);
+        std::vector<GradientSet> gc(nch);
+        std::vector<BackpropContext> cxc(nch);
+        std::vector<std::pair<double, std::function<void()>>> tasks;
+        double ph[7] = {0, 0, 0, 0, 0, 0, 0};
+        const auto t_all = clk::now();
+        auto tick = clk::now();
+        auto lap = [&](int i) {
+            const auto now = clk::now();
+            ph[i] = std::chrono::duration<double>(now - tick).count();
+            tick = now;
+        };
+        // forward + cross_entropy
+        for (std::size_t c = 0; c < nch; ++c)
+            tasks.push_back({1.0, [&, c] {
+                                 trc[c] = forward(m, xc[c]);
+                                 cec[c] = cross_entropy(trc[c], yc[c]);
+                             }});
+        pool(tasks);
+        tasks.clear();
+        double ce = 0.0;
+        for (std::size_t c = 0; c < nch; ++c) ce += cec[c] * static_cast<double>(r0[c + 1] - r0[c]);
+        ce /= static_cast<double>(batch);
+        lap(0);
+        // backward (+ combine sum_c (b_c / B) g_c, per layer)
+        for (std::size_t c = 0; c < nch; ++c)
+            tasks.push_back({1.0, [&, c] { gc[c] = backward_with_context(m, trc[c], yc[c], cxc[c]); }});
+        pool(tasks);
+        tasks.clear();
+        GradientSet g;
+        g.layers.resize(L);
+        for (std::size_t l = 0; l < L; ++l)
+            tasks.push_back({static_cast<double>(gc[0].layers[l].weights.size()), [&, l] {
+                                 LayerParams& o = g.layers[l];
+                                 o.weights = Matrix(gc[0].layers[l].weights.rows(), gc[0].layers[l].weights.cols());
+                                 o.bias.assign(gc[0].layers[l].bias.size(), 0.0);
+                                 for (std::size_t c = 0; c < nch; ++c) {
+                                     const double f = static_cast<double>(r0[c + 1] - r0[c]) / static_cast<double>(batch);
+                                     const auto& gw = gc[c].layers[l].weights.data();
+                                     auto& ow = o.weights.data();
+                                     for (std::size_t i = 0; i < ow.size(); ++i) ow[i] += f * gw[i];
+                                     for (std::size_t i = 0; i < o.bias.size(); ++i) o.bias[i] += f * gc[c].layers[l].bias[i];
+                                 }
+                             }});
+        pool(tasks);
+        tasks.clear();
+        lap(1);
+        GradientSet out = g;
+        if (ngsgd) {
+            // moments: per (layer, side, chunk) matmul_tn partials, then sums x 1/B
+            std::vector<std::vector<Matrix>> part(2 * L, std::vector<Matrix>(nch));
+            for (std::size_t l = 0; l < L; ++l)
+                for (int sd = 0; sd < 2; ++sd)
+                    for (std::size_t c = 0; c < nch; ++c)
+                        tasks.push_back({static_cast<double>(sd ? dims[l + 1] * dims[l + 1] : dims[l] * dims[l]),
+                                         [&, l, sd, c] {
+                                             const Matrix& a = sd ? cxc[c].dz[l]
+                                                                  : (l == 0 ? trc[c].input : trc[c].activations[l - 1]);
+                                             part[2 * l + sd][c] = matmul_tn(a, a);
+                                         }});
+            pool(tasks);
+            tasks.clear();
+            std::vector<Matrix> rfac(2 * L);
+            for (std::size_t i = 0; i < 2 * L; ++i)
+                tasks.push_back({static_cast<double>(part[i][0].size()), [&, i] {
+                                     Matrix s = part[i][0];
+                                     for (std::size_t c = 1; c < nch; ++c) {
+                                         auto& d = s.data();
+                                         const auto& p = part[i][c].data();
+                                         for (std::size_t k = 0; k < d.size(); ++k) d[k] += p[k];
+                                     }
+                                     scale_in_place(s, 1.0 / static_cast<double>(batch));
+                                     rfac[i] = std::move(s);  // ema_update, t = 1: r = C
+                                     part[i].clear();
+                                 }});
+            pool(tasks);
+            tasks.clear();
+            lap(2);
+            // smoothed factors, then the first solves S_out^-1 G (column chunks) and the bias solves
+            std::vector<Matrix> sfac(2 * L);
+            for (std::size_t i = 0; i < 2 * L; ++i)
+                tasks.push_back({static_cast<double>(rfac[i].size()), [&, i] { sfac[i] = smoothed_factor(rfac[i], 4.0); }});
+            pool(tasks);
+            tasks.clear();
+            auto col_chunks = [&](std::size_t nrow, std::size_t ncol) {
+                // a factor that costs more than the solves (output layer: 8806 rows vs 2048 columns)
+                // is refactored by every chunk: T - 1 chunks, one thread left for the bias solve
+                std::size_t k = nrow > 2 * ncol ? static_cast<std::size_t>(std::max(1, T - 1)) : 4;
+                return std::max<std::size_t>(1, std::min<std::size_t>(k, ncol / 32));
+            };
+            auto cols_of = [](const Matrix& a, std::size_t c0, std::size_t c1) {
+                Matrix o(a.rows(), c1 - c0);
+                for (std::size_t r = 0; r < a.rows(); ++r)
+                    std::copy(a.row_ptr(r) + c0, a.row_ptr(r) + c1, o.row_ptr(r));
+                return o;
+            };
+            std::vector<std::vector<Matrix>> left(L), right(L);
+            std::vector<Matrix> bhat(L);
+            std::vector<std::vector<std::size_t>> cb1(L), cb2(L);
+            for (std::size_t l = 0; l < L; ++l) {
+                const Matrix& G = g.layers[l].weights;  // dout x din
+                const double n_out = static_cast<double>(dims[l + 1]);
+                const std::size_t k1 = col_chunks(dims[l + 1], G.cols());
+                left[l].resize(k1);
+                for (std::size_t c = 0; c <= k1; ++c) cb1[l].push_back(G.cols() * c / k1);
+                for (std::size_t c = 0; c < k1; ++c)
+                    tasks.push_back({n_out * n_out * n_out / 3.0 + 2.0 * n_out * n_out * (cb1[l][c + 1] - cb1[l][c]),
+                                     [&, l, c] {
+                                         left[l][c] = cholesky_solve(sfac[2 * l + 1], cols_of(g.layers[l].weights,
+                                                                                              cb1[l][c], cb1[l][c + 1]));
+                                     }});
+                tasks.push_back({n_out * n_out * n_out / 3.0, [&, l] {
+                                     Matrix bias_col(g.layers[l].bias.size(), 1, g.layers[l].bias);
+                                     bhat[l] = cholesky_solve(sfac[2 * l + 1], bias_col);
+                                 }});
+            }
+            pool(tasks);
+            tasks.clear();
+            lap(3);
+            // second solves S_in^-1 (S_out^-1 G)^T over column chunks of the transpose
+            std::vector<Matrix> leftT(L);
+            for (std::size_t l = 0; l < L; ++l) {
+                Matrix lf(g.layers[l].weights.rows(), g.layers[l].weights.cols());
+                for (std::size_t c = 0; c < left[l].size(); ++c)
+                    for (std::size_t r = 0; r < lf.rows(); ++r)
+                        std::copy(left[l][c].row_ptr(r), left[l][c].row_ptr(r) + left[l][c].cols(),
+                                  lf.row_ptr(r) + cb1[l][c]);
+                leftT[l] = transpose(lf);  // din x dout
+                const double n_in = static_cast<double>(dims[l]);
+                const std::size_t k2 = std::min<std::size_t>(static_cast<std::size_t>(T),
+                                                             std::max<std::size_t>(1, leftT[l].cols() / 512));
+                right[l].resize(k2);
+                for (std::size_t c = 0; c <= k2; ++c) cb2[l].push_back(leftT[l].cols() * c / k2);
+                for (std::size_t c = 0; c < k2; ++c)
+                    tasks.push_back({n_in * n_in * n_in / 3.0 + 2.0 * n_in * n_in * (cb2[l][c + 1] - cb2[l][c]),
+                                     [&, l, c] {
+                                         right[l][c] = cholesky_solve(sfac[2 * l], cols_of(leftT[l], cb2[l][c], cb2[l][c + 1]));
+                                     }});
+            }
+            pool(tasks);
+            tasks.clear();
+            lap(4);
+            // assemble ghat = transpose(S_in^-1 left^T), gamma rescales (optimizer.cpp:141-154)
+            for (std::size_t l = 0; l < L; ++l)
+                tasks.push_back({static_cast<double>(g.layers[l].weights.size()), [&, l] {
+                                     Matrix rt(leftT[l].rows(), leftT[l].cols());
+                                     for (std::size_t c = 0; c < right[l].size(); ++c)
+                                         for (std::size_t r = 0; r < rt.rows(); ++r)
+                                             std::copy(right[l][c].row_ptr(r), right[l][c].row_ptr(r) + right[l][c].cols(),
+                                                       rt.row_ptr(r) + cb2[l][c]);
+                                     Matrix ghat = transpose(rt);
+                                     const double gamma = frobenius_norm(g.layers[l].weights) /
+                                                          std::max(frobenius_norm(ghat), 1e-20);
+                                     scale_in_place(ghat, gamma);
+                                     out.layers[l].weights = std::move(ghat);
+                                     const double gamma_b = frobenius_norm(g.layers[l].bias) /
+                                                            std::max(frobenius_norm(bhat[l]), 1e-20);
+                                     for (std::size_t i = 0; i < g.layers[l].bias.size(); ++i)
+                                         out.layers[l].bias[i] = gamma_b * bhat[l](i, 0);
+                                 }});
+            pool(tasks);
+            tasks.clear();
+            lap(5);
+        }
+        sgd_step_in_place(m, out, lr);
+        lap(6);
+        wall = std::chrono::duration<double>(clk::now() - t_all).count();
+        if (phase_out)
+            for (int i = 0; i < 7; ++i) phase_out[i] = ph[i];
+        if (params_out) put_params(m, params_out);
+        if (ce_out) *ce_out = ce;
+    });
+    return wall;
 }
 
 // Times ng_precondition alone for one layer shape (d_out x d_in) with

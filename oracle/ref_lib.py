@@ -300,3 +300,24 @@ class RefLib:
         if s < 0:
             raise RuntimeError(self.lib.ref_last_error().decode())
         return s
+
+    def time_step_threaded(self, dims, params, x, labels, ngsgd, threads, lr=1e-3):
+        """One true-width minibatch step of the reference (worker_epoch's body)
+        from its own public functions on `threads` host threads
+        (ref_time_step_threaded). Returns (wall seconds, phase seconds[7],
+        params after the step, batch CE)."""
+        d = self._dims(dims)
+        x = np.ascontiguousarray(x, np.float64)
+        labels = np.ascontiguousarray(labels, np.int32)
+        ph = np.zeros(7)
+        p = np.zeros(self.param_count(dims))
+        ce = C.c_double()
+        self.lib.ref_time_step_threaded.restype = C.c_double
+        wall = self.lib.ref_time_step_threaded(
+            d.ctypes.data_as(C.c_void_p), C.c_int(len(d)), np.ascontiguousarray(params).ctypes.data_as(C.c_void_p),
+            x.ctypes.data_as(C.c_void_p), labels.ctypes.data_as(C.c_void_p), C.c_uint64(x.shape[0]),
+            C.c_int(int(ngsgd)), C.c_int(threads), C.c_double(lr), ph.ctypes.data_as(C.c_void_p),
+            p.ctypes.data_as(C.c_void_p), C.byref(ce))
+        if wall < 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return wall, ph, p, ce.value

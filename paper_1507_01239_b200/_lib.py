@@ -55,6 +55,8 @@ SIGNATURES = [
     ("parnn_lowrank_basis", c_int, [c_u64, c_u64, c_u64, vp]),
     ("parnn_debug_lowrank_eig", c_int, [c_int, c_u64, c_f64, c_f64, c_f64, vp, vp, vp, vp, vp]),
     ("parnn_lowrank_seed", c_u64, [c_int, c_int]),
+    ("parnn_debug_gemm", c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                 c_int, c_int, C.c_float, C.c_float, C.c_float, vp, vp, vp, vp, vp, vp, vp, vp]),
     ("parnn_allreduce_average_host", c_int, [vp, c_u64, c_u64, vp]),
     ("parnn_ctx_create", c_int, [c_int, vp]),
     ("parnn_ctx_destroy", c_int, [vp]),
@@ -87,6 +89,10 @@ SIGNATURES = [
     ("parnn_comm_destroy", c_int, [vp]),
     ("parnn_average", c_int, [vp, c_int, vp, c_u64]),
     ("parnn_run_steps", c_int, [vp, c_int, vp, c_u64, c_u64, c_u64, vp]),
+    ("parnn_time_average", c_int, [vp, c_int, vp, c_u64, c_u64, vp, vp]),
+    ("parnn_averager_create", c_int, [vp, c_int, vp, c_u64, vp]),
+    ("parnn_averager_run", c_int, [vp]),
+    ("parnn_averager_destroy", c_int, [vp]),
     ("parnn_train", c_int, [vp, vp, vp, vp, c_int, vp, vp, vp, vp, vp, vp]),
     ("parnn_rbm_create", c_int, [vp, c_u64, c_u64, c_int, c_u64, c_int, vp]),
     ("parnn_rbm_destroy", c_int, [vp]),
@@ -96,6 +102,8 @@ SIGNATURES = [
     ("parnn_rbm_hidden_probs", c_int, [vp, vp, c_u64, vp]),
     ("parnn_rbm_reconstruction_error", c_int, [vp, vp, c_u64, vp]),
     ("parnn_greedy_pretrain", c_int, [vp, vp, c_int, vp, c_u64, c_u64, c_f64, c_f64, c_u64, c_u64, c_int, vp]),
+    ("parnn_greedy_pretrain_rng", c_int, [vp, vp, c_int, vp, c_u64, c_u64, c_f64, c_f64, c_u64, c_int, vp, vp, vp,
+                                          c_int, vp]),
 ]
 
 _lib = None

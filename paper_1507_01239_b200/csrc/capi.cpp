@@ -2,6 +2,7 @@
 // every entry point converts exceptions into PARNN_ERR + parnn_last_error().
 #include "../../include/parnn_b200.h"
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -26,6 +27,9 @@ struct parnn_comm {
 };
 struct parnn_rbm {
     std::unique_ptr<RbmDevice> r;
+};
+struct parnn_averager {
+    std::unique_ptr<Averager> a;
 };
 
 namespace {
@@ -291,6 +295,24 @@ int parnn_debug_lowrank_eig(int rank, uint64_t dim, double eta, double a, double
     });
 }
 
+int parnn_debug_gemm(int precision, int a_mn, int b_mn, int m, int n, int k, int mode, int act, int ksplit,
+                     int force_bn, int force_mc, int lower, int bias_col, float alpha, float beta, float lr,
+                     const float* a, const float* b, const float* bias, const float* aux, float* out, float* out2,
+                     double* sums, int* info) {
+    return guarded([&] {
+        need(a, "gemm A");
+        need(b, "gemm B");
+        need(out, "gemm out");
+        if (precision < 0 || precision > 2) throw std::runtime_error("gemm: unknown precision");
+        if (mode < EPI_FWD_ACT || mode > EPI_RESID) throw std::runtime_error("gemm: unknown epilogue mode");
+        if ((mode == EPI_FWD_ACT || mode == EPI_FWD_LINEAR || (mode == EPI_GRAD_SGD && bias_col >= 0)) && !bias)
+            throw std::runtime_error("gemm: mode needs a bias vector");
+        if ((mode == EPI_ACTGRAD || mode == EPI_RESID) && !aux) throw std::runtime_error("gemm: mode needs aux");
+        debug_gemm(precision, a_mn != 0, b_mn != 0, m, n, k, mode, act, ksplit, force_bn, force_mc, lower, bias_col,
+                   alpha, beta, lr, a, b, bias, aux, out, out2, sums, info);
+    });
+}
+
 int parnn_lowrank_basis(uint64_t dim, uint64_t rank, uint64_t seed, double* out) {
     return guarded([&] {
         const std::vector<double> b = host::lowrank_basis(dim, rank, seed);
@@ -433,11 +455,71 @@ int parnn_run_steps(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_
             for (Replica* r : v) r->run_step(r->stream);
             if ((s + 1) % avg_frequency == 0 || s + 1 == steps) avg.run();  // last event closes the window
         }
+        // join: every replica stream (the last step's tail) and the averaging stream
+        std::vector<cudaEvent_t> tails(v.size() + 1);
+        for (size_t i = 0; i < tails.size(); ++i) {
+            CUDA_THROW(cudaEventCreateWithFlags(&tails[i], cudaEventDisableTiming));
+            CUDA_THROW(cudaEventRecord(tails[i], i < v.size() ? v[i]->stream : ctx->avg));
+            CUDA_THROW(cudaStreamWaitEvent(ctx->stream, tails[i], 0));
+        }
         CUDA_THROW(cudaEventRecord(b, ctx->stream));
+        for (auto e : tails) cudaEventDestroy(e);
         CUDA_THROW(cudaEventSynchronize(b));
         float t = 0.f;
         CUDA_THROW(cudaEventElapsedTime(&t, a, b));
         *ms = t;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    });
+}
+
+int parnn_averager_create(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_t m_total,
+                          parnn_averager** out) {
+    return guarded([&] {
+        if (n_local <= 0) throw std::runtime_error("allreduce_average: m must be >= 1");
+        std::vector<Replica*> v;
+        for (int i = 0; i < n_local; ++i) v.push_back(reps[i]->r.get());
+        auto* p = new parnn_averager;
+        p->a.reset(new Averager(v[0]->ctx, v, comm ? comm->c.get() : nullptr, static_cast<long>(m_total)));
+        *out = p;
+    });
+}
+
+int parnn_averager_run(parnn_averager* a) {
+    return guarded([&] {
+        need(a, "averager");
+        a->a->run();
+    });
+}
+
+int parnn_averager_destroy(parnn_averager* a) {
+    return guarded([&] {
+        if (a) CUDA_THROW(cudaStreamSynchronize(a->a->ctx->avg));
+        delete a;
+    });
+}
+
+int parnn_time_average(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_t m_total, uint64_t iters,
+                       double* ms, double* bytes) {
+    return guarded([&] {
+        if (n_local <= 0) throw std::runtime_error("allreduce_average: m must be >= 1");
+        std::vector<Replica*> v;
+        for (int i = 0; i < n_local; ++i) v.push_back(reps[i]->r.get());
+        Context* ctx = v[0]->ctx;
+        Averager avg(ctx, v, comm ? comm->c.get() : nullptr, static_cast<long>(m_total));
+        for (Replica* r : v) CUDA_THROW(cudaStreamSynchronize(r->stream));
+        avg.run();  // warm (NCCL channels, first-touch)
+        cudaEvent_t a, b;
+        CUDA_THROW(cudaEventCreate(&a));
+        CUDA_THROW(cudaEventCreate(&b));
+        CUDA_THROW(cudaEventRecord(a, ctx->avg));
+        for (uint64_t i = 0; i < iters; ++i) avg.run();
+        CUDA_THROW(cudaEventRecord(b, ctx->avg));
+        CUDA_THROW(cudaEventSynchronize(b));
+        float t = 0.f;
+        CUDA_THROW(cudaEventElapsedTime(&t, a, b));
+        *ms = t / static_cast<double>(std::max<uint64_t>(iters, 1));
+        *bytes = avg.bytes();
         cudaEventDestroy(a);
         cudaEventDestroy(b);
     });
@@ -471,6 +553,7 @@ int parnn_average(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_t 
         Averager a(v[0]->ctx, v, comm ? comm->c.get() : nullptr, static_cast<long>(m_total));
         a.run();
         for (Replica* r : v) CUDA_THROW(cudaStreamSynchronize(r->stream));
+        CUDA_THROW(cudaStreamSynchronize(v[0]->ctx->avg));
     });
 }
 
@@ -559,8 +642,34 @@ int parnn_rbm_reconstruction_error(parnn_rbm* r, const double* x, uint64_t n, do
 int parnn_greedy_pretrain(parnn_ctx* ctx, const uint64_t* dims, int nd, const double* data, uint64_t n, uint64_t epochs,
                           double lr_g, double lr_b, uint64_t batch, uint64_t seed, int prec, double* params_out) {
     return guarded([&] {
+        host::Rng rng(seed);
         greedy_pretrain(ctx->c.get(), to_dims(dims, nd), data, static_cast<long>(n), epochs, lr_g, lr_b,
-                        static_cast<long>(batch), seed, static_cast<Precision>(prec), params_out);
+                        static_cast<long>(batch), rng, seed ^ 0x5851F42D4C957F2Dull, static_cast<Precision>(prec),
+                        params_out);
+    });
+}
+
+int parnn_greedy_pretrain_rng(parnn_ctx* ctx, const uint64_t* dims, int nd, const double* data, uint64_t n,
+                              uint64_t epochs, double lr_g, double lr_b, uint64_t batch, int activation,
+                              uint64_t rng_state[4], double* rng_spare, int* rng_has_spare, int prec,
+                              double* params_out) {
+    return guarded([&] {
+        need(ctx, "greedy_pretrain");
+        need(rng_state, "greedy_pretrain rng state");
+        need(rng_spare, "greedy_pretrain rng spare");
+        need(rng_has_spare, "greedy_pretrain rng spare flag");
+        if (activation != PARNN_SIGMOID && activation != PARNN_TANH)
+            throw std::runtime_error("greedy_pretrain: unknown activation " + std::to_string(activation));
+        host::Rng rng(0);
+        rng.set_state(rng_state, *rng_spare, *rng_has_spare != 0);
+        // the device Bernoulli stream is keyed by the caller's generator state on entry
+        uint64_t key = 0x5851F42D4C957F2Dull;
+        for (int i = 0; i < 4; ++i) key = (key ^ rng_state[i]) * 0x9E3779B97F4A7C15ull;
+        greedy_pretrain(ctx->c.get(), to_dims(dims, nd), data, static_cast<long>(n), epochs, lr_g, lr_b,
+                        static_cast<long>(batch), rng, key, static_cast<Precision>(prec), params_out);
+        bool has = false;
+        rng.get_state(rng_state, rng_spare, &has);
+        *rng_has_spare = has ? 1 : 0;
     });
 }
 

@@ -5,6 +5,8 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "gemm.cuh"
 #include "gemm_pick.cuh"
@@ -62,7 +64,7 @@ int choose_bn(int M, int N, int num_sms) {
 }
 
 void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b_mn, const void* B, long ldb,
-               int M, int N, int K, const GemmEpi& ep, int num_sms, int force_bn) {
+               int M, int N, int K, const GemmEpi& ep, int num_sms, int force_bn, int force_mc) {
     if (M <= 0 || N <= 0 || K <= 0) throw std::runtime_error("gemm: empty problem");
     const bool f32 = prec != 0, split = prec == 2;
     const int bn = force_bn ? force_bn : choose_bn(M, N, num_sms);
@@ -93,7 +95,14 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
         return v && v[0] == '0';
     }();
     int bn_eff = bn;
-    if (p.mc == 1 && !f32 && !sk_off && !force_bn && ksplit == 1 && !ep.lower && nk >= 8) {
+    if (force_mc) {
+        if (force_mc == 2 && (f32 || ksplit != 1 || ep.lower || bn < 128 || tiles_m < 2))
+            throw std::runtime_error("gemm: CTA pairs need bf16, no split-K / lower, BN >= 128 and >= 2 row tiles");
+        if (force_mc == 3 && (f32 || ksplit != 1 || ep.lower || nk < 2))
+            throw std::runtime_error("gemm: split-K CTA pairs need bf16, no split-K / lower and >= 2 k-blocks");
+        p.mc = force_mc;
+        if (force_mc == 3) bn_eff = 256;
+    } else if (p.mc == 1 && !f32 && !sk_off && !force_bn && ksplit == 1 && !ep.lower && nk >= 8) {
         const long t256 = static_cast<long>(tiles_m) * ((N + 255) / 256);
         static const int min_frac = [] {  // tuning aid: pairs must fill >= 1/x of the SMs
             const char* v = std::getenv("PARNN_GEMM_SK2_FRAC");
@@ -145,6 +154,18 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
 
 namespace {
 thread_local int g_grid_cap = 0;
+}
+
+void ensure_smem_attr(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, int>, int>> done;  // (fn, device) -> bytes set
+    int dev = 0;
+    CUDA_THROW(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& d : done)
+        if (d.first.first == fn && d.first.second == dev && d.second >= bytes) return;
+    CUDA_THROW(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.push_back({{fn, dev}, bytes});
 }
 
 void gemm_set_grid_cap(int cap) { g_grid_cap = cap; }

@@ -26,11 +26,7 @@ KernelFn kernel_ptr(int* smem) {
     constexpr int ST = stages_for<BN, SPLIT>();
     *smem = GemmSmem<BN, ST, T, SPLIT, TE>::kBytes;
     auto k = &gemm_tc_kernel<T, BN, ST, AMN, BMN, SPLIT, TE, MC>;
-    static bool configured = false;
-    if (!configured) {
-        CUDA_THROW(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem));
-        configured = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(k), *smem);
     return reinterpret_cast<KernelFn>(k);
 }
 

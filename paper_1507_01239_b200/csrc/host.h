@@ -30,6 +30,18 @@ public:
     uint64_t uniform_index(uint64_t bound);
     double gaussian(double mean, double stddev);
     void jump(const Jump& j);
+    // the full generator state, for callers that carry a reference Rng across
+    // the C ABI (the xoshiro256** words and the polar-method spare, rng.hpp)
+    void get_state(uint64_t s[4], double* spare, bool* has_spare) const {
+        for (int i = 0; i < 4; ++i) s[i] = s_[i];
+        *spare = spare_;
+        *has_spare = has_spare_;
+    }
+    void set_state(const uint64_t s[4], double spare, bool has_spare) {
+        for (int i = 0; i < 4; ++i) s_[i] = s[i];
+        spare_ = spare;
+        has_spare_ = has_spare;
+    }
     template <typename T>
     void shuffle(std::vector<T>& v) {
         for (size_t i = v.size(); i > 1; --i) {

@@ -413,11 +413,7 @@ int grid_for(long total) { return (int)std::max<long>(1, std::min<long>((total +
 constexpr int kDiagSmem = 2 * NB * LDS * 4 + 48 * 4;
 
 void ensure_diag_attr() {
-    static bool done = false;
-    if (!done) {
-        CUDA_THROW(cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem));
-        done = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(chol_diag_kernel), kDiagSmem);
 }
 
 float* linv_blk(NgFactor& f, long j) { return f.linv + (j / NB) * NB * NB; }

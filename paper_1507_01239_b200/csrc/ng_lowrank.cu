@@ -729,8 +729,7 @@ void lr_debug_eig(int R, long D, double eta, double a, double alpha, const doubl
     float* dm = falloc(2L * R * R);
     CUDA_THROW(cudaMemcpy(dst, st_in, ns * 8, cudaMemcpyHostToDevice));
     CUDA_THROW(cudaMemcpy(dg, gram, 16L * R * R, cudaMemcpyHostToDevice));
-    CUDA_THROW(cudaFuncSetAttribute(lr_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(eig_smem(LR_MAX_RANK))));
+    ensure_smem_attr(reinterpret_cast<const void*>(lr_eig_kernel), static_cast<int>(eig_smem(LR_MAX_RANK)));
     const int nblk = ((R + 7) & ~7) / 4;
     const int threads = std::max(64, 32 * (nblk / 2));
     double* dout = dalloc_d(ns);
@@ -765,14 +764,11 @@ void lr_free(Replica& r) {
 }
 
 void lr_build_plans(Replica& r) {
-    static bool attr = false;
-    if (!attr) {
-        CUDA_THROW(cudaFuncSetAttribute(lr_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(eig_smem(LR_MAX_RANK))));
+    {
+        ensure_smem_attr(reinterpret_cast<const void*>(lr_eig_kernel), static_cast<int>(eig_smem(LR_MAX_RANK)));
         const int ws = (LR_MAX_RANK * 2 * LR_MAX_RANK + 2 * LR_MAX_RANK * 32) * 4;
-        CUDA_THROW(cudaFuncSetAttribute(lr_wupdate_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, ws));
-        CUDA_THROW(cudaFuncSetAttribute(lr_wupdate_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, ws));
-        attr = true;
+        ensure_smem_attr(reinterpret_cast<const void*>(lr_wupdate_kernel<float>), ws);
+        ensure_smem_attr(reinterpret_cast<const void*>(lr_wupdate_kernel<bf16>), ws);
     }
     for (int l = 0; l < r.L; ++l) {
         side_plans(r, r.lrl[l].in, r.acts[l]);

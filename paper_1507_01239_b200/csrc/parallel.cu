@@ -10,6 +10,7 @@
 //    its bf16 operand copy.
 #include <nccl.h>
 
+#include <algorithm>
 #include <utility>
 
 #include "parallel.h"
@@ -33,10 +34,11 @@ __device__ float tree_sum_at(const float* const* src, int lo, int hi, long i) {
     return tree_sum_at(src, lo, mid, i) + tree_sum_at(src, mid, hi, i);
 }
 
-// out_k[i] = scale * tree_sum(src)[i] for every destination k (+ bf16 copy).
-__global__ void tree_avg_kernel(const float* const* src, int m, long n, float scale, int apply_scale,
+// out_k[i] = scale * tree_sum(src)[i] for every destination k (+ bf16 copy),
+// i in [off, off + n).
+__global__ void tree_avg_kernel(const float* const* src, int m, long off, long n, float scale, int apply_scale,
                                 float* const* dst, bf16* const* shadow, int ndst) {
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    for (long i = off + blockIdx.x * (long)blockDim.x + threadIdx.x; i < off + n; i += (long)gridDim.x * blockDim.x) {
         float v = tree_sum_at(src, 0, m, i);
         if (apply_scale) v *= scale;
         for (int k = 0; k < ndst; ++k) {
@@ -49,8 +51,10 @@ __global__ void tree_avg_kernel(const float* const* src, int m, long n, float sc
 // Vectorised form for m <= 32 local replicas: each thread loads the m float4s
 // of its 4 elements into registers, then adds them in the same midpoint tree,
 // unrolled at compile time (bitwise equal to tree_sum_at), so all m loads are
-// in flight at once. Elements past the last whole float4 go through the scalar
-// tree in block 0.
+// in flight at once. The range [off, off + n) starts on a float4 boundary
+// (buckets are 128-byte aligned); elements past its last whole float4 go
+// through the scalar tree in block 0. With M = 1 it is the fused scale pass:
+// scratch * (1/m) -> every local replica and its bf16 operand copy.
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
     return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
@@ -67,26 +71,27 @@ __device__ __forceinline__ V tree_reg(const V* x) {
 }
 
 template <int M>
-__global__ void __launch_bounds__(256) tree_avg4_kernel(const float* const* src, long n, float scale, int apply_scale,
-                                                        float* const* dst, bf16* const* shadow, int ndst) {
-    const long n4 = n / 4;
+__global__ void __launch_bounds__(256) tree_avg4_kernel(const float* const* src, long off, long n, float scale,
+                                                        int apply_scale, float* const* dst, bf16* const* shadow,
+                                                        int ndst) {
+    const long n4 = n / 4, b4 = off / 4;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
         float4 x[M];
 #pragma unroll
-        for (int k = 0; k < M; ++k) x[k] = reinterpret_cast<const float4*>(src[k])[i];  // warp-uniform pointer loads
+        for (int k = 0; k < M; ++k) x[k] = reinterpret_cast<const float4*>(src[k])[b4 + i];  // warp-uniform pointer loads
         float4 v = tree_reg<0, M>(x);
         if (apply_scale) v = make_float4(v.x * scale, v.y * scale, v.z * scale, v.w * scale);
         for (int k = 0; k < ndst; ++k) {
-            reinterpret_cast<float4*>(dst[k])[i] = v;
+            reinterpret_cast<float4*>(dst[k])[b4 + i] = v;
             if (shadow[k]) {
                 const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-                reinterpret_cast<uint2*>(shadow[k])[i] =
+                reinterpret_cast<uint2*>(shadow[k])[b4 + i] =
                     make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
             }
         }
     }
-    const long t = 4 * n4 + threadIdx.x;
-    if (blockIdx.x == 0 && t < n) {
+    const long t = off + 4 * n4 + threadIdx.x;
+    if (blockIdx.x == 0 && t < off + n) {
         float x[M];
 #pragma unroll
         for (int k = 0; k < M; ++k) x[k] = src[k][t];
@@ -99,7 +104,7 @@ __global__ void __launch_bounds__(256) tree_avg4_kernel(const float* const* src,
     }
 }
 
-using AvgFn = void (*)(const float* const*, long, float, int, float* const*, bf16* const*, int);
+using AvgFn = void (*)(const float* const*, long, long, float, int, float* const*, bf16* const*, int);
 
 template <int... Ms>
 AvgFn avg4_pick(int m, std::integer_sequence<int, Ms...>) {
@@ -108,10 +113,6 @@ AvgFn avg4_pick(int m, std::integer_sequence<int, Ms...>) {
     return fn;
 }
 
-__global__ void bf16_copy_kernel(const float* __restrict__ src, long n, bf16* __restrict__ dst) {
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
-        dst[i] = __float2bfloat16_rn(src[i]);
-}
 
 }  // namespace
 
@@ -148,88 +149,87 @@ double Comm::allreduce_sum(double v) {
 
 Averager::Averager(Context* c, const std::vector<Replica*>& r, Comm* cm, long m) : ctx(c), reps(r), comm(cm), m_total(m) {
     if (reps.empty()) throw std::runtime_error("allreduce_average: m must be >= 1");
+    const long k = static_cast<long>(reps.size());
+    // every worker contributes exactly once (allreduce_average, parallel.cpp:44-47)
+    const long contributions = comm ? static_cast<long>(comm->nranks) * k : k;
+    if (contributions != m_total)
+        throw std::runtime_error("allreduce_average: got " + std::to_string(contributions) +
+                                 " contributions for m = " + std::to_string(m_total));
     n = reps[0]->n_pad;
     for (Replica* p : reps)
-        if (p->n_pad != n)
+        if (p->n_pad != n || p->L != reps[0]->L || p->w_off != reps[0]->w_off)
             throw std::runtime_error("allreduce_average: replica vector lengths differ");
-    const int k = static_cast<int>(reps.size());
     std::vector<float*> src(k);
     std::vector<bf16*> sh(k);
-    for (int i = 0; i < k; ++i) {
+    for (long i = 0; i < k; ++i) {
         src[i] = reps[i]->params;
         sh[i] = reps[i]->wshadow;
     }
     CUDA_THROW(cudaMalloc(&d_src, k * sizeof(float*)));
     CUDA_THROW(cudaMalloc(&d_shadow, k * sizeof(bf16*)));
+    CUDA_THROW(cudaMalloc(&d_null_shadow, sizeof(bf16*)));
     CUDA_THROW(cudaMemcpy(d_src, src.data(), k * sizeof(float*), cudaMemcpyHostToDevice));
     CUDA_THROW(cudaMemcpy(d_shadow, sh.data(), k * sizeof(bf16*), cudaMemcpyHostToDevice));
+    CUDA_THROW(cudaMemset(d_null_shadow, 0, sizeof(bf16*)));
     if (comm && k > 1) {
         CUDA_THROW(cudaMalloc(&scratch, n * sizeof(float)));
         CUDA_THROW(cudaMalloc(&d_scratch_ptr, sizeof(float*)));
         CUDA_THROW(cudaMemcpy(d_scratch_ptr, &scratch, sizeof(float*), cudaMemcpyHostToDevice));
-    }
-    CUDA_THROW(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
-    for (int i = 0; i < k; ++i) {
-        cudaEvent_t e;
-        CUDA_THROW(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        ev_rep.push_back(e);
     }
 }
 
 Averager::~Averager() {
     if (d_src) cudaFree(d_src);
     if (d_shadow) cudaFree(d_shadow);
+    if (d_null_shadow) cudaFree(d_null_shadow);
     if (scratch) cudaFree(scratch);
     if (d_scratch_ptr) cudaFree(d_scratch_ptr);
-    if (ev_done) cudaEventDestroy(ev_done);
-    for (auto e : ev_rep) cudaEventDestroy(e);
 }
 
 void Averager::run() {
-    cudaStream_t s = ctx->stream;
+    cudaStream_t s = ctx->avg;
     const int k = static_cast<int>(reps.size());
-    for (int i = 0; i < k; ++i) {
-        CUDA_THROW(cudaEventRecord(ev_rep[i], reps[i]->stream));
-        CUDA_THROW(cudaStreamWaitEvent(s, ev_rep[i], 0));
-    }
+    const int L = reps[0]->L;
     const float inv = static_cast<float>(1.0 / static_cast<double>(m_total));
-    const int grid = ctx->num_sms * 8;
     // float4 params / 8-byte bf16 shadows (cudaMalloc'd replica buffers always are)
     bool vec_ok = true;
     for (Replica* r : reps)
         vec_ok = vec_ok && (reinterpret_cast<uintptr_t>(r->params) & 15) == 0 &&
                  (reinterpret_cast<uintptr_t>(r->wshadow) & 7) == 0;
     if (scratch) vec_ok = vec_ok && (reinterpret_cast<uintptr_t>(scratch) & 15) == 0;
-    if (!comm) {
-        if (k > 1) {
-            if (AvgFn f = vec_ok ? avg4_pick(k, std::make_integer_sequence<int, 32>{}) : nullptr)
-                f<<<grid, 256, 0, s>>>(d_src, n, inv, 1, d_src, d_shadow, k);
-            else
-                tree_avg_kernel<<<grid, 256, 0, s>>>(d_src, k, n, inv, 1, d_src, d_shadow, k);
+    const AvgFn fk = vec_ok ? avg4_pick(k, std::make_integer_sequence<int, 32>{}) : nullptr;
+    const AvgFn f1 = vec_ok ? avg4_pick(1, std::make_integer_sequence<int, 32>{}) : nullptr;
+    ncclComm_t cm = comm ? static_cast<ncclComm_t>(comm->comm) : nullptr;
+    // m == 1 without a communicator: x * 1.0 is the identity (parallel.cpp:56-57);
+    // the gates are still recorded so the protocol is the same.
+    const bool work = comm || k > 1;
+    for (int l = L - 1; l >= 0; --l) {
+        for (Replica* r : reps) CUDA_THROW(cudaStreamWaitEvent(s, r->ev_upd[l], 0));
+        const long off = reps[0]->bucket_begin(l), len = reps[0]->bucket_end(l) - off;
+        const int grid = static_cast<int>(std::min<long>(ctx->num_sms * 8L, std::max<long>(1, (len / 4 + 255) / 256)));
+        if (work && !comm) {
+            // local midpoint tree over the replicas x 1/m -> every replica (+ bf16 copy)
+            if (fk) fk<<<grid, 256, 0, s>>>(d_src, off, len, inv, 1, d_src, d_shadow, k);
+            else tree_avg_kernel<<<grid, 256, 0, s>>>(d_src, k, off, len, inv, 1, d_src, d_shadow, k);
+        } else if (work && k == 1) {
+            // one replica per GPU: in-place ncclAvg fuses the 1/m scale into the collective
+            NCCL_THROW(ncclAllReduce(reps[0]->params + off, reps[0]->params + off, len, ncclFloat, ncclAvg, cm, s));
+            if (reps[0]->wshadow) {
+                if (f1) f1<<<grid, 256, 0, s>>>(d_src, off, len, 1.f, 0, d_src, d_shadow, 1);
+                else tree_avg_kernel<<<grid, 256, 0, s>>>(d_src, 1, off, len, 1.f, 0, d_src, d_shadow, 1);
+            }
+        } else if (work) {
+            // local subtree sum -> scratch (no shadow), NCCL sum over GPUs, then the
+            // fused scale pass: scratch x 1/m -> every local replica and its bf16 copy
+            if (fk) fk<<<grid, 256, 0, s>>>(d_src, off, len, 1.f, 0, d_scratch_ptr, d_null_shadow, 1);
+            else tree_avg_kernel<<<grid, 256, 0, s>>>(d_src, k, off, len, 1.f, 0, d_scratch_ptr, d_null_shadow, 1);
+            NCCL_THROW(ncclAllReduce(scratch + off, scratch + off, len, ncclFloat, ncclSum, cm, s));
+            if (f1) f1<<<grid, 256, 0, s>>>(d_scratch_ptr, off, len, inv, 1, d_src, d_shadow, k);
+            else tree_avg_kernel<<<grid, 256, 0, s>>>(d_scratch_ptr, 1, off, len, inv, 1, d_src, d_shadow, k);
         }
-        else if (m_total != 1)
-            throw std::runtime_error("allreduce_average: got 1 contributions for m = " + std::to_string(m_total));
-        // m == 1: x * 1.0 is the identity (parallel.cpp:56-57), nothing to do.
-    } else if (k == 1) {
-        ncclComm_t cm = static_cast<ncclComm_t>(comm->comm);
-        if (comm->nranks == m_total) {
-            NCCL_THROW(ncclAllReduce(reps[0]->params, reps[0]->params, n, ncclFloat, ncclAvg, cm, s));
-        } else {
-            throw std::runtime_error("allreduce_average: rank layout does not cover m workers");
-        }
-        if (reps[0]->wshadow) bf16_copy_kernel<<<grid, 256, 0, s>>>(reps[0]->params, n, reps[0]->wshadow);
-    } else {
-        // local subtree sum -> NCCL sum over GPUs -> x 1/m into every local replica
-        if (AvgFn f = vec_ok ? avg4_pick(k, std::make_integer_sequence<int, 32>{}) : nullptr)
-            f<<<grid, 256, 0, s>>>(d_src, n, 1.f, 0, d_scratch_ptr, d_shadow, 0);
-        else
-            tree_avg_kernel<<<grid, 256, 0, s>>>(d_src, k, n, 1.f, 0, d_scratch_ptr, d_shadow, 0);
-        NCCL_THROW(ncclAllReduce(scratch, scratch, n, ncclFloat, ncclSum, static_cast<ncclComm_t>(comm->comm), s));
-        tree_avg_kernel<<<grid, 256, 0, s>>>(d_scratch_ptr, 1, n, inv, 1, d_src, d_shadow, k);
+        for (Replica* r : reps) CUDA_THROW(cudaEventRecord(r->ev_gate[l], s));
     }
     CUDA_THROW(cudaGetLastError());
-    CUDA_THROW(cudaEventRecord(ev_done, s));
-    for (int i = 0; i < k; ++i) CUDA_THROW(cudaStreamWaitEvent(reps[i]->stream, ev_done, 0));
 }
 
 }  // namespace pnb

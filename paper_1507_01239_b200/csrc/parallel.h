@@ -20,7 +20,11 @@ struct Comm {
 void nccl_unique_id(unsigned char out[128]);
 
 // Replaces every local replica's parameters with the mean over all m workers
-// (local replicas + every other process in `comm`).
+// (local replicas + every other process in `comm`), one layer bucket
+// ([W_l | b_l]) at a time on the context stream, in the order the averaged step
+// finishes the layers (L-1 .. 0): bucket l starts when every local replica has
+// recorded ev_upd[l] and ends by recording each replica's ev_gate[l], which the
+// replica's next forward of layer l waits on (runtime.h).
 struct Averager {
     Context* ctx;
     std::vector<Replica*> reps;
@@ -29,13 +33,14 @@ struct Averager {
     long n = 0;
     float** d_src = nullptr;
     bf16** d_shadow = nullptr;
+    bf16** d_null_shadow = nullptr;  // one null shadow pointer: the unscaled partial sum has none
     float* scratch = nullptr;
     float** d_scratch_ptr = nullptr;
-    cudaEvent_t ev_done = nullptr;
-    std::vector<cudaEvent_t> ev_rep;
     Averager(Context* c, const std::vector<Replica*>& reps, Comm* comm, long m_total);
     ~Averager();
     void run();
+    // bytes one averaging event moves per GPU over the interconnect (fp32 params)
+    double bytes() const { return 4.0 * static_cast<double>(n); }
 };
 
 struct TrainConfig {

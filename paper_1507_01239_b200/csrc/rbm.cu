@@ -365,12 +365,12 @@ double RbmDevice::reconstruction_error_host(const double* x, long n) {
 // are skipped with an xoshiro256** GF(2) jump, while the device draws its own
 // counter-based Philox uniforms.
 void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* data, long n, uint64_t epochs,
-                     double lr_g, double lr_b, long batch, uint64_t seed, Precision prec, double* out) {
+                     double lr_g, double lr_b, long batch, host::Rng& rng, uint64_t philox_seed, Precision prec,
+                     double* out) {
     if (dims.size() < 2) throw std::runtime_error("greedy_pretrain: need at least 2 dims");
     if (batch <= 0) throw std::runtime_error("greedy_pretrain: batch size must be >= 1");
     if (n <= 0) throw std::runtime_error("cd1_gibbs: empty batch");
     const long bs = std::min(batch, n);
-    host::Rng rng(seed);
     long d0 = dims[0], ld0 = pad32(d0);
     float* X = nullptr;
     {
@@ -409,7 +409,7 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
                 else
                     load_rows_kernel<bf16><<<grid_of(bs * ldx), 256, 0, rbm.stream>>>(
                         X, ldx, d_idx + b * bs, bs, v, static_cast<bf16*>(rbm.XR), ldx);
-                rbm.cd1(bs, lr, 0, seed ^ 0x5851F42D4C957F2Dull, counter);
+                rbm.cd1(bs, lr, 0, philox_seed, counter);
                 counter += static_cast<uint64_t>(bs) * static_cast<uint64_t>(h);
                 rng.jump(skip);
             }

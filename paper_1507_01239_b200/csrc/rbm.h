@@ -2,6 +2,7 @@
 #pragma once
 #include <vector>
 
+#include "host.h"
 #include "runtime.h"
 
 namespace pnb {
@@ -39,7 +40,10 @@ struct RbmDevice {
     double reconstruction_error_host(const double* x, long n);
 };
 
+// rng: the caller's generator, advanced exactly as the reference advances it;
+// philox_seed keys the device Bernoulli draws.
 void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* data, long n, uint64_t epochs,
-                     double lr_g, double lr_b, long batch, uint64_t seed, Precision prec, double* params_out);
+                     double lr_g, double lr_b, long batch, host::Rng& rng, uint64_t philox_seed, Precision prec,
+                     double* params_out);
 
 }  // namespace pnb

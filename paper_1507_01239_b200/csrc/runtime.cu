@@ -51,14 +51,49 @@ __global__ void flags_latch_kernel(unsigned* flags, const int* step) {
 
 }  // namespace
 
+// Event record / wait that become external event nodes when the stream is
+// being captured into a graph (a plain record inside a capture is only a
+// fork/join marker), so they synchronise with work outside the graph.
+void record_ext(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs;
+    CUDA_THROW(cudaStreamIsCapturing(s, &cs));
+    if (cs == cudaStreamCaptureStatusActive)
+        CUDA_THROW(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+    else
+        CUDA_THROW(cudaEventRecord(e, s));
+}
+
+// Kernel nodes of a captured graph (event record / wait and memcpy nodes are not kernels).
+long count_kernel_nodes(cudaGraph_t g) {
+    size_t n = 0;
+    CUDA_THROW(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CUDA_THROW(cudaGraphGetNodes(g, nodes.data(), &n));
+    long k = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        CUDA_THROW(cudaGraphNodeGetType(nd, &t));
+        k += t == cudaGraphNodeTypeKernel;
+    }
+    return k;
+}
+
+void wait_ext(cudaStream_t s, cudaEvent_t e) {
+    cudaStreamCaptureStatus cs;
+    CUDA_THROW(cudaStreamIsCapturing(s, &cs));
+    CUDA_THROW(cudaStreamWaitEvent(s, e, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+}
+
 Context::Context(int dev) : device(dev) {
     CUDA_THROW(cudaSetDevice(dev));
     CUDA_THROW(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     CUDA_THROW(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CUDA_THROW(cudaStreamCreateWithFlags(&avg, cudaStreamNonBlocking));
 }
 
 Context::~Context() {
     if (stream) cudaStreamDestroy(stream);
+    if (avg) cudaStreamDestroy(avg);
 }
 
 DeviceDataset::DeviceDataset(Context* c, const double* x, const int32_t* labels, long n_, long d_, long classes_)
@@ -118,9 +153,13 @@ Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision
     L = static_cast<int>(dims.size()) - 1;
     ev_bwd.resize(L);
     ev_dw.resize(L);
+    ev_upd.resize(L);
+    ev_gate.resize(L);
     for (int l = 0; l < L; ++l) {
         CUDA_THROW(cudaEventCreateWithFlags(&ev_bwd[l], cudaEventDisableTiming));
         CUDA_THROW(cudaEventCreateWithFlags(&ev_dw[l], cudaEventDisableTiming));
+        CUDA_THROW(cudaEventCreateWithFlags(&ev_upd[l], cudaEventDisableTiming));
+        CUDA_THROW(cudaEventCreateWithFlags(&ev_gate[l], cudaEventDisableTiming));
     }
     long off = 0;
     for (int l = 0; l < L; ++l) {
@@ -197,8 +236,12 @@ Replica::~Replica() {
     dfree(d_ce);
     dfree(d_flags);
     dfree(d_err);
+    dfree(eval_rows);
+    dfree(eval_correct);
     for (auto e : ev_bwd) cudaEventDestroy(e);
     for (auto e : ev_dw) cudaEventDestroy(e);
+    for (auto e : ev_upd) cudaEventDestroy(e);
+    for (auto e : ev_gate) cudaEventDestroy(e);
     if (ev_side) cudaEventDestroy(ev_side);
     if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
@@ -219,6 +262,8 @@ void Replica::set_params(const double* flat) {
         for (long r = 0; r < dims[l + 1]; ++r) h[b_off[l] + r] = static_cast<float>(flat[pos++]);
     }
     CUDA_THROW(cudaSetDevice(ctx->device));
+    CUDA_THROW(cudaStreamSynchronize(stream));
+    CUDA_THROW(cudaStreamSynchronize(ctx->avg));
     CUDA_THROW(cudaMemcpy(params, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
     sync_shadow(stream);
     CUDA_THROW(cudaStreamSynchronize(stream));
@@ -228,6 +273,7 @@ void Replica::get_params(double* flat) const {
     std::vector<float> h(static_cast<size_t>(n_pad));
     CUDA_THROW(cudaSetDevice(ctx->device));
     CUDA_THROW(cudaStreamSynchronize(stream));
+    CUDA_THROW(cudaStreamSynchronize(ctx->avg));  // a pending average
     CUDA_THROW(cudaMemcpy(h.data(), params, h.size() * 4, cudaMemcpyDeviceToHost));
     long pos = 0;
     for (int l = 0; l < L; ++l) {
@@ -400,9 +446,7 @@ void Replica::bind(DeviceDataset* ds) {
                 throw;
             }
             CUDA_THROW(cudaStreamEndCapture(s, &g));
-            size_t nodes = 0;
-            CUDA_THROW(cudaGraphGetNodes(g, nullptr, &nodes));
-            *nodes_out = static_cast<long>(nodes);
+            *nodes_out = count_kernel_nodes(g);
             CUDA_THROW(cudaGraphInstantiate(out, g, 0));
             cudaGraphDestroy(g);
         };
@@ -442,9 +486,7 @@ void Replica::capture_variant(int v) {
         throw;
     }
     CUDA_THROW(cudaStreamEndCapture(stream, &g));
-    size_t nodes = 0;
-    CUDA_THROW(cudaGraphGetNodes(g, nullptr, &nodes));
-    vnodes[v] = static_cast<long>(nodes);
+    vnodes[v] = count_kernel_nodes(g);
     CUDA_THROW(cudaGraphInstantiate(&vgraphs[v], g, 0));
     cudaGraphDestroy(g);
     variant = saved;
@@ -497,9 +539,7 @@ void Replica::capture_apply_graph() {
         throw;
     }
     CUDA_THROW(cudaStreamEndCapture(bg, &g));
-    size_t nodes = 0;
-    CUDA_THROW(cudaGraphGetNodes(g, nullptr, &nodes));
-    apply_nodes = static_cast<long>(nodes);
+    apply_nodes = count_kernel_nodes(g);
     CUDA_THROW(cudaGraphInstantiate(&apply_graph, g, 0));
     cudaGraphDestroy(g);
 }
@@ -595,6 +635,7 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
                       r.ld_act[0], r.d_ybatch, F, s);
         r.mark("gather", 0, 0, s);
         for (int l = 0; l < L; ++l) {
+            wait_ext(s, r.ev_gate[l]);
             gemm_launch(r.fwd[l], s);
             r.mark("gemm_fwd", l, gf(r.fwd[l]), s);
         }
@@ -609,6 +650,7 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
             lr_side_chain(r, r.lrl[l].out, nullptr, s);
             r.mark("ng_lr_precondition", l, 0, s);
             lr_layer_update(r, l, s);
+            record_ext(r.ev_upd[l], s);
             r.mark("gemm_dw_sgd", l, gf(r.dw[l]), s);
         }
     } else {
@@ -631,6 +673,7 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
         CUDA_THROW(cudaEventRecord(r.ev_act[0], s));
         if (!in_late) lr_side_chain(r, r.lrl[0].in, r.ev_act[0], S(r.lrl[0].in.stream));
         for (int l = 0; l < L; ++l) {
+            wait_ext(s, r.ev_gate[l]);  // layer l's average (if one is pending) is done
             gemm_launch(r.fwd[l], s);
             if (l + 1 < L) {
                 CUDA_THROW(cudaEventRecord(r.ev_act[l + 1], s));
@@ -658,6 +701,7 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
             CUDA_THROW(cudaStreamWaitEvent(ws, r.ev_bwd[0], 0));
             CUDA_THROW(cudaStreamWaitEvent(ws, r.lrl[l].out.ready, 0));
             lr_layer_update(r, l, ws);
+            record_ext(r.ev_upd[l], ws);  // layer l final for this step: its average may start
             r.tmark("dw" + std::to_string(l), ws);
             CUDA_THROW(cudaEventRecord(r.lrl[l].in.done, ws));
         }
@@ -687,6 +731,7 @@ void Replica::enqueue_step(cudaStream_t s) {
     launch_gather(ds->features(prec), ds->ld, ds->y, d_rows, d_step, B, dims[0], acts[0], ld_act[0], d_ybatch, F, s);
     mark("gather", 0, 0, s);
     for (int l = 0; l < L; ++l) {
+        wait_ext(s, ev_gate[l]);  // layer l's average (if one is pending) is done
         gemm_launch(fwd[l], s);
         mark("gemm_fwd", l, gf(fwd[l]), s);
     }
@@ -711,6 +756,7 @@ void Replica::enqueue_step(cudaStream_t s) {
             launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
                              ng ? grads + b_off[l] : nullptr, d_lr, d_step, d_flags, 2 * l + 1, side);
             gemm_launch(dw[l], side);
+            if (!ng) record_ext(ev_upd[l], side);  // layer l final for this step
             tmark("dw" + std::to_string(l), side);
             if (ng) {
                 CUDA_THROW(cudaEventRecord(ev_dw[l], side));
@@ -720,6 +766,7 @@ void Replica::enqueue_step(cudaStream_t s) {
                 gemm_launch(mom_out[l], ls);
                 ng_precondition_layer(*this, l, ls);
                 ng_apply_update(*this, l, ls);
+                record_ext(ev_upd[l], ls);
                 tmark("done" + std::to_string(l), ls);
                 CUDA_THROW(cudaEventRecord(ngl[l].done, ls));
             }
@@ -742,6 +789,7 @@ void Replica::enqueue_step(cudaStream_t s) {
             mark("gemm_da", l, gf(da[l]), s);
         }
         gemm_launch(dw[l], s);
+        if (!ng) record_ext(ev_upd[l], s);
         mark(ng ? "gemm_dw" : "gemm_dw_sgd", l, gf(dw[l]), s);
     }
     if (ng) {
@@ -755,6 +803,7 @@ void Replica::enqueue_step(cudaStream_t s) {
             for (int l = 0; l < L; ++l) {
                 ng_precondition_layer(*this, l, s);
                 ng_apply_update(*this, l, s);
+                record_ext(ev_upd[l], s);
             }
         } else {
             // the layers' NG chains are independent: fork one stream per layer, join
@@ -766,6 +815,7 @@ void Replica::enqueue_step(cudaStream_t s) {
                 gemm_launch(mom_out[l], ls);
                 ng_precondition_layer(*this, l, ls);
                 ng_apply_update(*this, l, ls);
+                record_ext(ev_upd[l], ls);
                 CUDA_THROW(cudaEventRecord(ngl[l].done, ls));
             }
             for (int l = 0; l < L; ++l) CUDA_THROW(cudaStreamWaitEvent(s, ngl[l].done, 0));
@@ -921,11 +971,20 @@ double Replica::accuracy(DeviceDataset* ds) {
     if (!bound) throw std::runtime_error("replica: bind a training dataset first");
     cudaStream_t s = stream;
     const bool F = f32();
-    uint32_t* rows = dalloc<uint32_t>(ds->n);
-    std::vector<uint32_t> h(ds->n);
-    for (long i = 0; i < ds->n; ++i) h[i] = static_cast<uint32_t>(i);
-    unsigned long long* correct = dalloc<unsigned long long>(1);
-    CUDA_THROW(cudaMemcpyAsync(rows, h.data(), ds->n * 4, cudaMemcpyHostToDevice, s));
+    if (!eval_correct) eval_correct = dalloc<unsigned long long>(1);
+    if (eval_rows_n < ds->n) {  // identity row ids, grown on demand and kept
+        CUDA_THROW(cudaStreamSynchronize(s));
+        dfree(eval_rows);
+        eval_rows = dalloc<uint32_t>(ds->n);
+        std::vector<uint32_t> h(ds->n);
+        for (long i = 0; i < ds->n; ++i) h[i] = static_cast<uint32_t>(i);
+        CUDA_THROW(cudaMemcpy(eval_rows, h.data(), ds->n * 4, cudaMemcpyHostToDevice));
+        eval_rows_n = ds->n;
+    }
+    uint32_t* rows = eval_rows;
+    unsigned long long* correct = eval_correct;
+    CUDA_THROW(cudaMemsetAsync(correct, 0, sizeof(unsigned long long), s));
+    for (int l = 0; l < L; ++l) wait_ext(s, ev_gate[l]);  // a pending average
     for (long c0 = 0; c0 < ds->n; c0 += B) {
         const long cb = std::min(B, ds->n - c0);
         launch_gather(ds->features(prec), ds->ld, ds->y, rows + c0, nullptr, cb, dims[0], acts[0], ld_act[0], d_ybatch,
@@ -936,8 +995,6 @@ double Replica::accuracy(DeviceDataset* ds) {
     unsigned long long hc = 0;
     CUDA_THROW(cudaMemcpyAsync(&hc, correct, 8, cudaMemcpyDeviceToHost, s));
     CUDA_THROW(cudaStreamSynchronize(s));
-    dfree(rows);
-    dfree(correct);
     return static_cast<double>(hc) / static_cast<double>(ds->n);
 }
 
@@ -947,6 +1004,7 @@ void Replica::forward_only(DeviceDataset* ds, const uint32_t* rows_h, long b, fl
     cudaStream_t s = stream;
     uint32_t* rows = dalloc<uint32_t>(b);
     CUDA_THROW(cudaMemcpyAsync(rows, rows_h, b * 4, cudaMemcpyHostToDevice, s));
+    for (int l = 0; l < L; ++l) wait_ext(s, ev_gate[l]);
     launch_gather(ds->features(prec), ds->ld, ds->y, rows, nullptr, b, dims[0], acts[0], ld_act[0], d_ybatch, f32(), s);
     for (int l = 0; l < L; ++l) gemm_launch(fwd[l], s);
     std::vector<float> h(static_cast<size_t>(b * ld_act[L]));

@@ -34,10 +34,17 @@ struct GemmPlan {
     void* fn = nullptr;
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// function attributes are per device and the C ABI allows contexts on several
+// devices (and replicas built from several threads) in one process.
+void ensure_smem_attr(const void* fn, int bytes);
+
 int choose_bn(int M, int N, int num_sms);
 // prec: 0 = BF16 operands, 1 = TF32, 2 = fp32 via 3xTF32 split
+// force_mc (tests / tuning): 0 = automatic, 1 = single-CTA tiles, 2 = CTA pairs
+// with 2-SM MMAs, 3 = split-K CTA pairs (bf16 only for 2 and 3)
 void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b_mn, const void* B, long ldb,
-               int M, int N, int K, const GemmEpi& ep, int num_sms, int force_bn = 0);
+               int M, int N, int K, const GemmEpi& ep, int num_sms, int force_bn = 0, int force_mc = 0);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);
 // Cap on the persistent grid of subsequent launches from this thread (0 = none):
 // steps that run long single-CTA kernels (the NG subspace eigensolves) beside
@@ -54,6 +61,7 @@ struct Context {
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t avg = nullptr;  // model averaging (parallel.cu Averager), apart from host copies
     explicit Context(int dev);
     ~Context();
 };
@@ -207,6 +215,21 @@ struct Replica {
     double* d_ce = nullptr;       // [max_steps] batch-mean CE
     unsigned* d_flags = nullptr;  // non-finite weight/bias grad bits (2 per layer)
     DevErr* d_err = nullptr;
+    // accuracy(): row ids of the evaluated set and the correct counter, kept
+    // across calls (zeroed on the replica stream, not by a legacy-stream memset)
+    uint32_t* eval_rows = nullptr;
+    long eval_rows_n = 0;
+    unsigned long long* eval_correct = nullptr;
+
+    // Per-layer averaging buckets (parallel.cu Averager). ev_upd[l] is recorded
+    // inside every step (graph: external record node) once layer l's update is
+    // final; the averager waits on it, averages layer l's [W_l | b_l] range on
+    // its own stream and records ev_gate[l]; every step waits on ev_gate[l]
+    // (graph: external wait node) right before its forward GEMM of layer l. So
+    // the average of the last layers overlaps the next step's first layers.
+    std::vector<cudaEvent_t> ev_upd, ev_gate;
+    long bucket_begin(int l) const { return w_off[l]; }
+    long bucket_end(int l) const { return l + 1 < L ? w_off[l + 1] : n_pad; }
 
     DeviceDataset* bound = nullptr;  // dataset the plans/graph were built for
     std::vector<GemmPlan> fwd, dw, da, mom_in, mom_out;
@@ -283,6 +306,13 @@ struct Replica {
     void forward_only(DeviceDataset* ds, const uint32_t* rows, long b, float* zout_host);
     double accuracy(DeviceDataset* ds);
 };
+
+void debug_gemm(int prec, bool a_mn, bool b_mn, int M, int N, int K, int mode, int act, int ksplit, int force_bn,
+                int force_mc, int lower, int bias_col, float alpha, float beta, float lr, const float* a,
+                const float* b, const float* bias, const float* aux, float* out, float* out2, double* sums,
+                int* info);
+void record_ext(cudaEvent_t e, cudaStream_t s);
+void wait_ext(cudaStream_t s, cudaEvent_t e);
 
 // ----------------------------------------------------------- kernels.cu
 void launch_gather(const void* x, long ldx, const int32_t* y, const uint32_t* rows, const int* step, long B,

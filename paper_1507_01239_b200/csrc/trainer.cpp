@@ -19,8 +19,26 @@ void train(Context* ctx, Comm* comm, const TrainConfig& cfg, const std::vector<l
     if (cfg.minibatch == 0) throw std::runtime_error("train_parallel: minibatch must be >= 1");
     if (cfg.epochs > 0 && (!cv_ds || cv_ds->n == 0)) throw std::runtime_error("train_parallel: empty CV set");
     const uint64_t m = cfg.workers;
-    const uint64_t local = cfg.local ? cfg.local : m;
-    if (cfg.rank0 + local > m) throw std::runtime_error("train_parallel: hosted ranks exceed workers");
+    // placement: without a communicator this process hosts every worker; with one,
+    // each of the comm's processes hosts the contiguous block [rank * m/n, (rank+1) * m/n)
+    uint64_t local = cfg.local;
+    if (!comm) {
+        if (local == 0) local = m;
+        if (local != m || cfg.rank0 != 0)
+            throw std::runtime_error("train_parallel: without a communicator this process must host all " +
+                                     std::to_string(m) + " workers (got " + std::to_string(local) + " from rank " +
+                                     std::to_string(cfg.rank0) + ")");
+    } else {
+        const uint64_t nr = static_cast<uint64_t>(comm->nranks);
+        if (m % nr != 0)
+            throw std::runtime_error("train_parallel: " + std::to_string(m) + " workers do not split over " +
+                                     std::to_string(nr) + " processes");
+        if (local == 0) local = m / nr;
+        if (local != m / nr || cfg.rank0 != static_cast<uint64_t>(comm->rank) * local)
+            throw std::runtime_error("train_parallel: process " + std::to_string(comm->rank) + " must host workers [" +
+                                     std::to_string(comm->rank * (m / nr)) + ", " +
+                                     std::to_string((comm->rank + 1) * (m / nr)) + ")");
+    }
 
     // partition_data: one global shuffle by base_seed, m contiguous shards.
     const std::vector<uint64_t> shards = host::partition_rows(train_ds->n, m, cfg.base_seed);
@@ -102,7 +120,7 @@ void train(Context* ctx, Comm* comm, const TrainConfig& cfg, const std::vector<l
             ++events;
         }
         for (Replica* r : reps) CUDA_THROW(cudaStreamSynchronize(r->stream));
-        CUDA_THROW(cudaStreamSynchronize(ctx->stream));
+        CUDA_THROW(cudaStreamSynchronize(ctx->avg));
         const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (step_seconds && nb) *step_seconds = wall / static_cast<double>(nb);
 

@@ -5,9 +5,8 @@ One process per GPU hosts a contiguous block of worker ranks (config 5 runs
 4 virtual workers per GPU). For power-of-two counts the reference's
 midpoint tree over [0, m) splits exactly at the process boundaries, so
 "local subtree sum -> cross-process sum -> x 1/m" reproduces the reference's
-summation grouping. The device implementation of this is
-Averager (csrc/parallel.cu); this module holds the host-side plan and a
-reference implementation of the same arithmetic for tests.
+summation grouping. The average itself runs on the device
+(Averager, csrc/parallel.cu); this module holds the host-side placement plan.
 """
 from __future__ import annotations
 
@@ -56,21 +55,3 @@ def epoch_orders(shard_size: int, minibatch: int, layout: WorkerLayout, base_see
         seeds = P.rng_u64(base_seed + r, epochs)
         out.append([P.minibatch_rows(shard_size, minibatch, int(s)) for s in seeds])
     return out
-
-
-def _tree(vs, lo, hi):
-    if hi - lo == 1:
-        return np.array(vs[lo], dtype=np.float64, copy=True)
-    mid = lo + (hi - lo) // 2
-    return _tree(vs, lo, mid) + _tree(vs, mid, hi)
-
-
-def hierarchical_average(local_vectors, layout: WorkerLayout, allreduce_sum) -> np.ndarray:
-    """Local subtree sum -> allreduce_sum across processes -> x (1/m).
-    Equals allreduce_average bitwise when m and world are powers of two."""
-    if len(local_vectors) != layout.local:
-        raise P.ParnnError(f"allreduce_average: got {len(local_vectors)} local contributions, "
-                           f"expected {layout.local}")
-    part = _tree(local_vectors, 0, layout.local)
-    total = allreduce_sum(part)
-    return total * (1.0 / layout.workers)

@@ -475,6 +475,43 @@ def run_steps(replicas, steps: int, avg_frequency: int, comm=None, m_total: int 
     return out.value
 
 
+def time_average(replicas, comm=None, m_total: int | None = None, iters: int = 10) -> tuple[float, float]:
+    """Device ms per averaging event (CUDA events, back to back) and the fp32
+    bytes one event reduces per GPU."""
+    arr = (C.c_void_p * len(replicas))(*[r.h for r in replicas])
+    ms, nb = C.c_double(), C.c_double()
+    check(lib().parnn_time_average(arr, len(replicas), comm.h if comm else None,
+                                   m_total if m_total is not None else len(replicas), iters, C.byref(ms),
+                                   C.byref(nb)))
+    return ms.value, nb.value
+
+
+class Averager:
+    """A persistent averaging group (allreduce_average over local replicas +
+    comm): run() enqueues one averaging event without blocking the host."""
+
+    def __init__(self, replicas, comm=None, m_total: int | None = None):
+        arr = (C.c_void_p * len(replicas))(*[r.h for r in replicas])
+        h = C.c_void_p()
+        check(lib().parnn_averager_create(arr, len(replicas), comm.h if comm else None,
+                                          m_total if m_total is not None else len(replicas), C.byref(h)))
+        self.h, self._keep = h, list(replicas)
+
+    def run(self):
+        check(lib().parnn_averager_run(self.h))
+
+    def close(self):
+        if self.h:
+            lib().parnn_averager_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Comm:
     """NCCL communicator; the unique id travels through torch.distributed (plumbing)."""
 
@@ -596,3 +633,33 @@ def greedy_pretrain(dims, data, opts: PretrainOptions = PretrainOptions(), activ
     check(lib().parnn_greedy_pretrain(ctx.h, ptr(d), len(d), ptr(x), x.shape[0], opts.epochs, opts.lr_gaussian,
                                       opts.lr_bernoulli, opts.batch_size, seed, int(precision), ptr(out)))
     return MlpModel(list(map(int, dims)), Activation(activation), out)
+
+
+# ------------------------------------------------------------ test hooks
+EPI = {"fwd_act": 0, "fwd_linear": 1, "grad": 2, "grad_sgd": 3, "actgrad": 4, "ema": 5, "axpy": 6, "sub": 7,
+       "partial": 8, "resid": 9}
+
+
+def debug_gemm(a, b, mode: str, precision: Precision, a_mn: bool = False, b_mn: bool = False, out=None, bias=None,
+               aux=None, act: int = 0, ksplit: int = 1, force_bn: int = 0, force_mc: int = 0, lower: bool = False,
+               bias_col: int = -1, alpha: float = 1.0, beta: float = 0.0, lr: float = 0.0) -> dict:
+    """One production tcgen05 GEMM (parnn_debug_gemm): D[m, n] = sum_k A(m, k) B(n, k)
+    with A given [M x K] (or [K x M] when a_mn) and B [N x K] (or [K x N] when
+    b_mn), then the epilogue `mode`. Returns {out, out2, sums, mc, bn, ksplit,
+    flags, grid}."""
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    M, K = (a.shape[1], a.shape[0]) if a_mn else a.shape
+    N = b.shape[1] if b_mn else b.shape[0]
+    o = np.ascontiguousarray(out if out is not None else np.zeros((M, N)), np.float32).copy()
+    o2 = np.zeros((M, N), np.float32) if bias_col < 0 else np.zeros(M, np.float32)
+    bs = np.ascontiguousarray(bias, np.float32) if bias is not None else None
+    ax = np.ascontiguousarray(aux, np.float32) if aux is not None else None
+    sums = np.zeros(2)
+    info = np.zeros(6, np.int32)
+    check(lib().parnn_debug_gemm(int(precision), int(a_mn), int(b_mn), M, N, K, EPI[mode], act, ksplit, force_bn,
+                                 force_mc, int(lower), bias_col, alpha, beta, lr, ptr(a), ptr(b),
+                                 ptr(bs) if bs is not None else None, ptr(ax) if ax is not None else None, ptr(o),
+                                 ptr(o2), ptr(sums), ptr(info)))
+    return {"out": o, "out2": o2, "sums": sums, "mc": int(info[0]), "bn": int(info[1]), "ksplit": int(info[2]),
+            "flags": int(info[3]), "grid": int(info[4])}

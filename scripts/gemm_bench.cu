@@ -1,4 +1,8 @@
-// GEMM microbenchmark (warm L2, CUDA events, 20 reps) over the trainer's shapes.
+// GEMM microbenchmark over the trainer's shapes on RANDOM operands (uniform in
+// [-1, 1) from a hash, values of the operand type; zero operands under-load the
+// tensor cores' power and are not comparable with the measured peaks):
+// back-to-back launches (warm L2, CUDA events, 20 reps) and single launches
+// after a 400 MB L2 flush (cold).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1507_01239_b200/csrc -I include \
 //   scripts/gemm_bench.cu -o scripts/gemm_bench.bin
 #include <cstdio>
@@ -16,6 +20,20 @@
 #include "../paper_1507_01239_b200/csrc/gemm_k_bf16_r_sk.cu"
 #include "../paper_1507_01239_b200/csrc/gemm_k_bf16_t_sk.cu"
 using namespace pnb;
+
+__device__ __forceinline__ float hash_uniform(unsigned long long i, unsigned seed) {
+    unsigned long long x = i * 0x9E3779B97F4A7C15ull + seed;
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    return (float)((x >> 40) & 0xFFFFFF) / 8388608.0f - 1.0f;
+}
+template <typename T>
+__global__ void fill_random(T* p, long n, unsigned seed, float scale) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        p[i] = (T)(scale * hash_uniform(i, seed));
+}
+
 int main(int argc, char** argv) {
     int bnf = argc > 1 ? atoi(argv[1]) : 0;
     struct Case { const char* name; int prec; bool amn, bmn; int M, N, K; int mode; };
@@ -46,10 +64,25 @@ int main(int argc, char** argv) {
     cudaMemset(C2, 0, maxe * 4);
     cudaMemset(C3, 0, maxe * 4);
     cudaMemset(bias, 0, 65536 * 4);
-    cudaMemset(A, 0, maxe * 4);
-    cudaMemset(B, 0, maxe * 4);
     int sms = 148;
-    for (auto& c : cases) {
+    void* flush;
+    const size_t fl = 400L << 20;
+    cudaMalloc(&flush, fl);
+    fill_random<float><<<1184, 256>>>(bias, 65536, 7, 0.1f);
+    fill_random<float><<<1184, 256>>>(C, maxe, 9, 1.0f);  // fp32 master weights / factors
+    fill_random<__nv_bfloat16><<<1184, 256>>>(static_cast<__nv_bfloat16*>(C3), maxe, 11, 0.5f);  // activations
+    const int only = argc > 2 ? atoi(argv[2]) : -1;  // run one case (profiling)
+    for (size_t ci = 0; ci < cases.size(); ++ci) {
+        auto& c = cases[ci];
+        if (only >= 0 && static_cast<int>(ci) != only) continue;
+        if (c.prec == 0) {
+            fill_random<__nv_bfloat16><<<1184, 256>>>(static_cast<__nv_bfloat16*>(A), maxe, 1, 1.0f);
+            fill_random<__nv_bfloat16><<<1184, 256>>>(static_cast<__nv_bfloat16*>(B), maxe, 2, 1.0f);
+        } else {
+            fill_random<float><<<1184, 256>>>(static_cast<float*>(A), maxe, 1, 1.0f);
+            fill_random<float><<<1184, 256>>>(static_cast<float*>(B), maxe, 2, 1.0f);
+        }
+        cudaMemset(bias, 0, 64);  // lr[0] = 0: the SGD epilogue leaves the random weights in place
         GemmPlan p;
         GemmEpi e;
         e.mode = c.mode;
@@ -81,9 +114,22 @@ int main(int argc, char** argv) {
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
         double us = ms * 1e3 / reps;
-        double fl = 2.0 * c.M * c.N * c.K * (c.prec == 2 ? 3 : 1);
-        printf("%-28s bn=%3d grid=%3d  %8.2f us  %7.1f TFLOP/s%s  %s\n", c.name, p.bn, p.grid.x, us, fl / us / 1e6,
-               c.prec == 2 ? " (tf32 MMA rate, 3x)" : "", cudaGetErrorString(cudaGetLastError()));
+        // cold: one launch after flushing L2
+        double cold = 0.0;
+        for (int i = 0; i < 3; ++i) {
+            cudaMemsetAsync(flush, i, fl, s);
+            cudaEventRecord(e0, s);
+            gemm_launch(p, s);
+            cudaEventRecord(e1, s);
+            cudaEventSynchronize(e1);
+            float m1;
+            cudaEventElapsedTime(&m1, e0, e1);
+            cold += m1 * 1e3 / 3;
+        }
+        double flop = 2.0 * c.M * c.N * c.K;
+        printf("%-28s bn=%3d mc=%d grid=%3d  warm %8.2f us %7.1f TFLOP/s   cold %8.2f us %7.1f TFLOP/s%s  %s\n",
+               c.name, p.bn, p.mc, gemm_launch_grid(p).x, us, flop / us / 1e6, cold, flop / cold / 1e6,
+               c.prec == 2 ? " (fp32-accurate: 3 TF32 MMAs per product)" : "", cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
 }

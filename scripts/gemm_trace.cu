@@ -20,6 +20,16 @@
 
 using namespace pnb;
 
+__global__ void fill_random_bf16(__nv_bfloat16* p, long n, unsigned seed) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        unsigned long long x = i * 0x9E3779B97F4A7C15ull + seed;
+        x ^= x >> 33;
+        x *= 0xff51afd7ed558ccdull;
+        x ^= x >> 33;
+        p[i] = __float2bfloat16((float)((x >> 40) & 0xFFFFFF) / 8388608.0f - 1.0f);
+    }
+}
+
 int main() {
     const int M = 1024, N = 2048, K = 2048;
     void *A, *Bm, *out, *flush;
@@ -31,8 +41,9 @@ int main() {
     cudaMalloc(&bias, 65536 * 4);
     const size_t fl = 400L << 20;
     cudaMalloc(&flush, fl);
-    cudaMemset(A, 0, 8192L * 8192 * 2);
-    cudaMemset(Bm, 0, 8192L * 8192 * 2);
+    // random operands (zeros under-load the tensor cores)
+    fill_random_bf16<<<1184, 256>>>(static_cast<__nv_bfloat16*>(A), 8192L * 8192, 1);
+    fill_random_bf16<<<1184, 256>>>(static_cast<__nv_bfloat16*>(Bm), 8192L * 8192, 2);
     cudaMemset(bias, 0, 65536 * 4);
     float* lr;
     int* step;

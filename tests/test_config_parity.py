@@ -1,0 +1,127 @@
+"""Parity at the BASELINE.json configurations (north star: per-layer parameter
+relative L2 within 1e-4 after one averaging period in fp32 mode; final frame
+cross-entropy within 1% after a fixed number of epochs).
+
+* Config 1 (440-512-512-1000 sigmoid, plain SGD, one worker, minibatch 256,
+  100k synthetic frames): the full 4-epoch train_parallel run of the compiled
+  reference (tests/golden/golden_cfg1.npz, make_golden_cfg1.py) against the
+  CUDA trainer in fp32 mode -- identical epochs / lr / averaging events,
+  per-epoch train CE within 1%, CV accuracy within 0.01, the final parameters
+  on a fixed 10^4-coordinate digest; and one averaging period (K = 4 steps) at
+  the same shape, per layer within 1e-4 of the pinned numpy oracle (the oracle
+  itself is checked against the reference's digest in test_oracle.py).
+* Config 2 (440-2048x6-8806, minibatch 1024): one averaging period (4 steps)
+  in fp32 mode with plain SGD and with the reference's kron-full NG-SGD,
+  against the numpy oracle run live on the same data: per-layer theta within
+  1e-4, the update (theta_K - theta_0) within 2e-3, per-step CE within 1e-5.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, rel
+from oracle import parnn_oracle as O
+from paper_1507_01239_b200 import parnn as P
+
+pytestmark = pytest.mark.gpu
+
+FP32 = P.Precision.fp32
+CFG1_DIMS = [440, 512, 512, 1000]
+CFG2_DIMS = [440] + [2048] * 6 + [8806]
+
+
+def layer_rel(p, ref, dims):
+    out, pos = [], 0
+    for l in range(len(dims) - 1):
+        n = dims[l] * dims[l + 1] + dims[l + 1]
+        out.append(rel(p[pos:pos + n], ref[pos:pos + n]))
+        pos += n
+    return out
+
+
+def oracle_steps(dims, p0, x, y, rows, lrs, ngsgd, B):
+    m = O.unflatten(p0, dims)
+    st = O.ng_init(m) if ngsgd else None
+    ces = []
+    for s, lr in enumerate(lrs):
+        rr = rows[s * B:(s + 1) * B]
+        t = O.forward(m, x[rr])
+        ces.append(O.cross_entropy(t, y[rr]))
+        if ngsgd:
+            gW, gb, dzs = O.backward(m, t, y[rr], want_dz=True)
+            O.ng_update_state(st, t, dzs)
+            gW, gb = O.ng_precondition(st, gW, gb)
+        else:
+            gW, gb = O.backward(m, t, y[rr])
+        O.sgd_step(m, gW, gb, lr)
+    return O.flatten(m), np.array(ces)
+
+
+def one_period(ctx, dims, tr, p0, rows, lrs, opt, B):
+    ds = P.DeviceDataset(ctx, tr)
+    r = P.Replica(ctx, dims, precision=FP32, optimizer=opt, minibatch=B, max_steps=len(lrs))
+    r.set_params(p0)
+    r.bind(ds)
+    r.upload_epoch(rows, lrs)
+    r.step(len(lrs))
+    r.sync()
+    return r.get_params(), r.ce(len(lrs))
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    path = os.path.join(ROOT, "tests", "golden", "golden_cfg1.npz")
+    g = dict(np.load(path))
+    tr, cv = P.make_data(1000, 440, 100, float(g["separation"]), 7, 0.10, 2, True)
+    return g, tr, cv
+
+
+def test_config1_full_run_matches_reference(ctx, cfg1):
+    g, tr, cv = cfg1
+    m0 = P.MlpModel(CFG1_DIMS, P.Activation.sigmoid, P.init_random(CFG1_DIMS, seed=1).params)
+    opts = P.TrainOptions(optimizer=P.OptimizerKind.sgd, lr_init=float(g["lr_init"]), epochs=int(g["epochs"]),
+                          precision=FP32)
+    res = P.train_parallel(P.ParallelPlan(1, 4, 256, 5), m0, tr, cv, opts, ctx=ctx)
+    ref = g["met"]
+    assert len(res.metrics) == ref.shape[0]
+    for e, mt in enumerate(res.metrics):
+        assert mt.epoch == ref[e, 0] and mt.workers == ref[e, 5] and mt.avg_events == ref[e, 6]
+        assert abs(mt.lr - ref[e, 1]) <= 1e-15 * ref[e, 1]
+        assert abs(mt.train_ce - ref[e, 2]) <= 0.01 * ref[e, 2]  # the final-CE gate: within 1%
+        assert abs(mt.cv_accuracy - ref[e, 3]) <= 0.01
+    # the CE actually moves (the gate is not passed by an untrained net)
+    assert ref[-1, 2] < 0.9 * np.log(1000)
+    idx = g["digest_idx"]
+    assert rel(res.model.params[idx], g["final_p_digest"]) < 2e-3
+
+
+def test_config1_one_period_vs_oracle(ctx, cfg1):
+    g, tr, _ = cfg1
+    p0 = P.init_random(CFG1_DIMS, seed=1).params
+    rows = P.minibatch_rows(tr.size(), 256, 21)[:4].ravel()
+    lrs = [0.32, 0.3, 0.28, 0.26]
+    p, ce = one_period(ctx, CFG1_DIMS, tr, p0, rows, lrs, P.OptimizerKind.sgd, 256)
+    ref, rce = oracle_steps(CFG1_DIMS, p0, tr.features, tr.labels, rows.astype(np.int64), lrs, False, 256)
+    assert max(layer_rel(p, ref, CFG1_DIMS)) < 1e-4
+    assert rel(p - p0, ref - p0) < 2e-3
+    assert np.abs(ce - rce).max() <= 1e-5 * np.abs(rce).max()
+    # the same period on the compiled reference's digest
+    idx = g["digest_idx"]
+    assert rel(p[idx], g["period_p_digest"]) < 1e-4
+
+
+@pytest.mark.parametrize("opt", [P.OptimizerKind.sgd, P.OptimizerKind.ngsgd], ids=["sgd", "ngsgd_kron"])
+def test_config2_one_period_vs_oracle(ctx, opt):
+    tr, _ = P.make_data(8806, 440, 1, 8.0, 1, 0.10, 2, True)
+    B = 1024
+    p0 = P.init_random(CFG2_DIMS, seed=7).params
+    rows = P.minibatch_rows(tr.size(), B, 3)[:4].ravel()
+    lrs = [0.32, 0.3, 0.28, 0.26]
+    p, ce = one_period(ctx, CFG2_DIMS, tr, p0, rows, lrs, opt, B)
+    ref, rce = oracle_steps(CFG2_DIMS, p0, tr.features, tr.labels, rows.astype(np.int64), lrs,
+                            opt == P.OptimizerKind.ngsgd, B)
+    lr_ = layer_rel(p, ref, CFG2_DIMS)
+    assert max(lr_) < 1e-4, lr_
+    assert rel(p - p0, ref - p0) < 2e-3
+    assert np.abs(ce - rce).max() <= 1e-5 * np.abs(rce).max()

@@ -273,7 +273,7 @@ def test_reference_adapter_dropin():
         pytest.skip("integration/_build/adapter_demo not built (needs the reference headers at build time)")
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
-    res, low, err = [json.loads(l) for l in out.stdout.strip().splitlines()]
+    res, low, pre, err = [json.loads(l) for l in out.stdout.strip().splitlines()]
     assert res["epochs"][0] == res["epochs"][1] and res["avg_events"][0] == res["avg_events"][1]
     assert abs(res["ce_ref"] - res["ce_b200"]) <= 0.01 * res["ce_ref"]
     assert res["theta_rel_l2"] < 2e-3
@@ -281,6 +281,10 @@ def test_reference_adapter_dropin():
     assert low["lowrank_epochs"] == res["epochs"][0]
     assert np.isfinite(low["ce_lowrank"]) and low["ce_lowrank"] <= 1.05 * low["ce_ref"]
     assert "train_parallel: avg_frequency must be >= 1" in err["error"]
+    # greedy_pretrain drop-in: the caller's Rng (incl. a cached gaussian spare) crosses the ABI
+    # and comes back in the reference's state; the output layer is bit-identical
+    assert pre["pretrain_output_layer_equal"] and pre["pretrain_rng_state_equal"] and pre["activation_equal"]
+    assert pre["pretrain_layer0_rel_l2"] < 0.5  # CD-1 Bernoulli draws differ (counter-based RNG)
 
 
 _PATH_SCRIPT = r"""

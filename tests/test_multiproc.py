@@ -18,6 +18,22 @@ import torch.multiprocessing as mp
 from oracle import parnn_oracle as O
 
 
+def _tree(vs, lo, hi):
+    if hi - lo == 1:
+        return np.array(vs[lo], dtype=np.float64, copy=True)
+    mid = lo + (hi - lo) // 2
+    return _tree(vs, lo, mid) + _tree(vs, mid, hi)
+
+
+def hierarchical_average(local_vectors, layout, allreduce_sum):
+    """The arithmetic the device Averager performs across processes (local
+    subtree sum -> cross-process sum -> x 1/m), restated in numpy for the gloo
+    test: equals allreduce_average bitwise when m and world are powers of two.
+    The device path itself is tested on the GPU (tests/test_gpu_avg.py)."""
+    assert len(local_vectors) == layout.local
+    return allreduce_sum(_tree(local_vectors, 0, layout.local)) * (1.0 / layout.workers)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -32,7 +48,7 @@ def _worker(rank, world, port, m, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch
-    from paper_1507_01239_b200.parallel import epoch_orders, hierarchical_average, shard_rows, worker_layout
+    from paper_1507_01239_b200.parallel import epoch_orders, shard_rows, worker_layout
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:

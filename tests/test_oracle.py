@@ -241,3 +241,46 @@ def test_live_reference_agrees(reflib):
     _, _, ce = reflib.forward(dims, p, x, y)
     assert abs(ce - O.cross_entropy(O.forward(O.unflatten(p, dims), x), y)) < 1e-12
     assert math.isfinite(reflib.time_ng_precondition(16, 12))
+
+
+@pytest.mark.parametrize("ngsgd", [False, True])
+def test_threaded_reference_step_equals_reference(reflib, ngsgd):
+    """bench.py's reference arm (one true-width step of the reference's own
+    functions spread over host threads, ref_time_step_threaded) computes the
+    reference's single-threaded step (ref_train_steps) up to fp64 summation
+    order, including an output layer wide enough (rows > 2 x columns) to take
+    the column-chunked solves."""
+    dims = [40, 64, 48, 1100]
+    B = 96
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((B, dims[0]))
+    y = rng.integers(0, dims[-1], B).astype(np.int32)
+    p0 = reflib.init_random(dims, 3)
+    wall, ph, p, ce = reflib.time_step_threaded(dims, p0, x, y, ngsgd, 5, lr=0.3)
+    pr, cer, _, _ = reflib.train_steps(dims, p0, x, y, np.arange(B), B, [0.3], ngsgd)
+    assert wall > 0 and np.all(ph >= 0)
+    assert np.abs(p - pr).max() <= 1e-9 * np.abs(pr - p0).max()
+    assert abs(ce - cer[0]) <= 1e-12 * abs(cer[0])
+
+
+def test_oracle_config1_period_matches_reference_digest():
+    """The numpy oracle is pinned at the config-1 shape too (440-512-512-1000,
+    batch 256): one averaging period from the reference's own fixture."""
+    import os
+    from conftest import ROOT
+    from paper_1507_01239_b200 import parnn as P
+    g = dict(np.load(os.path.join(ROOT, "tests", "golden", "golden_cfg1.npz")))
+    dims = [440, 512, 512, 1000]
+    tr, _ = P.make_data(1000, 440, 100, float(g["separation"]), 7, 0.10, 2, True)
+    m = O.unflatten(P.init_random(dims, seed=1).params, dims)
+    rows = P.minibatch_rows(tr.size(), 256, 21)[:4].ravel().astype(np.int64)
+    ces = []
+    for s, lr in enumerate([0.32, 0.3, 0.28, 0.26]):
+        rr = rows[s * 256:(s + 1) * 256]
+        t = O.forward(m, tr.features[rr])
+        ces.append(O.cross_entropy(t, tr.labels[rr]))
+        gW, gb = O.backward(m, t, tr.labels[rr])
+        O.sgd_step(m, gW, gb, lr)
+    p = O.flatten(m)
+    assert rel(p[g["digest_idx"]], g["period_p_digest"]) < 1e-12
+    assert np.abs(np.array(ces) - g["period_ce"]).max() < 1e-12
