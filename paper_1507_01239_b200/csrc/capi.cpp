@@ -452,8 +452,9 @@ int parnn_run_steps(parnn_replica** reps, int n_local, parnn_comm* comm, uint64_
         CUDA_THROW(cudaEventRecord(a, ctx->stream));
         for (Replica* r : v) CUDA_THROW(cudaStreamWaitEvent(r->stream, a, 0));
         for (uint64_t s = 0; s < steps; ++s) {
-            for (Replica* r : v) r->run_step(r->stream);
-            if ((s + 1) % avg_frequency == 0 || s + 1 == steps) avg.run();  // last event closes the window
+            const bool window_end = (s + 1) % avg_frequency == 0 || s + 1 == steps;  // last event closes the window
+            for (Replica* r : v) r->run_step(r->stream, window_end);
+            if (window_end) avg.run();
         }
         // join: every replica stream (the last step's tail) and the averaging stream
         std::vector<cudaEvent_t> tails(v.size() + 1);

@@ -120,6 +120,9 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
     p.M = M;
     p.N = N;
     p.K = K;
+    p.prec = prec;
+    p.a_mn = a_mn;
+    p.b_mn = b_mn;
     p.ep = ep;
     p.ep.ksplit = ksplit;
     if (p.mc == 3) {
@@ -179,25 +182,101 @@ dim3 gemm_launch_grid(const GemmPlan& p) {
     return p.grid;
 }
 
+// Every GEMM is launched with programmatic stream serialization (PDL): the
+// kernel may start while the previous kernel of its stream finishes; it runs
+// its prologue (barriers, TMEM, descriptor prefetch) and then waits in
+// griddepcontrol.wait until that kernel has completed and its writes are
+// visible. The previous GEMM releases it once its own mainloop is done. Every
+// grid here fits the GPU in one wave (persistent, <= #SMs CTAs), so an early
+// dependent can only take SMs its predecessor does not hold.
+// PARNN_NO_PDL=1 turns it off (A/B timing).
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {
+    static const bool pdl = [] {
+        const char* v = std::getenv("PARNN_NO_PDL");
+        return !(v && v[0] == '1');
+    }();
     auto fn = reinterpret_cast<KernelFn>(p.fn);
-    if (p.mc == 1) {
-        fn<<<gemm_launch_grid(p), p.threads, p.smem, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.ep);
-    } else {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = gemm_launch_grid(p);
-        cfg.blockDim = dim3(p.threads, 1, 1);
-        cfg.dynamicSmemBytes = p.smem;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        CUDA_THROW(cudaLaunchKernelEx(&cfg, fn, p.ta, p.tb, p.M, p.N, p.K, p.ep));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = gemm_launch_grid(p);
+    cfg.blockDim = dim3(p.threads, 1, 1);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (p.mc != 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 2;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
     }
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    GemmParams<1> args;
+    args.ta[0] = p.ta;
+    args.tb[0] = p.tb;
+    args.ep[0] = p.ep;
+    args.M[0] = p.M;
+    args.N[0] = p.N;
+    args.K[0] = p.K;
+    args.tile0[0] = 0;
+    args.tile0[1] = p.tiles;
+    args.np = 1;
+    CUDA_THROW(cudaLaunchKernelEx(&cfg, fn, args));
+    CUDA_THROW(cudaGetLastError());
+}
+
+bool gemm_groupable(const GemmPlan& p) {
+    return p.prec == PREC_BF16 && p.a_mn && p.b_mn && p.bn == 256 && p.mc == 1 && p.ep.ksplit == 1 && !p.ep.lower &&
+           p.ep.mode == EPI_GRAD_SGD && p.ep.out32;
+}
+
+void gemm_group_plan(GemmGroupPlan& g, const std::vector<const GemmPlan*>& parts, int num_sms) {
+    if (parts.empty() || parts.size() > static_cast<size_t>(kGroupMax))
+        throw std::runtime_error("gemm: a group holds 1.." + std::to_string(kGroupMax) + " problems");
+    g.np = static_cast<int>(parts.size());
+    int t = 0;
+    for (int i = 0; i < g.np; ++i) {
+        const GemmPlan& p = *parts[i];
+        if (!gemm_groupable(p)) throw std::runtime_error("gemm: problem " + std::to_string(i) + " cannot be grouped");
+        g.args.ta[i] = p.ta;
+        g.args.tb[i] = p.tb;
+        g.args.ep[i] = p.ep;
+        g.args.M[i] = p.M;
+        g.args.N[i] = p.N;
+        g.args.K[i] = p.K;
+        g.args.tile0[i] = t;
+        t += ((p.M + 127) / 128) * ((p.N + 255) / 256);
+    }
+    g.args.tile0[g.np] = t;
+    g.args.np = g.np;
+    g.tiles = t;
+    g.grid = dim3(static_cast<unsigned>(std::min(t, num_sms)), 1, 1);
+    g.fn = reinterpret_cast<void*>(gemm_pick_group_dw(&g.smem));
+    g.threads = 320;
+}
+
+void gemm_group_launch(const GemmGroupPlan& g, cudaStream_t s) {
+    static const bool pdl = [] {
+        const char* v = std::getenv("PARNN_NO_PDL");
+        return !(v && v[0] == '1');
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = (g_grid_cap > 0 && static_cast<int>(g.grid.x) > g_grid_cap) ? dim3(g_grid_cap, 1, 1) : g.grid;
+    cfg.blockDim = dim3(g.threads, 1, 1);
+    cfg.dynamicSmemBytes = g.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CUDA_THROW(cudaLaunchKernelEx(&cfg, reinterpret_cast<GroupKernelFn>(g.fn), g.args));
     CUDA_THROW(cudaGetLastError());
 }
 

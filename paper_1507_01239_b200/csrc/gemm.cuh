@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <type_traits>
+
 #include "ptx.cuh"
 
 namespace pnb {
@@ -87,6 +89,19 @@ struct GemmEpi {
     double* part = nullptr; // RESID: [gridDim.x][2] per-CTA {sum aux^2, sum out^2}
 };
 
+// Kernel parameters: NP problems (1, or up to kGroupMax for a grouped launch).
+// Problem p owns the global tiles [tile0[p], tile0[p+1]).
+constexpr int kGroupMax = 8;
+template <int NP>
+struct GemmParams {
+    CUtensorMap ta[NP];
+    CUtensorMap tb[NP];
+    GemmEpi ep[NP];
+    int M[NP], N[NP], K[NP];
+    int tile0[NP + 1];
+    int np;
+};
+
 template <typename T>
 struct OpTraits;
 template <>
@@ -100,13 +115,41 @@ struct OpTraits<float> {
     static constexpr uint32_t kFmt = 2;
 };
 
+// sigmoid on the MUFU path: 1 / (1 + 2^(-z log2 e)) with ex2.approx and
+// rcp.approx (~2 ulp). The .ftz forms skip the denormal range fix-up that
+// __expf adds (an e^-z below 2^-126 leaves 1 + e^-z == 1 either way).
+__device__ __forceinline__ float sigmoid_fast(float z) {
+    float t, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(-1.4426950408889634f * z));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + t));
+    return r;
+}
+// ACT: 0 sigmoid, 1 tanh (the accurate tanhf: its 1 - 2/(1+e^2z) form cancels
+// near 0), 2 identity. Compile-time, so the epilogue loops over a chunk's 32
+// values carry no per-element branch and the MUFU chains interleave.
+template <int ACT>
+__device__ __forceinline__ float act_fwd_t(float z) {
+    if constexpr (ACT == 0) return sigmoid_fast(z);
+    else if constexpr (ACT == 1) return tanhf(z);
+    else return z;
+}
+template <int ACT>
+__device__ __forceinline__ float act_grad_t(float a) {
+    if constexpr (ACT == 0) return a * (1.f - a);
+    else return 1.f - a * a;
+}
 __device__ __forceinline__ float act_fwd(int act, float z) {
-    // sigmoid on the MUFU path (ex2 + approximate reciprocal, ~2 ulp); tanh keeps
-    // the accurate tanhf (its 1 - 2/(1+e^2z) form cancels near 0)
-    return act == 0 ? __fdividef(1.f, 1.f + __expf(-z)) : (act == 1 ? tanhf(z) : z);
+    return act == 0 ? act_fwd_t<0>(z) : (act == 1 ? act_fwd_t<1>(z) : z);
 }
 __device__ __forceinline__ float act_grad(int act, float a) {
-    return act == 0 ? a * (1.f - a) : 1.f - a * a;
+    return act == 0 ? act_grad_t<0>(a) : act_grad_t<1>(a);
+}
+// apply f<ACT>(i) for the runtime activation with the switch outside the loop
+template <typename F>
+__device__ __forceinline__ void with_act(int act, F&& f) {
+    if (act == 0) f(std::integral_constant<int, 0>{});
+    else if (act == 1) f(std::integral_constant<int, 1>{});
+    else f(std::integral_constant<int, 2>{});
 }
 
 template <typename T>
@@ -275,10 +318,12 @@ __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, const uint32_t
         case EPI_FWD_ACT: {
             float b[1][4];
             load_pieces<float, 1>(ep.bias + c, 0, 0, 1, nvc, b);
+            with_act(ep.act, [&](auto A) {
 #pragma unroll
-            for (int i = 0; i < PP; ++i)
+                for (int i = 0; i < PP; ++i)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) a[i][e] = ep.out_scale * act_fwd(ep.act, a[i][e] + b[0][e]);
+                    for (int e = 0; e < 4; ++e) a[i][e] = ep.out_scale * act_fwd_t<A.value>(a[i][e] + b[0][e]);
+            });
             store_pieces<T, PP>(static_cast<T*>(ep.out) + c, ep.ld_out, rb, M, nvc, a);
             break;
         }
@@ -336,10 +381,12 @@ __device__ __forceinline__ bool epilogue_chunk(const GemmEpi& ep, const uint32_t
         case EPI_ACTGRAD: {
             float x[PP][4];
             load_pieces<T, PP>(static_cast<const T*>(ep.aux) + c, ep.ld_aux, rb, M, nvc, x);
+            with_act(ep.act, [&](auto A) {
 #pragma unroll
-            for (int i = 0; i < PP; ++i)
+                for (int i = 0; i < PP; ++i)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) a[i][e] *= act_grad(ep.act, x[i][e]);
+                    for (int e = 0; e < 4; ++e) a[i][e] *= act_grad_t<A.value == 0 ? 0 : 1>(x[i][e]);
+            });
             store_pieces<T, PP>(static_cast<T*>(ep.out) + c, ep.ld_out, rb, M, nvc, a);
             break;
         }
@@ -498,14 +545,18 @@ __device__ __forceinline__ void epilogue_chunk_rows(const GemmEpi& ep, float (&v
     if (ep.mode == EPI_FWD_ACT) {
         if (have) rows_x_convert<float>(raw, x);
         else load_row32<float>(ep.bias + n, x, valid);
+        with_act(ep.act, [&](auto A) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = ep.out_scale * act_fwd(ep.act, v[j] + x[j]);
+            for (int j = 0; j < 32; ++j) v[j] = ep.out_scale * act_fwd_t<A.value>(v[j] + x[j]);
+        });
     } else {
         if (have) rows_x_convert<T>(raw, x);
         else load_row32<T>(static_cast<const T*>(ep.aux) + row * ep.ld_aux + n, x, valid);
         if (ep.mode == EPI_ACTGRAD) {
+            with_act(ep.act, [&](auto A) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] *= act_grad(ep.act, x[j]);
+                for (int j = 0; j < 32; ++j) v[j] *= act_grad_t<A.value == 0 ? 0 : 1>(x[j]);
+            });
         } else {  // EPI_RESID
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -542,16 +593,29 @@ inline bool gemm_epi_transposed(int mode) {
 // operand x as hi = x with the low 13 mantissa bits cleared (exact TF32, in
 // place) and lo = x - hi (exact in fp32) next to it; the MMA warp then
 // accumulates hi*hi + hi*lo + lo*hi: relative error ~2^-21 instead of 2^-11.
-template <typename T, int BN, int STAGES, bool A_MN, bool B_MN, bool SPLIT, bool TE, int MC>
+//
+// NP > 1 (grouped launch, MC == 1 only): NP independent problems of the same
+// operand type / tile shape / majors / epilogue style -- e.g. every layer's
+// dW -- in one persistent grid. The global tile index runs over the problems'
+// tiles back to back (problem p owns tiles [tile0[p], tile0[p+1])); each CTA
+// takes tiles b, b + grid, ... whatever problem they belong to, so the
+// epilogue of one problem's tile overlaps the mainloop of the next tile, of
+// the same or another problem. Every role re-selects the tile's problem.
+template <typename T, int BN, int STAGES, bool A_MN, bool B_MN, bool SPLIT, bool TE, int MC, int NP>
 __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   int M, int N, int K, GemmEpi ep) {
+    gemm_tc_kernel(const __grid_constant__ GemmParams<NP> P) {
     using S = GemmSmem<BN, STAGES, T, SPLIT, TE>;
     constexpr bool kTf32 = OpTraits<T>::kTf32;
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
     static_assert(!SPLIT || kTf32, "3xTF32 split needs fp32 operands");
     static_assert(MC == 1 || ((MC == 2 || MC == 3) && !SPLIT && !kTf32 && BN >= 128), "CTA pairs: bf16, BN >= 128");
     static_assert(MC != 3 || STAGES * S::kStage >= 2 * 128 * (BN / 2) * 4, "split-K pair: receive + send buffers in the ring");
+    static_assert(NP == 1 || MC == 1, "grouped launches: single-CTA tiles");
+    // problem 0; a grouped launch re-selects per tile (select() below)
+    const CUtensorMap& tmA = P.ta[0];
+    const CUtensorMap& tmB = P.tb[0];
+    const int M = P.M[0], N = P.N[0], K = P.K[0];
+    const GemmEpi& ep = P.ep[0];
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -576,34 +640,59 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     // CTA rank r runs the k-blocks of half r; the partial tiles are exchanged
     // through distributed shared memory and rank r finalises columns r BN/2 ...
     const int tmp = (tiles_m + 1) / 2;
-    const int tiles = MC == 1 ? tiles_mn * ep.ksplit : (MC == 3 ? tiles_mn : tmp * ((N + BN - 1) / BN));
+    const int tiles = NP > 1 ? P.tile0[P.np]
+                             : (MC == 1 ? tiles_mn * ep.ksplit : (MC == 3 ? tiles_mn : tmp * ((N + BN - 1) / BN)));
     const int w0 = MC == 1 ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x) / 2;
     const int wstep = MC == 1 ? static_cast<int>(gridDim.x) : static_cast<int>(gridDim.x) / 2;
     const int rank = MC == 1 ? 0 : static_cast<int>(cluster_ctarank());
-    auto tile_mn = [&](int w, int& m0, int& n0) {
-        if (MC != 2) {
-            m0 = (w % tiles_m) * 128;
-            n0 = ((w % tiles_mn) / tiles_m) * BN;
-        } else {
-            m0 = (2 * (w % tmp) + rank) * 128;
-            n0 = (w / tmp) * BN;
-        }
-    };
     const int nk_all = (K + S::kBK - 1) / S::kBK;
     const int nk_per = (nk_all + ep.ksplit - 1) / ep.ksplit;
-    auto tile_skipped = [&](int m0, int n0) { return ep.lower && n0 > m0 + 127; };
-    // k-block range [kb0, kb1) of split ks (gemm_plan guarantees it is non-empty)
-    auto krange = [&](int tile, int& kb0, int& kb1) {
+    // Work item -> problem, tile origin, split, k-block range [kb0, kb1) (gemm_plan
+    // guarantees it is non-empty), and whether a SYRK-style update skips it.
+    struct TileInfo {
+        int p, m0, n0, ks, kb0, kb1, M, N;
+        bool skip;
+    };
+    auto select = [&](int w) {
+        TileInfo t;
+        if constexpr (NP > 1) {
+            int p = 0;
+            while (p + 1 < P.np && w >= P.tile0[p + 1]) ++p;
+            const int lw = w - P.tile0[p];
+            const int tm = (P.M[p] + 127) / 128;
+            t.p = p;
+            t.M = P.M[p];
+            t.N = P.N[p];
+            t.m0 = (lw % tm) * 128;
+            t.n0 = (lw / tm) * BN;
+            t.ks = 0;
+            t.kb0 = 0;
+            t.kb1 = (P.K[p] + S::kBK - 1) / S::kBK;
+            t.skip = false;
+            return t;
+        }
+        t.p = 0;
+        t.M = M;
+        t.N = N;
+        if (MC != 2) {
+            t.m0 = (w % tiles_m) * 128;
+            t.n0 = ((w % tiles_mn) / tiles_m) * BN;
+        } else {
+            t.m0 = (2 * (w % tmp) + rank) * 128;
+            t.n0 = (w / tmp) * BN;
+        }
+        t.skip = ep.lower && t.n0 > t.m0 + 127;
         if (MC == 3) {
             const int half = (nk_all + 1) / 2;
-            kb0 = rank * half;
-            kb1 = min(nk_all, kb0 + half);
-            return 0;
+            t.ks = 0;
+            t.kb0 = rank * half;
+            t.kb1 = min(nk_all, t.kb0 + half);
+        } else {
+            t.ks = w / tiles_mn;
+            t.kb0 = t.ks * nk_per;
+            t.kb1 = min(nk_all, t.kb0 + nk_per);
         }
-        const int ks = tile / tiles_mn;
-        kb0 = ks * nk_per;
-        kb1 = min(nk_all, kb0 + nk_per);
-        return ks;
+        return t;
     };
 
     if (threadIdx.x == 0) {
@@ -620,8 +709,10 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
         mbar_init(&xbar[0], 2);  // MC == 3: each CTA's MMA completion, multicast to both
         for (int w = 1; w <= 8; ++w) mbar_init(&xbar[w], 1);  // MC == 3: own expect_tx + the peer warp's copy
         fence_barrier_init();
-        tma_prefetch_desc(&tmA);
-        tma_prefetch_desc(&tmB);
+        for (int p = 0; p < (NP > 1 ? P.np : 1); ++p) {
+            tma_prefetch_desc(&P.ta[p]);
+            tma_prefetch_desc(&P.tb[p]);
+        }
     }
     if (warp == 1) {
         if constexpr (MC == 2)
@@ -636,6 +727,10 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
     if constexpr (MC == 3) cluster_arrive_relaxed();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+    // Programmatic dependent launch (gemm_launch): everything above -- barrier
+    // init, TMEM allocation, descriptor prefetch -- overlapped the previous
+    // kernel of the stream; every operand, bias, aux or weight read comes after this.
+    grid_dep_wait();
     if (threadIdx.x == 0) PNB_TRACE(1);
 
     if (warp == 0) {
@@ -643,11 +738,11 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
         if (lane == 0) {
             int it = 0;  // global k-block counter (ring position)
             for (int tile = w0; tile < tiles; tile += wstep) {
-                int m0, n0;
-                tile_mn(tile, m0, n0);
-                if (tile_skipped(m0, n0)) continue;
-                int kb0, kb1;
-                krange(tile, kb0, kb1);
+                const TileInfo ti = select(tile);
+                if (ti.skip) continue;
+                const int m0 = ti.m0, n0 = ti.n0, kb0 = ti.kb0, kb1 = ti.kb1;
+                const CUtensorMap& tA = P.ta[ti.p];
+                const CUtensorMap& tB = P.tb[ti.p];
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
                     if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
@@ -677,18 +772,18 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     }
                     mbar_arrive_expect_tx(&full[s], S::kLoad);
                     if constexpr (!A_MN) {
-                        tma_load_2d(sa, &tmA, &full[s], k0, m0);
+                        tma_load_2d(sa, &tA, &full[s], k0, m0);
                     } else {
 #pragma unroll
                         for (int a = 0; a < 128 / S::kAtom; ++a)
-                            tma_load_2d(sa + a * (S::kBK * 128), &tmA, &full[s], m0 + a * S::kAtom, k0);
+                            tma_load_2d(sa + a * (S::kBK * 128), &tA, &full[s], m0 + a * S::kAtom, k0);
                     }
                     if constexpr (!B_MN) {
-                        tma_load_2d(sb, &tmB, &full[s], k0, n0);
+                        tma_load_2d(sb, &tB, &full[s], k0, n0);
                     } else {
 #pragma unroll
                         for (int a = 0; a < BN / S::kAtom; ++a)
-                            tma_load_2d(sb + a * (S::kBK * 128), &tmB, &full[s], n0 + a * S::kAtom, k0);
+                            tma_load_2d(sb + a * (S::kBK * 128), &tB, &full[s], n0 + a * S::kAtom, k0);
                     }
                 }
             }
@@ -716,15 +811,13 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
             };
             int it = 0, local = 0;
             for (int tile = w0; tile < tiles; tile += wstep) {
-                int m0, n0;
-                tile_mn(tile, m0, n0);
-                if (tile_skipped(m0, n0)) continue;
+                const TileInfo ti = select(tile);
+                if (ti.skip) continue;
                 const int acc = local & 1;
                 if (local >= 2) mbar_wait(&tempty[acc], ((local >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t d = tmem + acc * BN;
-                int kb0, kb1;
-                krange(tile, kb0, kb1);
+                const int kb0 = ti.kb0, kb1 = ti.kb1;
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(SPLIT ? &split_done[s] : &full[s], (it / STAGES) & 1);
@@ -771,20 +864,28 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
         const int quad = warp & 3;
         const int eset = (warp - 2) >> 2;
         uint4* ebuf = reinterpret_cast<uint4*>(smem + STAGES * S::kStage + 512) + (warp - 2) * 256;
-        float lr = 0.f, alpha_eff = ep.alpha;
-        if (ep.mode == EPI_GRAD_SGD) {
-            lr = ep.lr[ep.step ? *ep.step : 0];
-            if (ep.coef) alpha_eff = ep.alpha * ep.coef[0];
-            if (ep.gscale_a) alpha_eff = static_cast<float>(ep.alpha * *ep.gscale_a * *ep.gscale_b);
-        }
+        auto sgd_scalars = [](const GemmEpi& e, float& lr_, float& alpha_) {
+            lr_ = 0.f;
+            alpha_ = e.alpha;
+            if (e.mode == EPI_GRAD_SGD) {
+                lr_ = e.lr[e.step ? *e.step : 0];
+                if (e.coef) alpha_ = e.alpha * e.coef[0];
+                if (e.gscale_a) alpha_ = static_cast<float>(e.alpha * *e.gscale_a * *e.gscale_b);
+            }
+        };
+        float lr, alpha_eff;
+        sgd_scalars(ep, lr, alpha_eff);
         bool bad = false;
         float s_aux = 0.f, s_out = 0.f;  // RESID sums (per thread, this CTA's tiles)
         int local = 0;
         for (int tile = w0; tile < tiles; tile += wstep) {
-            int m0, n0;
-            tile_mn(tile, m0, n0);
-            if (tile_skipped(m0, n0)) continue;
-            const int ks = tile / tiles_mn;
+            const TileInfo ti = select(tile);
+            if (ti.skip) continue;
+            const int m0 = ti.m0, n0 = ti.n0, ks = ti.ks;
+            // this tile's problem (grouped launches); the names shadow problem 0's
+            const GemmEpi& ep = P.ep[ti.p];
+            const int M = ti.M, N = ti.N;
+            if constexpr (NP > 1) sgd_scalars(ep, lr, alpha_eff);
             const int acc = local & 1;
             const int row = m0 + quad * 32 + lane;
             const bool row_ok = row < M;
@@ -815,6 +916,9 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                 if (row_ok && n < N) xhave = rows_x_fetch<T>(ep, row, n, min(32, N - n), xraw);
             }
             mbar_wait_sleep(&tfull[acc], (local >> 1) & 1);
+            // the mainloop of this CTA's first tile is done: the next kernel may
+            // start its prologue on the SMs that free up
+            if (local == 0) grid_dep_launch();
             if (warp == 2 && lane == 0) PNB_TRACE(4);
             tc_fence_after();
             // Exchange buffers in the idle ring, one contiguous region per epilogue warp
@@ -873,13 +977,19 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     bad |= epilogue_chunk<T, SPLIT ? 4 : 8>(ep, r, ebuf, lane, m0 + quad * 32, M, n, N, lr, alpha_eff,
                                                             ks, s_aux, s_out);
                 } else if (row_ok) {
+                    // next chunk of this warp: its x loads are issued before this chunk's
+                    // math and stores, so their latency overlaps them
+                    const int nn = n + 64;
+                    uint4 xnext[8];
+                    const bool nhave =
+                        nn < N && c + 2 < c_end && rows_x_fetch<T>(ep, row, nn, min(32, N - nn), xnext);
                     float v[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
                     epilogue_chunk_rows<T>(ep, v, row, n, min(32, N - n), xraw, xhave, s_aux, s_out);
-                    // next chunk of this warp: its x loads overlap the next TMEM load
-                    const int nn = n + 64;
-                    xhave = nn < N && c + 2 < c_end && rows_x_fetch<T>(ep, row, nn, min(32, N - nn), xraw);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) xraw[i] = xnext[i];
+                    xhave = nhave;
                 }
             }
             tc_fence_before();
@@ -891,6 +1001,10 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
             }
             if (warp == 2 && lane == 0) PNB_TRACE(5);
             ++local;
+            if constexpr (NP > 1) {  // each problem has its own non-finite flag bit
+                if (bad && ep.flag) atomicOr(ep.flag, 1u << ep.flag_bit);
+                bad = false;
+            }
         }
         if (bad && ep.flag) atomicOr(ep.flag, 1u << ep.flag_bit);
         if (ep.mode == EPI_RESID) {
@@ -921,12 +1035,9 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
         const int t = threadIdx.x - 320;
         int it = 0;
         for (int tile = w0; tile < tiles; tile += wstep) {
-            int m0, n0;
-            tile_mn(tile, m0, n0);
-            if (tile_skipped(m0, n0)) continue;
-            int kb0, kb1;
-            krange(tile, kb0, kb1);
-            for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            const TileInfo ti = select(tile);
+            if (ti.skip) continue;
+            for (int kb = ti.kb0; kb < ti.kb1; ++kb, ++it) {
                 const int s = it % STAGES;
                 mbar_wait(&full[s], (it / STAGES) & 1);
                 float4* hi = reinterpret_cast<float4*>(smem + s * S::kStage);

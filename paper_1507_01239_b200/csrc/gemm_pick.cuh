@@ -11,7 +11,8 @@
 
 namespace pnb {
 
-using KernelFn = void (*)(CUtensorMap, CUtensorMap, int, int, int, GemmEpi);
+using KernelFn = void (*)(GemmParams<1>);
+using GroupKernelFn = void (*)(GemmParams<kGroupMax>);
 
 namespace gemm_pick_detail {
 
@@ -25,7 +26,7 @@ template <typename T, int BN, bool AMN, bool BMN, bool SPLIT, bool TE, int MC>
 KernelFn kernel_ptr(int* smem) {
     constexpr int ST = stages_for<BN, SPLIT>();
     *smem = GemmSmem<BN, ST, T, SPLIT, TE>::kBytes;
-    auto k = &gemm_tc_kernel<T, BN, ST, AMN, BMN, SPLIT, TE, MC>;
+    auto k = &gemm_tc_kernel<T, BN, ST, AMN, BMN, SPLIT, TE, MC, 1>;
     ensure_smem_attr(reinterpret_cast<const void*>(k), *smem);
     return reinterpret_cast<KernelFn>(k);
 }
@@ -66,6 +67,9 @@ KernelFn gemm_pick_bf16_r_mc(int bn, bool amn, bool bmn, int* smem);  // CTA pai
 KernelFn gemm_pick_bf16_t_mc(int bn, bool amn, bool bmn, int* smem);
 KernelFn gemm_pick_bf16_r_sk(int bn, bool amn, bool bmn, int* smem);  // split-K CTA pairs (DSMEM exchange)
 KernelFn gemm_pick_bf16_t_sk(int bn, bool amn, bool bmn, int* smem);
+// grouped launches (gemm_k_group.cu): bf16, BN = 256, both operands MN-major,
+// transposed epilogue, single-CTA tiles -- the trainer's dW GEMMs
+GroupKernelFn gemm_pick_group_dw(int* smem);
 
 #define PNB_GEMM_PICK(name, T, SPLIT, TE, MC)                                 \
     KernelFn gemm_pick_##name(int bn, bool amn, bool bmn, int* smem) {        \

@@ -22,9 +22,13 @@ __device__ __forceinline__ float to_f<bf16>(bf16 v) {
 
 // Dataset::select / minibatches row gather (data.cpp:12-25, 185-203): one
 // CTA per batch row, 16-byte vector copies (rows are 128-B aligned, zero padded).
+// Row b of the batch <- dataset row rows[step * B + b] (Dataset::select,
+// data.cpp:12-25). ones_col >= 0: that column of the output row is set to 1
+// (the constant input whose dW column is the bias gradient, runtime.cu).
 __global__ void gather_kernel(const uint4* __restrict__ x, long ldx_v, const int32_t* __restrict__ y,
                               const uint32_t* __restrict__ rows, const int* __restrict__ step, long B,
-                              long nvec, uint4* __restrict__ out, long ldo_v, int32_t* __restrict__ yout) {
+                              long nvec, uint4* __restrict__ out, long ldo_v, int32_t* __restrict__ yout,
+                              long ones_col, int esz) {
     const long b = blockIdx.x;
     const long st = step ? *step : 0;
     const uint32_t src = rows[st * B + b];
@@ -32,6 +36,22 @@ __global__ void gather_kernel(const uint4* __restrict__ x, long ldx_v, const int
     uint4* o = out + b * ldo_v;
     for (long j = threadIdx.x; j < nvec; j += blockDim.x) o[j] = xs[j];
     if (threadIdx.x == 0) yout[b] = y[src];
+    if (ones_col >= 0) {
+        __syncthreads();  // the vector holding column ones_col is written
+        if (threadIdx.x == 0) {
+            char* row = reinterpret_cast<char*>(o);
+            if (esz == 4) reinterpret_cast<float*>(row)[ones_col] = 1.f;
+            else reinterpret_cast<__nv_bfloat16*>(row)[ones_col] = __float2bfloat16_rn(1.f);
+        }
+    }
+}
+
+// column `col` of a [rows x ld] buffer (fp32 / bf16) <- 1
+__global__ void fill_ones_column_kernel(void* buf, long ld, long rows, long col, int esz) {
+    for (long r = blockIdx.x * (long)blockDim.x + threadIdx.x; r < rows; r += (long)gridDim.x * blockDim.x) {
+        if (esz == 4) static_cast<float*>(buf)[r * ld + col] = 1.f;
+        else static_cast<__nv_bfloat16*>(buf)[r * ld + col] = __float2bfloat16_rn(1.f);
+    }
 }
 
 __device__ __forceinline__ float block_reduce_max(float v, float* sh) {
@@ -252,11 +272,16 @@ __global__ void argmax_correct_kernel(const float* __restrict__ z, long ldz, lon
 }  // namespace
 
 void launch_gather(const void* x, long ldx, const int32_t* y, const uint32_t* rows, const int* step, long B, long d,
-                   void* out, long ldo, int32_t* yout, bool f32, cudaStream_t s) {
+                   void* out, long ldo, int32_t* yout, bool f32, cudaStream_t s, long ones_col) {
     const long per = f32 ? 4 : 8;  // elements per uint4
     const long nvec = (pad32(d) + per - 1) / per;
     gather_kernel<<<B, 128, 0, s>>>(static_cast<const uint4*>(x), ldx / per, y, rows, step, B, nvec,
-                                    static_cast<uint4*>(out), ldo / per, yout);
+                                    static_cast<uint4*>(out), ldo / per, yout, ones_col, f32 ? 4 : 2);
+}
+
+void launch_fill_ones_column(void* buf, long ld, long rows, long col, bool f32, cudaStream_t s) {
+    fill_ones_column_kernel<<<static_cast<int>(std::min<long>((rows + 255) / 256, 1024)), 256, 0, s>>>(
+        buf, ld, rows, col, f32 ? 4 : 2);
 }
 
 void launch_softmax_ce(const float* z, long ldz, long B, long C, const int32_t* y, void* dz, long lddz,

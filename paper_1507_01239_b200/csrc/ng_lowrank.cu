@@ -523,38 +523,68 @@ __global__ void lr_split_kernel(const float* __restrict__ w, long n, long rstrid
 }
 
 
-// W' = M [J; W] per 32-column chunk into the next-W buffers (fp32 + bf16 hi/lo
-// operand copy); the commit copies them over W.
+// W' = M [J; W] per 64-column chunk into the next-W buffers (fp32 + bf16 hi/lo
+// operand copy); the commit copies them over W. The chunk's 2R x 64 slice of
+// [J; W] and M^T (2R x Rp, zero-padded rows) sit in shared memory; thread
+// (column c, group g) accumulates rows [g q, (g+1) q) of its column in
+// registers, reading M^T as broadcast float4s: 1 + q/4 shared loads per q FMAs.
 template <typename T>
 __global__ void __launch_bounds__(256) lr_wupdate_kernel(const float* __restrict__ YW, long ldY, int R, long D,
                                                          const float* __restrict__ M, float* __restrict__ wn,
                                                          T* __restrict__ wop) {
     extern __shared__ float smf[];
     const int R2 = 2 * R;
-    float* Ms = smf;             // [R][2R]
-    float* Ys = Ms + R * R2;     // [2R][32]
-    const long c0 = blockIdx.x * 32L;
+    const int q = ((R + 3) / 4 + 3) & ~3;  // rows per group, a multiple of 4 (<= 24 for R <= 96)
+    const int Rp = 4 * q;
+    float* Mt = smf;              // [2R][Rp]: Mt[j][k] = M[k][j], 0 for k >= R
+    float* Ys = Mt + R2 * Rp;     // [2R][64]
+    const long c0 = blockIdx.x * 64L;
     const int t = threadIdx.x;
-    for (int i = t; i < R * R2; i += blockDim.x) Ms[i] = M[i];
-    for (int i = t; i < R2 * 32; i += blockDim.x) {
-        const int r = i >> 5, c = i & 31;
-        Ys[i] = (c0 + c < D) ? YW[r * ldY + c0 + c] : 0.f;
+    for (int i = t; i < R2 * Rp; i += blockDim.x) {
+        const int j = i / Rp, k = i - j * Rp;
+        Mt[i] = k < R ? M[k * R2 + j] : 0.f;
+    }
+    for (int i = t; i < R2 * 64; i += blockDim.x) {
+        const int j = i >> 6, c = i & 63;
+        Ys[i] = (c0 + c < D) ? YW[j * ldY + c0 + c] : 0.f;
     }
     __syncthreads();
-    const int c = t & 31, rg = t >> 5;
+    const int c = t & 63, g = t >> 6;
     if (c0 + c >= D) return;
-    for (int k = rg; k < R; k += 8) {
-        float acc = 0.f;
-        const float* mk = Ms + k * R2;
-#pragma unroll 8
-        for (int j = 0; j < R2; ++j) acc = fmaf(mk[j], Ys[j * 32 + c], acc);
-        wn[k * ldY + c0 + c] = acc;
-        if (wop) {  // bf16: W_hi and W_lo = W - W_hi
-            const T hi = from_f<T>(acc);
-            wop[k * ldY + c0 + c] = hi;
-            wop[(R + k) * ldY + c0 + c] = from_f<T>(acc - to_f<T>(hi));
+    float acc[24];
+#pragma unroll
+    for (int i = 0; i < 24; ++i) acc[i] = 0.f;
+    for (int j = 0; j < R2; ++j) {
+        const float y = Ys[j * 64 + c];
+        const float4* mj = reinterpret_cast<const float4*>(Mt + j * Rp + g * q);
+#pragma unroll
+        for (int i4 = 0; i4 < 6; ++i4) {
+            if (4 * i4 < q) {
+                const float4 mv = mj[i4];
+                acc[4 * i4] = fmaf(mv.x, y, acc[4 * i4]);
+                acc[4 * i4 + 1] = fmaf(mv.y, y, acc[4 * i4 + 1]);
+                acc[4 * i4 + 2] = fmaf(mv.z, y, acc[4 * i4 + 2]);
+                acc[4 * i4 + 3] = fmaf(mv.w, y, acc[4 * i4 + 3]);
+            }
         }
     }
+#pragma unroll
+    for (int i = 0; i < 24; ++i) {
+        const int k = g * q + i;
+        if (i < q && k < R) {
+            wn[k * ldY + c0 + c] = acc[i];
+            if (wop) {  // bf16: W_hi and W_lo = W - W_hi
+                const T hi = from_f<T>(acc[i]);
+                wop[k * ldY + c0 + c] = hi;
+                wop[(R + k) * ldY + c0 + c] = from_f<T>(acc[i] - to_f<T>(hi));
+            }
+        }
+    }
+}
+
+size_t wupdate_smem(int R) {
+    const int q = ((R + 3) / 4 + 3) & ~3;
+    return (static_cast<size_t>(2 * R) * 4 * q + 2 * R * 64) * sizeof(float);
 }
 
 int lr_rank(int want, long dim) { return static_cast<int>(std::max<long>(1, std::min<long>(want, dim - 1))); }
@@ -589,7 +619,8 @@ void side_alloc(Replica& r, LrSide& sd, bool in, long dx, int want_rank, int lay
     sd.wopn = r.f32() ? nullptr : valloc(2 * R * sd.ldY * 2);
     sd.M = falloc(2L * R * R);
     sd.xhat = valloc(B * sd.ldxh * es);
-    CUDA_THROW(cudaStreamCreateWithFlags(&sd.stream, cudaStreamNonBlocking));
+    // out-side chains gate the weight update at the end of the step; in-side chains run beside the forward
+    sd.stream = make_stream(in ? 1 : 0);
     CUDA_THROW(cudaEventCreateWithFlags(&sd.ready, cudaEventDisableTiming));
     CUDA_THROW(cudaEventCreateWithFlags(&sd.done, cudaEventDisableTiming));
     // initial state: d = rho = eps, e = d / (d + beta), W = E^1/2 R0
@@ -766,7 +797,7 @@ void lr_free(Replica& r) {
 void lr_build_plans(Replica& r) {
     {
         ensure_smem_attr(reinterpret_cast<const void*>(lr_eig_kernel), static_cast<int>(eig_smem(LR_MAX_RANK)));
-        const int ws = (LR_MAX_RANK * 2 * LR_MAX_RANK + 2 * LR_MAX_RANK * 32) * 4;
+        const int ws = static_cast<int>(wupdate_smem(LR_MAX_RANK));
         ensure_smem_attr(reinterpret_cast<const void*>(lr_wupdate_kernel<float>), ws);
         ensure_smem_attr(reinterpret_cast<const void*>(lr_wupdate_kernel<bf16>), ws);
     }
@@ -816,9 +847,8 @@ void lr_apply_update(Replica& r, LrSide& sd, cudaStream_t s) {
     const int ethreads = std::max(64, 32 * (nblk / 2));  // one warp per block pair
     lr_eig_kernel<<<1, ethreads, eig_smem(sd.R), s>>>(sd.st, sd.trxx_snap, sd.stn, sd.gram, sd.R, sd.D, eta, a,
                                                       r.lrc.alpha, sd.M, 40);
-    const int R2 = 2 * sd.R;
-    const size_t ws = (static_cast<size_t>(sd.R) * R2 + R2 * 32) * 4;
-    const unsigned grid = static_cast<unsigned>((sd.D + 31) / 32);
+    const size_t ws = wupdate_smem(sd.R);
+    const unsigned grid = static_cast<unsigned>((sd.D + 63) / 64);
     if (r.f32())
         lr_wupdate_kernel<float><<<grid, 256, ws, s>>>(sd.YW, sd.ldY, sd.R, sd.D, sd.M, sd.Wn, nullptr);
     else

@@ -171,6 +171,9 @@ Averager::Averager(Context* c, const std::vector<Replica*>& r, Comm* cm, long m)
     CUDA_THROW(cudaMemcpy(d_src, src.data(), k * sizeof(float*), cudaMemcpyHostToDevice));
     CUDA_THROW(cudaMemcpy(d_shadow, sh.data(), k * sizeof(bf16*), cudaMemcpyHostToDevice));
     CUDA_THROW(cudaMemset(d_null_shadow, 0, sizeof(bf16*)));
+    work = comm != nullptr || k > 1;
+    if (work)
+        for (Replica* p : reps) p->precapture_gates();
     if (comm && k > 1) {
         CUDA_THROW(cudaMalloc(&scratch, n * sizeof(float)));
         CUDA_THROW(cudaMalloc(&d_scratch_ptr, sizeof(float*)));
@@ -200,25 +203,35 @@ void Averager::run() {
     const AvgFn fk = vec_ok ? avg4_pick(k, std::make_integer_sequence<int, 32>{}) : nullptr;
     const AvgFn f1 = vec_ok ? avg4_pick(1, std::make_integer_sequence<int, 32>{}) : nullptr;
     ncclComm_t cm = comm ? static_cast<ncclComm_t>(comm->comm) : nullptr;
-    // m == 1 without a communicator: x * 1.0 is the identity (parallel.cpp:56-57);
-    // the gates are still recorded so the protocol is the same.
-    const bool work = comm || k > 1;
+    // m == 1 without a communicator: x * 1.0 is the identity (parallel.cpp:56-57)
+    if (!work) {
+        for (Replica* r : reps) r->last_recorded = false;
+        return;
+    }
+    // a replica whose last step was not launched as a window end (GATE_REC) has no
+    // per-layer update events: wait for the whole step instead
+    for (Replica* r : reps)
+        if (!r->last_recorded) {
+            CUDA_THROW(cudaEventRecord(r->ev_tail, r->stream));
+            CUDA_THROW(cudaStreamWaitEvent(s, r->ev_tail, 0));
+        }
     for (int l = L - 1; l >= 0; --l) {
-        for (Replica* r : reps) CUDA_THROW(cudaStreamWaitEvent(s, r->ev_upd[l], 0));
+        for (Replica* r : reps)
+            if (r->last_recorded) CUDA_THROW(cudaStreamWaitEvent(s, r->ev_upd[l], 0));
         const long off = reps[0]->bucket_begin(l), len = reps[0]->bucket_end(l) - off;
         const int grid = static_cast<int>(std::min<long>(ctx->num_sms * 8L, std::max<long>(1, (len / 4 + 255) / 256)));
-        if (work && !comm) {
+        if (!comm) {
             // local midpoint tree over the replicas x 1/m -> every replica (+ bf16 copy)
             if (fk) fk<<<grid, 256, 0, s>>>(d_src, off, len, inv, 1, d_src, d_shadow, k);
             else tree_avg_kernel<<<grid, 256, 0, s>>>(d_src, k, off, len, inv, 1, d_src, d_shadow, k);
-        } else if (work && k == 1) {
+        } else if (k == 1) {
             // one replica per GPU: in-place ncclAvg fuses the 1/m scale into the collective
             NCCL_THROW(ncclAllReduce(reps[0]->params + off, reps[0]->params + off, len, ncclFloat, ncclAvg, cm, s));
             if (reps[0]->wshadow) {
                 if (f1) f1<<<grid, 256, 0, s>>>(d_src, off, len, 1.f, 0, d_src, d_shadow, 1);
                 else tree_avg_kernel<<<grid, 256, 0, s>>>(d_src, 1, off, len, 1.f, 0, d_src, d_shadow, 1);
             }
-        } else if (work) {
+        } else {
             // local subtree sum -> scratch (no shadow), NCCL sum over GPUs, then the
             // fused scale pass: scratch x 1/m -> every local replica and its bf16 copy
             if (fk) fk<<<grid, 256, 0, s>>>(d_src, off, len, 1.f, 0, d_scratch_ptr, d_null_shadow, 1);
@@ -228,6 +241,10 @@ void Averager::run() {
             else tree_avg_kernel<<<grid, 256, 0, s>>>(d_scratch_ptr, 1, off, len, inv, 1, d_src, d_shadow, k);
         }
         for (Replica* r : reps) CUDA_THROW(cudaEventRecord(r->ev_gate[l], s));
+    }
+    for (Replica* r : reps) {
+        r->gate_pending = true;  // the next step waits on the gates
+        r->last_recorded = false;
     }
     CUDA_THROW(cudaGetLastError());
 }

@@ -36,6 +36,7 @@ struct Averager {
     bf16** d_null_shadow = nullptr;  // one null shadow pointer: the unscaled partial sum has none
     float* scratch = nullptr;
     float** d_scratch_ptr = nullptr;
+    bool work = false;  // false: one local replica, no communicator, m = 1 -- the identity
     Averager(Context* c, const std::vector<Replica*>& reps, Comm* comm, long m_total);
     ~Averager();
     void run();

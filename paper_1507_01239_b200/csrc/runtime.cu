@@ -1,5 +1,6 @@
 // Contexts, device-resident datasets and replicas; the fused minibatch step
 // (worker_epoch's body, parallel.cpp:117-130) as one CUDA graph.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -63,6 +64,15 @@ void record_ext(cudaEvent_t e, cudaStream_t s) {
         CUDA_THROW(cudaEventRecord(e, s));
 }
 
+cudaStream_t make_stream(int level) {
+    int least = 0, greatest = 0;
+    CUDA_THROW(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    const int prio = level <= 0 ? greatest : (level >= 2 ? least : (least + greatest) / 2);
+    cudaStream_t s;
+    CUDA_THROW(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio));
+    return s;
+}
+
 // Kernel nodes of a captured graph (event record / wait and memcpy nodes are not kernels).
 long count_kernel_nodes(cudaGraph_t g) {
     size_t n = 0;
@@ -88,7 +98,7 @@ Context::Context(int dev) : device(dev) {
     CUDA_THROW(cudaSetDevice(dev));
     CUDA_THROW(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     CUDA_THROW(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    CUDA_THROW(cudaStreamCreateWithFlags(&avg, cudaStreamNonBlocking));
+    avg = make_stream(0);  // the next steps' forwards wait on its gates
 }
 
 Context::~Context() {
@@ -147,8 +157,8 @@ Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision
         if (d <= 0) throw std::runtime_error("replica: zero layer dimension");
     if (B <= 0) throw std::runtime_error("replica: minibatch must be >= 1");
     CUDA_THROW(cudaSetDevice(c->device));
-    CUDA_THROW(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    CUDA_THROW(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    stream = make_stream(0);  // the forward / dz chain: the step's critical path
+    side = make_stream(1);
     CUDA_THROW(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
     L = static_cast<int>(dims.size()) - 1;
     ev_bwd.resize(L);
@@ -161,6 +171,7 @@ Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision
         CUDA_THROW(cudaEventCreateWithFlags(&ev_upd[l], cudaEventDisableTiming));
         CUDA_THROW(cudaEventCreateWithFlags(&ev_gate[l], cudaEventDisableTiming));
     }
+    CUDA_THROW(cudaEventCreateWithFlags(&ev_tail, cudaEventDisableTiming));
     long off = 0;
     for (int l = 0; l < L; ++l) {
         ldw.push_back(pad32(dims[l]));
@@ -174,8 +185,13 @@ Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision
     if (!f32()) wshadow = dalloc<bf16>(n_pad);
     if (opt == OPT_NG_KRON) grads = dalloc<float>(n_pad);
     if (opt == OPT_NG_LOWRANK) lrc.alpha = ng_smoothing;
-    for (int l = 0; l <= L; ++l) ld_act.push_back(pad32(dims[l]));
+    bias_in_dw = !f32() && opt == OPT_SGD;
+    for (int l = 0; l <= L; ++l) ld_act.push_back(pad32(dims[l] + (bias_in_dw && l < L ? 1 : 0)));
     for (int l = 0; l < L; ++l) acts.push_back(f32() ? (void*)dalloc<float>(B * ld_act[l]) : (void*)dalloc<bf16>(B * ld_act[l]));
+    if (bias_in_dw) {  // the constant-1 column of every layer input (acts[0]'s is set by each gather)
+        for (int l = 1; l < L; ++l) launch_fill_ones_column(acts[l], ld_act[l], B, dims[l], false, stream);
+        CUDA_THROW(cudaStreamSynchronize(stream));
+    }
     acts.push_back(nullptr);  // the last layer keeps Z (fp32) in zout
     zout = dalloc<float>(B * ld_act[L]);
     for (int l = 0; l < L; ++l)
@@ -206,7 +222,6 @@ Replica::Replica(Context* c, const std::vector<long>& dims_, int act_, Precision
 
 Replica::~Replica() {
     if (stream) cudaStreamSynchronize(stream);
-    if (graph) cudaGraphExecDestroy(graph);
     if (bg) cudaStreamSynchronize(bg);
     for (auto g : vgraphs)
         if (g) cudaGraphExecDestroy(g);
@@ -242,6 +257,7 @@ Replica::~Replica() {
     for (auto e : ev_dw) cudaEventDestroy(e);
     for (auto e : ev_upd) cudaEventDestroy(e);
     for (auto e : ev_gate) cudaEventDestroy(e);
+    if (ev_tail) cudaEventDestroy(ev_tail);
     if (ev_side) cudaEventDestroy(ev_side);
     if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
@@ -335,6 +351,13 @@ void Replica::bind(DeviceDataset* ds) {
     mom_in.assign(L, GemmPlan());
     mom_out.assign(L, GemmPlan());
     float* coef = reinterpret_cast<float*>(scal + 16 * (L + 1) + 480);
+    static const bool no_group = [] {
+        const char* v = std::getenv("PARNN_NO_DW_GROUP");
+        return v && v[0] == '1';
+    }();
+    // bf16 dW plans use the group's tile shape (BN = 256) even when launched per layer,
+    // so both launch forms compute identical tiles (tests/test_gpu.py)
+    const bool group_dw = !F && (opt == OPT_SGD || opt == OPT_NG_LOWRANK) && L <= kGroupMax;
     for (int l = 0; l < L; ++l) {
         const long din = dims[l], dout = dims[l + 1];
         const void* W = F ? static_cast<const void*>(params + w_off[l]) : static_cast<const void*>(wshadow + w_off[l]);
@@ -379,9 +402,17 @@ void Replica::bind(DeviceDataset* ds) {
             g.gscale_b = so.st + 2 * so.R + 2;
             g.bias_col = static_cast<int>(din);
             g.bias32 = params + b_off[l];
-            gemm_plan(dw[l], prec, true, so.xhat, so.ldxh, true, si.xhat, si.ldxh, dout, din + 1, B, g, sms);
+            gemm_plan(dw[l], prec, true, so.xhat, so.ldxh, true, si.xhat, si.ldxh, dout, din + 1, B, g, sms,
+                      group_dw ? 256 : 0);
+        } else if (bias_in_dw) {
+            // [dW | db] = dz^T [A_prev | 1] / B: the ones column's output is the bias gradient
+            g.bias_col = static_cast<int>(din);
+            g.bias32 = params + b_off[l];
+            gemm_plan(dw[l], prec, true, dz[l], ld_act[l + 1], true, acts[l], ld_act[l], dout, din + 1, B, g, sms,
+                      group_dw ? 256 : 0);
         } else {
-            gemm_plan(dw[l], prec, true, dz[l], ld_act[l + 1], true, acts[l], ld_act[l], dout, din, B, g, sms);
+            gemm_plan(dw[l], prec, true, dz[l], ld_act[l + 1], true, acts[l], ld_act[l], dout, din, B, g, sms,
+                      group_dw ? 256 : 0);
         }
 
         if (l > 0) {
@@ -407,21 +438,25 @@ void Replica::bind(DeviceDataset* ds) {
             gemm_plan(mom_out[l], prec, true, dz[l], ld_act[l + 1], true, dz[l], ld_act[l + 1], dout, dout, B, m, sms);
         }
     }
+    dw_group = group_dw && !no_group;
+    if (dw_group) {
+        std::vector<const GemmPlan*> parts;
+        for (int l = L - 1; l >= 0; --l) parts.push_back(&dw[l]);  // the largest (output) layer first
+        for (auto* p : parts) dw_group = dw_group && gemm_groupable(*p);
+        if (dw_group) gemm_group_plan(dwg, parts, sms);
+    }
     if (opt == OPT_NG_KRON) ng_build_plans(*this);
     if (opt == OPT_NG_LOWRANK) lr_build_plans(*this);
-    if (graph) {
-        cudaGraphExecDestroy(graph);
-        graph = nullptr;
-    }
+    graph = nullptr;  // an alias of vgraphs[0] (destroyed below)
     for (auto& g : vgraphs)
         if (g) {
             cudaGraphExecDestroy(g);
             g = nullptr;
         }
-    vgraphs.assign(32, nullptr);
-    vnodes.assign(32, 0);
+    vgraphs.assign(kVariants, nullptr);
+    vnodes.assign(kVariants, 0);
     if (opt == OPT_NG_LOWRANK && !bg) {
-        CUDA_THROW(cudaStreamCreateWithFlags(&bg, cudaStreamNonBlocking));
+        bg = make_stream(2);  // background subspace updates fill the gaps
         CUDA_THROW(cudaEventCreateWithFlags(&ev_jdone, cudaEventDisableTiming));
         CUDA_THROW(cudaEventCreateWithFlags(&ev_applied, cudaEventDisableTiming));
     }
@@ -434,22 +469,6 @@ void Replica::bind(DeviceDataset* ds) {
         for (auto& e : tl_pool) CUDA_THROW(cudaEventCreate(&e));
     }
     if (use_graph) {
-        auto capture = [&](int v, cudaGraphExec_t* out, long* nodes_out) {
-            variant = v;
-            cudaStream_t s = stream;
-            cudaGraph_t g;
-            CUDA_THROW(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-            try {
-                enqueue_step(s);
-            } catch (...) {
-                cudaStreamEndCapture(s, &g);
-                throw;
-            }
-            CUDA_THROW(cudaStreamEndCapture(s, &g));
-            *nodes_out = count_kernel_nodes(g);
-            CUDA_THROW(cudaGraphInstantiate(out, g, 0));
-            cudaGraphDestroy(g);
-        };
         if (opt == OPT_NG_LOWRANK) {
             // one graph per step kind (captured here for the first two update periods,
             // others on first use); kernels_per_step = average over one period
@@ -468,7 +487,9 @@ void Replica::bind(DeviceDataset* ds) {
             if (lr_lag() >= 2) sum += apply_nodes;
             kernels_per_step = sum / P;
         } else {
-            capture(0, &graph, &kernels_per_step);
+            capture_variant(0);  // the plain step; gated variants are captured on first use
+            graph = vgraphs[0];
+            kernels_per_step = vnodes[0];
         }
     }
 }
@@ -487,9 +508,25 @@ void Replica::capture_variant(int v) {
     }
     CUDA_THROW(cudaStreamEndCapture(stream, &g));
     vnodes[v] = count_kernel_nodes(g);
-    CUDA_THROW(cudaGraphInstantiate(&vgraphs[v], g, 0));
+    CUDA_THROW(cudaGraphInstantiate(&vgraphs[v], g, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(g);
     variant = saved;
+}
+
+void Replica::precapture_gates() {
+    if (!use_graph || !bound) return;
+    std::vector<int> base{0};
+    if (opt == OPT_NG_LOWRANK) {
+        base.clear();
+        const int P = std::max(1, lrc.update_period);
+        for (long t = 0; t < 3 * P + 3; ++t) {
+            const int v = lr_variant(t);
+            if (std::find(base.begin(), base.end(), v) == base.end()) base.push_back(v);
+        }
+    }
+    for (int b : base)
+        for (int g : {static_cast<int>(GATE_WAIT), static_cast<int>(GATE_REC), GATE_WAIT | GATE_REC})
+            if (!vgraphs[b | g]) capture_variant(b | g);
 }
 
 // lag >= 2 low-rank updates: the step that commits a background update waits for it
@@ -540,7 +577,7 @@ void Replica::capture_apply_graph() {
     }
     CUDA_THROW(cudaStreamEndCapture(bg, &g));
     apply_nodes = count_kernel_nodes(g);
-    CUDA_THROW(cudaGraphInstantiate(&apply_graph, g, 0));
+    CUDA_THROW(cudaGraphInstantiate(&apply_graph, g, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(g);
 }
 
@@ -635,7 +672,7 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
                       r.ld_act[0], r.d_ybatch, F, s);
         r.mark("gather", 0, 0, s);
         for (int l = 0; l < L; ++l) {
-            wait_ext(s, r.ev_gate[l]);
+            if (r.variant & GATE_WAIT) wait_ext(s, r.ev_gate[l]);
             gemm_launch(r.fwd[l], s);
             r.mark("gemm_fwd", l, gf(r.fwd[l]), s);
         }
@@ -645,13 +682,22 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
             gemm_launch(r.da[l], s);
             r.mark("gemm_da", l, gf(r.da[l]), s);
         }
+        double dwf = 0.0;
         for (int l = L - 1; l >= 0; --l) {
             lr_side_chain(r, r.lrl[l].in, nullptr, s);
             lr_side_chain(r, r.lrl[l].out, nullptr, s);
             r.mark("ng_lr_precondition", l, 0, s);
+            dwf += gf(r.dw[l]);
+            if (r.dw_group) continue;
             lr_layer_update(r, l, s);
-            record_ext(r.ev_upd[l], s);
+            if (r.variant & GATE_REC) record_ext(r.ev_upd[l], s);
             r.mark("gemm_dw_sgd", l, gf(r.dw[l]), s);
+        }
+        if (r.dw_group) {
+            gemm_group_launch(r.dwg, s);
+            if (r.variant & GATE_REC)
+                for (int l = 0; l < L; ++l) record_ext(r.ev_upd[l], s);
+            r.mark("gemm_dw_sgd", -1, dwf, s);  // all layers, one grouped launch
         }
     } else {
         static const bool serial = std::getenv("PARNN_LR_SERIAL") != nullptr;  // debugging: one stream
@@ -673,7 +719,7 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
         CUDA_THROW(cudaEventRecord(r.ev_act[0], s));
         if (!in_late) lr_side_chain(r, r.lrl[0].in, r.ev_act[0], S(r.lrl[0].in.stream));
         for (int l = 0; l < L; ++l) {
-            wait_ext(s, r.ev_gate[l]);  // layer l's average (if one is pending) is done
+            if (r.variant & GATE_WAIT) wait_ext(s, r.ev_gate[l]);  // layer l's pending average is done
             gemm_launch(r.fwd[l], s);
             if (l + 1 < L) {
                 CUDA_THROW(cudaEventRecord(r.ev_act[l + 1], s));
@@ -691,7 +737,20 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
             CUDA_THROW(cudaEventRecord(r.ev_bwd[l], s));  // W_l read; dz[l-1] ready
             if (l > 0) lr_side_chain(r, r.lrl[l - 1].out, r.ev_bwd[l], S(r.lrl[l - 1].out.stream));
         }
-        for (int l = L - 1; l >= 0; --l) {
+        if (r.dw_group) {
+            // [dW_l | db_l] of every layer in one grouped persistent launch once the dz
+            // chain and every side's preconditioning are done: the epilogues (the fp32
+            // weight read-modify-write) of one layer's tiles overlap the mainloops of others
+            for (int l = 0; l < L; ++l) {
+                CUDA_THROW(cudaStreamWaitEvent(s, r.lrl[l].in.ready, 0));
+                CUDA_THROW(cudaStreamWaitEvent(s, r.lrl[l].out.ready, 0));
+            }
+            gemm_group_launch(r.dwg, s);
+            r.tmark("dw", s);
+            if (r.variant & GATE_REC)
+                for (int l = 0; l < L; ++l) record_ext(r.ev_upd[l], s);
+        }
+        for (int l = L - 1; l >= 0 && !r.dw_group; --l) {
             // [dW_l | db_l] on the layer's input-side stream: the layers' weight updates are
             // independent and overlap each other and the remaining chains (a single side
             // stream made them the step's critical path). They start after the whole dz
@@ -701,7 +760,7 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
             CUDA_THROW(cudaStreamWaitEvent(ws, r.ev_bwd[0], 0));
             CUDA_THROW(cudaStreamWaitEvent(ws, r.lrl[l].out.ready, 0));
             lr_layer_update(r, l, ws);
-            record_ext(r.ev_upd[l], ws);  // layer l final for this step: its average may start
+            if (r.variant & GATE_REC) record_ext(r.ev_upd[l], ws);  // layer l final: its average may start
             r.tmark("dw" + std::to_string(l), ws);
             CUDA_THROW(cudaEventRecord(r.lrl[l].in.done, ws));
         }
@@ -728,10 +787,11 @@ void Replica::enqueue_step(cudaStream_t s) {
     auto gf = [](const GemmPlan& p) { return 2.0 * p.M * p.N * p.K; };
     mark("start", -1, 0, s);
     if (!prof) tmark("t0", s);
-    launch_gather(ds->features(prec), ds->ld, ds->y, d_rows, d_step, B, dims[0], acts[0], ld_act[0], d_ybatch, F, s);
+    launch_gather(ds->features(prec), ds->ld, ds->y, d_rows, d_step, B, dims[0], acts[0], ld_act[0], d_ybatch, F, s,
+                  ones_col0());
     mark("gather", 0, 0, s);
     for (int l = 0; l < L; ++l) {
-        wait_ext(s, ev_gate[l]);  // layer l's average (if one is pending) is done
+        if (variant & GATE_WAIT) wait_ext(s, ev_gate[l]);  // layer l's pending average is done
         gemm_launch(fwd[l], s);
         mark("gemm_fwd", l, gf(fwd[l]), s);
     }
@@ -752,11 +812,14 @@ void Replica::enqueue_step(cudaStream_t s) {
             if (l > 0) gemm_launch(da[l], s);
             CUDA_THROW(cudaEventRecord(ev_bwd[l], s));
             CUDA_THROW(cudaStreamWaitEvent(side, ev_bwd[l], 0));
-            // the bias gradient is off the dz chain: side stream, before dW_l
-            launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
-                             ng ? grads + b_off[l] : nullptr, d_lr, d_step, d_flags, 2 * l + 1, side);
+            // the bias gradient is off the dz chain: side stream, before dW_l (bf16 SGD:
+            // in the dW GEMM's ones column instead)
+            if (!bias_in_dw)
+                launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
+                                 ng ? grads + b_off[l] : nullptr, d_lr, d_step, d_flags, 2 * l + 1, side);
+            if (dw_group) continue;  // every layer's dW below, one grouped launch
             gemm_launch(dw[l], side);
-            if (!ng) record_ext(ev_upd[l], side);  // layer l final for this step
+            if (!ng && (variant & GATE_REC)) record_ext(ev_upd[l], side);  // layer l final for this step
             tmark("dw" + std::to_string(l), side);
             if (ng) {
                 CUDA_THROW(cudaEventRecord(ev_dw[l], side));
@@ -766,13 +829,19 @@ void Replica::enqueue_step(cudaStream_t s) {
                 gemm_launch(mom_out[l], ls);
                 ng_precondition_layer(*this, l, ls);
                 ng_apply_update(*this, l, ls);
-                record_ext(ev_upd[l], ls);
+                if (variant & GATE_REC) record_ext(ev_upd[l], ls);
                 tmark("done" + std::to_string(l), ls);
                 CUDA_THROW(cudaEventRecord(ngl[l].done, ls));
             }
         }
+        // grouped dW + SGD of every layer right behind the dz chain (PDL from the last dA):
+        // one persistent grid, the weight read-modify-write epilogues of one layer's tiles
+        // overlapping the mainloops of the next
+        if (dw_group) gemm_group_launch(dwg, s);
         CUDA_THROW(cudaEventRecord(ev_side, side));
         CUDA_THROW(cudaStreamWaitEvent(s, ev_side, 0));
+        if (dw_group && (variant & GATE_REC))
+            for (int l = 0; l < L; ++l) record_ext(ev_upd[l], s);
         if (ng)
             for (int l = 0; l < L; ++l) CUDA_THROW(cudaStreamWaitEvent(s, ngl[l].done, 0));
         flags_latch_kernel<<<1, 1, 0, s>>>(d_flags, d_step);
@@ -781,16 +850,27 @@ void Replica::enqueue_step(cudaStream_t s) {
         return;
     }
     for (int l = L - 1; l >= 0; --l) {
-        launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
-                         ng ? grads + b_off[l] : nullptr, d_lr, d_step, d_flags, 2 * l + 1, s);
-        mark("bias_grad", l, 0, s);
+        if (!bias_in_dw) {
+            launch_bias_grad(dz[l], ld_act[l + 1], B, dims[l + 1], F, ng ? nullptr : params + b_off[l],
+                             ng ? grads + b_off[l] : nullptr, d_lr, d_step, d_flags, 2 * l + 1, s);
+            mark("bias_grad", l, 0, s);
+        }
         if (l > 0) {
             gemm_launch(da[l], s);  // reads W_l before its update below
             mark("gemm_da", l, gf(da[l]), s);
         }
+        if (dw_group) continue;
         gemm_launch(dw[l], s);
-        if (!ng) record_ext(ev_upd[l], s);
+        if (!ng && (variant & GATE_REC)) record_ext(ev_upd[l], s);
         mark(ng ? "gemm_dw" : "gemm_dw_sgd", l, gf(dw[l]), s);
+    }
+    if (dw_group) {
+        double dwf = 0.0;
+        for (int l = 0; l < L; ++l) dwf += gf(dw[l]);
+        gemm_group_launch(dwg, s);
+        if (variant & GATE_REC)
+            for (int l = 0; l < L; ++l) record_ext(ev_upd[l], s);
+        mark("gemm_dw_sgd", -1, dwf, s);  // all layers, one grouped launch
     }
     if (ng) {
         ng_coeff_kernel<<<1, 1, 0, s>>>(tdev, ng_decay, 1.0 / static_cast<double>(B), coef);
@@ -803,7 +883,7 @@ void Replica::enqueue_step(cudaStream_t s) {
             for (int l = 0; l < L; ++l) {
                 ng_precondition_layer(*this, l, s);
                 ng_apply_update(*this, l, s);
-                record_ext(ev_upd[l], s);
+                if (variant & GATE_REC) record_ext(ev_upd[l], s);
             }
         } else {
             // the layers' NG chains are independent: fork one stream per layer, join
@@ -815,7 +895,7 @@ void Replica::enqueue_step(cudaStream_t s) {
                 gemm_launch(mom_out[l], ls);
                 ng_precondition_layer(*this, l, ls);
                 ng_apply_update(*this, l, ls);
-                record_ext(ev_upd[l], ls);
+                if (variant & GATE_REC) record_ext(ev_upd[l], ls);
                 CUDA_THROW(cudaEventRecord(ngl[l].done, ls));
             }
             for (int l = 0; l < L; ++l) CUDA_THROW(cudaStreamWaitEvent(s, ngl[l].done, 0));
@@ -834,8 +914,11 @@ void Replica::profile_steps(long steps, std::vector<std::string>& names, std::ve
     flops.clear();
     for (long it = 0; it < steps; ++it) {
         Profile p;
+        variant = gate_pending ? GATE_WAIT : 0;
+        gate_pending = false;
+        last_recorded = false;
         if (opt == OPT_NG_LOWRANK) {
-            variant = lr_variant(lr_t++);
+            variant |= lr_variant(lr_t++);
             lr_before_step(stream);
         }
         prof = &p;
@@ -902,7 +985,7 @@ double Replica::step_ce(long j) {
     return v;
 }
 
-void Replica::run_step(cudaStream_t s) {
+void Replica::run_step(cudaStream_t s, bool window_end) {
     if (!bound) throw std::runtime_error("replica: no dataset bound");
     if (epoch_steps >= epoch_len)
         throw std::runtime_error("replica: step " + std::to_string(epoch_steps) + " beyond the " +
@@ -917,10 +1000,14 @@ void Replica::run_step(cudaStream_t s) {
         cudaStream_t s;
         ~Rec() { cudaEventRecord(r->step_ev[r->epoch_steps++ % kStepRing], s); }
     } rec{this, s};
+    const int gating = (gate_pending ? GATE_WAIT : 0) | (window_end ? GATE_REC : 0);
+    gate_pending = false;
+    last_recorded = window_end;
     if (opt == OPT_NG_LOWRANK) {
         variant = lr_variant(lr_t);
         static const char* force = std::getenv("PARNN_LR_FORCE_VARIANT");  // timing aid (LRV_* bits)
         if (force && lr_t > 0) variant = std::atoi(force);
+        variant |= gating;
         lr_before_step(s);
         if (use_graph) {
             if (!vgraphs[variant]) capture_variant(variant);
@@ -932,10 +1019,13 @@ void Replica::run_step(cudaStream_t s) {
         ++lr_t;
         return;
     }
-    if (graph)
-        CUDA_THROW(cudaGraphLaunch(graph, s));
-    else
+    variant = gating;
+    if (use_graph) {
+        if (!vgraphs[variant]) capture_variant(variant);
+        CUDA_THROW(cudaGraphLaunch(vgraphs[variant], s));
+    } else {
         enqueue_step(s);
+    }
 }
 
 void Replica::check_errors() {
@@ -988,7 +1078,7 @@ double Replica::accuracy(DeviceDataset* ds) {
     for (long c0 = 0; c0 < ds->n; c0 += B) {
         const long cb = std::min(B, ds->n - c0);
         launch_gather(ds->features(prec), ds->ld, ds->y, rows + c0, nullptr, cb, dims[0], acts[0], ld_act[0], d_ybatch,
-                      F, s);
+                      F, s, ones_col0());
         for (int l = 0; l < L; ++l) gemm_launch(fwd[l], s);
         launch_argmax_correct(zout, ld_act[L], cb, dims[L], d_ybatch, correct, s);
     }
@@ -1005,7 +1095,8 @@ void Replica::forward_only(DeviceDataset* ds, const uint32_t* rows_h, long b, fl
     uint32_t* rows = dalloc<uint32_t>(b);
     CUDA_THROW(cudaMemcpyAsync(rows, rows_h, b * 4, cudaMemcpyHostToDevice, s));
     for (int l = 0; l < L; ++l) wait_ext(s, ev_gate[l]);
-    launch_gather(ds->features(prec), ds->ld, ds->y, rows, nullptr, b, dims[0], acts[0], ld_act[0], d_ybatch, f32(), s);
+    launch_gather(ds->features(prec), ds->ld, ds->y, rows, nullptr, b, dims[0], acts[0], ld_act[0], d_ybatch, f32(), s,
+                  ones_col0());
     for (int l = 0; l < L; ++l) gemm_launch(fwd[l], s);
     std::vector<float> h(static_cast<size_t>(b * ld_act[L]));
     CUDA_THROW(cudaMemcpyAsync(h.data(), zout, h.size() * 4, cudaMemcpyDeviceToHost, s));

@@ -30,9 +30,24 @@ struct GemmPlan {
     dim3 grid;
     int smem = 0, M = 0, N = 0, K = 0, bn = 0, threads = 128, tiles = 0;
     int mc = 1;  // 2: CTA pairs (clusters of 2) computing 256 x BN tiles with 2-SM MMAs
+    int prec = 0;
+    bool a_mn = false, b_mn = false;
     GemmEpi ep;
     void* fn = nullptr;
 };
+
+// One persistent launch over the problems of several plans -- the step's dW
+// GEMMs (gemm.cuh, NP > 1). Every member: bf16 operands, both MN-major, BN =
+// 256, transposed-epilogue mode, single-CTA tiles, no split-K.
+struct GemmGroupPlan {
+    GemmParams<kGroupMax> args;
+    dim3 grid;
+    int smem = 0, threads = 320, tiles = 0, np = 0;
+    void* fn = nullptr;
+};
+bool gemm_groupable(const GemmPlan& p);
+void gemm_group_plan(GemmGroupPlan& g, const std::vector<const GemmPlan*>& parts, int num_sms);
+void gemm_group_launch(const GemmGroupPlan& g, cudaStream_t s);
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
 // function attributes are per device and the C ABI allows contexts on several
@@ -160,7 +175,11 @@ enum LrVariantBits : int {
     LRV_J = 2,         // compute J of an update at the end of the step
     LRV_APPLY = 4,     // lag 1: compute + commit the pending update at the start of the step
     LRV_COMMIT = 8,    // lag >= 2: commit the update computed in the background
-    LRV_INFLIGHT = 16  // lag >= 2: the background update runs beside this step (GEMM grids capped)
+    LRV_INFLIGHT = 16,  // lag >= 2: the background update runs beside this step (GEMM grids capped)
+    // averaging gates (every optimizer): captured only into the steps that need them
+    GATE_WAIT = 32,  // an average is pending: wait on ev_gate[l] before the forward GEMM of layer l
+    GATE_REC = 64,   // the step ends an averaging window: record ev_upd[l] once layer l is final
+    kVariants = 128
 };
 struct LrLayer {
     LrSide in, out;
@@ -228,12 +247,25 @@ struct Replica {
     // (graph: external wait node) right before its forward GEMM of layer l. So
     // the average of the last layers overlaps the next step's first layers.
     std::vector<cudaEvent_t> ev_upd, ev_gate;
+    cudaEvent_t ev_tail = nullptr;  // end of the last step (averaging after a step launched without GATE_REC)
+    bool gate_pending = false;      // an average was enqueued: the next step waits on the gates
+    bool last_recorded = false;     // the last step recorded ev_upd (GATE_REC)
     long bucket_begin(int l) const { return w_off[l]; }
     long bucket_end(int l) const { return l + 1 < L ? w_off[l + 1] : n_pad; }
 
     DeviceDataset* bound = nullptr;  // dataset the plans/graph were built for
     std::vector<GemmPlan> fwd, dw, da, mom_in, mom_out;
-    cudaGraphExec_t graph = nullptr;
+    // every layer's dW GEMM (+ SGD update) in one persistent grouped launch
+    // (bf16 SGD and low-rank NG; PARNN_NO_DW_GROUP=1 launches them per layer)
+    GemmGroupPlan dwg;
+    bool dw_group = false;
+    // bf16 SGD: every activation buffer feeding a dW GEMM carries a constant-1
+    // column at index d_l, so the GEMM's extra output column is the bias
+    // gradient (sum over the batch of dz, network.cpp:203-208) and the epilogue
+    // updates the bias with the weights -- no separate bias-gradient kernel
+    bool bias_in_dw = false;
+    long ones_col0() const { return bias_in_dw ? dims[0] : -1; }
+    cudaGraphExec_t graph = nullptr;  // the plain step (SGD / kron-full): alias of vgraphs[0]
     bool use_graph = true;
     long kernels_per_step = 0;
 
@@ -257,6 +289,9 @@ struct Replica {
     bool apply_pending = false;
     long apply_nodes = 0;
     void capture_variant(int v);
+    // capture the averaging-gated variants of every step kind up front (an averaging
+    // group does this, so no capture happens inside a timed or steady-state loop)
+    void precapture_gates();
     void capture_apply_graph();
     void lr_before_step(cudaStream_t s);
     void lr_after_step(cudaStream_t s);
@@ -283,7 +318,8 @@ struct Replica {
     long epoch_steps = 0;  // steps launched since upload_epoch
     long epoch_len = 0;    // steps uploaded
     double step_ce(long j);
-    void run_step(cudaStream_t s);  // one minibatch (graph or eager)
+    // one minibatch (graph or eager); window_end: an average follows this step
+    void run_step(cudaStream_t s, bool window_end = false);
     void enqueue_step(cudaStream_t s);
     void sync_shadow(cudaStream_t s);  // recompute bf16 copy after external param writes
     void check_errors();               // throws the reference's messages
@@ -311,12 +347,16 @@ void debug_gemm(int prec, bool a_mn, bool b_mn, int M, int N, int K, int mode, i
                 int force_mc, int lower, int bias_col, float alpha, float beta, float lr, const float* a,
                 const float* b, const float* bias, const float* aux, float* out, float* out2, double* sums,
                 int* info);
+// non-blocking stream at priority level 0 (highest: the dz chain and whatever
+// gates it), 1 (concurrent side work) or 2 (lowest: background NG subspace updates)
+cudaStream_t make_stream(int level);
 void record_ext(cudaEvent_t e, cudaStream_t s);
 void wait_ext(cudaStream_t s, cudaEvent_t e);
 
 // ----------------------------------------------------------- kernels.cu
 void launch_gather(const void* x, long ldx, const int32_t* y, const uint32_t* rows, const int* step, long B,
-                   long d, void* out, long ldo, int32_t* yout, bool f32, cudaStream_t s);
+                   long d, void* out, long ldo, int32_t* yout, bool f32, cudaStream_t s, long ones_col = -1);
+void launch_fill_ones_column(void* buf, long ld, long rows, long col, bool f32, cudaStream_t s);
 void launch_softmax_ce(const float* z, long ldz, long B, long C, const int32_t* y, void* dz, long lddz,
                        float* ce_rows, bool f32, cudaStream_t s);
 void launch_ce_reduce(const float* ce_rows, long B, double* d_ce, int* step, int advance, cudaStream_t s);

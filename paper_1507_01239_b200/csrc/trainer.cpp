@@ -108,7 +108,10 @@ void train(Context* ctx, Comm* comm, const TrainConfig& cfg, const std::vector<l
 
         uint64_t since = 0, events = 0;
         for (uint64_t b = 0; b < nb; ++b) {
-            for (Replica* r : reps) r->run_step(r->stream);
+            // the step that closes an averaging window (K-th, or the epoch's last: forced
+            // average) records its per-layer update events for the bucketed average
+            const bool window_end = since + 1 == cfg.avg_frequency || b + 1 == nb;
+            for (Replica* r : reps) r->run_step(r->stream, window_end);
             if (++since == cfg.avg_frequency) {
                 avg.run();
                 since = 0;
