@@ -92,6 +92,27 @@ int parnn_ctx_sync(parnn_ctx* ctx);
 int parnn_dataset_create(parnn_ctx* ctx, const double* x, const int32_t* y, uint64_t n, uint64_t d,
                          uint64_t classes, parnn_dataset** out);
 int parnn_dataset_destroy(parnn_dataset* ds);
+/* generate_synthetic + split_cv + train-split feature_stats / standardize_in_place
+ * (data.cpp:124-242) computed ON THE DEVICE into a train and a CV dataset:
+ * labels and row order bit-exact with the reference, features within fp32
+ * rounding (the gaussian stream is the reference's Rng(seed) polar-method
+ * stream, reconstructed in parallel by xoshiro jump-ahead). */
+int parnn_dataset_generate(parnn_ctx* ctx, uint64_t classes, uint64_t dim, uint64_t per_class, double separation,
+                           uint64_t seed, double cv_fraction, uint64_t split_seed, int standardize,
+                           parnn_dataset** train, parnn_dataset** cv);
+/* rows, features, classes of a device dataset */
+int parnn_dataset_info(parnn_dataset* ds, uint64_t* n, uint64_t* d, uint64_t* classes);
+/* the dataset's fp32 features (n x d row-major) and labels back to the host */
+int parnn_dataset_download(parnn_dataset* ds, float* x, int32_t* y);
+/* load_csv (data.cpp:66-107): 'label,f1,...' rows, '#' comments, errors with
+ * the 1-based line (parsed on all host threads). Buffers of cap_rows x cap_dim;
+ * n / d / classes are always set, the arrays only when they fit. */
+int parnn_load_csv(const char* path, double* x, int32_t* y, uint64_t cap_rows, uint64_t cap_dim, uint64_t* n,
+                   uint64_t* d, uint64_t* classes);
+/* load_csv straight into a device dataset */
+int parnn_dataset_load_csv(parnn_ctx* ctx, const char* path, parnn_dataset** out);
+/* save_csv (data.cpp:109-122): '%.17g' features */
+int parnn_save_csv(const char* path, const double* x, const int32_t* y, uint64_t n, uint64_t d);
 
 /* One worker's model + NG state + workspaces (WorkerState, parallel.cpp:81-91). */
 int parnn_replica_create(parnn_ctx* ctx, const uint64_t* dims, int ndims, int activation, int precision,

@@ -866,3 +866,22 @@ double ref_time_ng_precondition(uint64_t d_out, uint64_t d_in, uint64_t batch, u
 }
 
 }  // extern "C"
+
+// load_csv / save_csv (data.cpp:66-122) of the reference, for the CSV parity tests.
+extern "C" int ref_load_csv(const char* path, double* x, int32_t* y, uint64_t cap_rows, uint64_t cap_dim,
+                            uint64_t* n, uint64_t* d, uint64_t* classes) {
+    return guarded([&] {
+        const Dataset ds = load_csv(path);
+        *n = ds.size();
+        *d = ds.dim();
+        *classes = ds.num_classes;
+        if (x && y && ds.size() <= cap_rows && ds.dim() <= cap_dim) {
+            std::memcpy(x, ds.features.data().data(), ds.features.size() * sizeof(double));
+            for (std::size_t i = 0; i < ds.size(); ++i) y[i] = ds.labels[i];
+        }
+    });
+}
+
+extern "C" int ref_save_csv(const char* path, const double* x, const int32_t* y, uint64_t n, uint64_t d) {
+    return guarded([&] { save_csv(path, make_dataset(x, y, n, d, 1)); });
+}

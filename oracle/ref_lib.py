@@ -321,3 +321,19 @@ class RefLib:
         if wall < 0:
             raise RuntimeError(self.lib.ref_last_error().decode())
         return wall, ph, p, ce.value
+
+    def load_csv(self, path):
+        """The reference's load_csv: (x, y, classes); raises RuntimeError with its message."""
+        n, d, k = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self._chk(self.lib.ref_load_csv(path.encode(), None, None, C.c_uint64(0), C.c_uint64(0), C.byref(n),
+                                        C.byref(d), C.byref(k)))
+        x = np.zeros((n.value, d.value)); y = np.zeros(n.value, np.int32)
+        self._chk(self.lib.ref_load_csv(path.encode(), x.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p),
+                                        C.c_uint64(n.value), C.c_uint64(d.value), C.byref(n), C.byref(d),
+                                        C.byref(k)))
+        return x, y, k.value
+
+    def save_csv(self, path, x, y):
+        x = np.ascontiguousarray(x, np.float64); y = np.ascontiguousarray(y, np.int32)
+        self._chk(self.lib.ref_save_csv(path.encode(), x.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p),
+                                        C.c_uint64(x.shape[0]), C.c_uint64(x.shape[1])))

@@ -63,6 +63,12 @@ SIGNATURES = [
     ("parnn_ctx_sync", c_int, [vp]),
     ("parnn_dataset_create", c_int, [vp, vp, vp, c_u64, c_u64, c_u64, vp]),
     ("parnn_dataset_destroy", c_int, [vp]),
+    ("parnn_dataset_generate", c_int, [vp, c_u64, c_u64, c_u64, c_f64, c_u64, c_f64, c_u64, c_int, vp, vp]),
+    ("parnn_dataset_info", c_int, [vp, vp, vp, vp]),
+    ("parnn_dataset_download", c_int, [vp, vp, vp]),
+    ("parnn_load_csv", c_int, [C.c_char_p, vp, vp, c_u64, c_u64, vp, vp, vp]),
+    ("parnn_dataset_load_csv", c_int, [vp, C.c_char_p, vp]),
+    ("parnn_save_csv", c_int, [C.c_char_p, vp, vp, c_u64, c_u64]),
     ("parnn_replica_create", c_int, [vp, vp, c_int, c_int, c_int, c_int, c_u64, c_u64, c_f64, c_f64, vp]),
     ("parnn_replica_destroy", c_int, [vp]),
     ("parnn_replica_set_params", c_int, [vp, vp, c_u64]),

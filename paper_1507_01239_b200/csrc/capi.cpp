@@ -230,6 +230,87 @@ int parnn_dataset_destroy(parnn_dataset* ds) {
     return guarded([&] { delete ds; });
 }
 
+int parnn_dataset_generate(parnn_ctx* ctx, uint64_t classes, uint64_t dim, uint64_t per_class, double sep,
+                           uint64_t seed, double cv_fraction, uint64_t split_seed, int standardize,
+                           parnn_dataset** train, parnn_dataset** cv) {
+    return guarded([&] {
+        need(ctx, "dataset");
+        need(train, "train dataset");
+        need(cv, "cv dataset");
+        DeviceDataset *tr = nullptr, *cvd = nullptr;
+        generate_device(ctx->c.get(), classes, dim, per_class, sep, seed, cv_fraction, split_seed, standardize != 0,
+                        &tr, &cvd);
+        auto* a = new parnn_dataset;
+        a->d.reset(tr);
+        auto* b = new parnn_dataset;
+        b->d.reset(cvd);
+        *train = a;
+        *cv = b;
+    });
+}
+
+int parnn_dataset_info(parnn_dataset* ds, uint64_t* n, uint64_t* d, uint64_t* classes) {
+    return guarded([&] {
+        need(ds, "dataset");
+        if (n) *n = static_cast<uint64_t>(ds->d->n);
+        if (d) *d = static_cast<uint64_t>(ds->d->d);
+        if (classes) *classes = static_cast<uint64_t>(ds->d->classes);
+    });
+}
+
+int parnn_dataset_download(parnn_dataset* ds, float* x, int32_t* y) {
+    return guarded([&] {
+        need(ds, "dataset");
+        DeviceDataset& D = *ds->d;
+        CUDA_THROW(cudaSetDevice(D.ctx->device));
+        CUDA_THROW(cudaDeviceSynchronize());
+        if (x && D.n)
+            CUDA_THROW(cudaMemcpy2D(x, D.d * 4, D.x32, D.ld * 4, D.d * 4, D.n, cudaMemcpyDeviceToHost));
+        if (y && D.n) CUDA_THROW(cudaMemcpy(y, D.y, D.n * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int parnn_load_csv(const char* path, double* x, int32_t* y, uint64_t cap_rows, uint64_t cap_dim, uint64_t* n,
+                   uint64_t* d, uint64_t* classes) {
+    return guarded([&] {
+        need(path, "load_csv path");
+        uint64_t k = 0;
+        const host::HostData h = host::load_csv(path, &k);
+        if (n) *n = h.n;
+        if (d) *d = h.d;
+        if (classes) *classes = k;
+        if (x && y && h.n <= cap_rows && h.d <= cap_dim) {
+            std::memcpy(x, h.x.data(), h.x.size() * 8);
+            std::memcpy(y, h.y.data(), h.y.size() * 4);
+        }
+    });
+}
+
+int parnn_dataset_load_csv(parnn_ctx* ctx, const char* path, parnn_dataset** out) {
+    return guarded([&] {
+        need(ctx, "dataset");
+        need(path, "load_csv path");
+        uint64_t k = 0;
+        const host::HostData h = host::load_csv(path, &k);
+        auto* p = new parnn_dataset;
+        p->d.reset(new DeviceDataset(ctx->c.get(), h.x.data(), h.y.data(), static_cast<long>(h.n),
+                                     static_cast<long>(h.d), static_cast<long>(k)));
+        *out = p;
+    });
+}
+
+int parnn_save_csv(const char* path, const double* x, const int32_t* y, uint64_t n, uint64_t d) {
+    return guarded([&] {
+        need(path, "save_csv path");
+        host::HostData h;
+        h.n = n;
+        h.d = d;
+        h.x.assign(x, x + n * d);
+        h.y.assign(y, y + n);
+        host::save_csv(path, h);
+    });
+}
+
 int parnn_replica_create(parnn_ctx* ctx, const uint64_t* dims, int nd, int act, int prec, int opt, uint64_t minibatch,
                          uint64_t max_steps, double decay, double smoothing, parnn_replica** out) {
     return guarded([&] {

@@ -1,9 +1,15 @@
 #include "host.h"
 
+#include <algorithm>
+#include <cerrno>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <iterator>
 #include <stdexcept>
+#include <thread>
 
 namespace pnb {
 namespace host {
@@ -114,6 +120,12 @@ Jump make_jump(uint64_t n) {
     return acc;
 }
 
+Jump jump_square(const Jump& j) {
+    Jump out;
+    compose(j, j, out);
+    return out;
+}
+
 void Rng::jump(const Jump& j) {
     uint64_t out[4];
     apply(j, s_, out);
@@ -216,6 +228,148 @@ void standardize(HostData& d, const std::vector<double>& mean, const std::vector
     if (mean.size() != d.d) fail("standardize: stats dim does not match data dim");
     for (uint64_t i = 0; i < d.n; ++i)
         for (uint64_t j = 0; j < d.d; ++j) d.x[i * d.d + j] = (d.x[i * d.d + j] - mean[j]) / sd[j];
+}
+
+// ---- load_csv / save_csv (data.cpp:29-122) --------------------------------
+namespace {
+
+std::string csv_trim(const std::string& s) {
+    const size_t a = s.find_first_not_of(" \t\r");
+    if (a == std::string::npos) return "";
+    const size_t b = s.find_last_not_of(" \t\r");
+    return s.substr(a, b - a + 1);
+}
+
+// std::stod semantics (data.cpp:29-41): strtod over the whole field, range errors
+// (errno ERANGE) and non-finite values rejected
+bool csv_number(const std::string& f, double& v) {
+    if (f.empty()) return false;
+    errno = 0;
+    char* end = nullptr;
+    v = std::strtod(f.c_str(), &end);
+    if (end == f.c_str() || errno == ERANGE) return false;
+    return static_cast<size_t>(end - f.c_str()) == f.size() && std::isfinite(v);
+}
+
+struct CsvChunk {
+    std::vector<double> x;
+    std::vector<int32_t> y;
+    uint64_t dim = 0;          // features of this chunk's first data row
+    uint64_t first_line = 0;   // its line number (0: no data rows)
+    uint64_t err_line = 0;     // first failing line of the chunk (0: none)
+    std::string err;
+    int max_label = -1;
+};
+
+// lines [l0, l1) of the file, numbered from line_base + 1
+void csv_parse_chunk(const char* text, const std::vector<size_t>& starts, size_t l0, size_t l1, size_t len,
+                     CsvChunk& c) {
+    for (size_t li = l0; li < l1; ++li) {
+        const size_t a = starts[li];
+        size_t b = li + 1 < starts.size() ? starts[li + 1] - 1 : len;  // drop the '\n'
+        if (li + 1 == starts.size() && b > a && text[b - 1] == '\n') --b;  // the file's final newline
+        const std::string stripped = csv_trim(std::string(text + a, text + b));
+        const uint64_t line_no = li + 1;
+        if (stripped.empty() || stripped[0] == '#') continue;
+        std::vector<std::string> fields;
+        size_t st = 0;
+        for (;;) {
+            const size_t comma = stripped.find(',', st);
+            if (comma == std::string::npos) {
+                fields.push_back(stripped.substr(st));
+                break;
+            }
+            fields.push_back(stripped.substr(st, comma - st));
+            st = comma + 1;
+        }
+        auto error = [&](const std::string& m) {
+            c.err_line = line_no;
+            c.err = m;
+        };
+        if (fields.size() < 2) return error("load_csv: expected 'label,f1,...' at line " + std::to_string(line_no));
+        double lv = 0.0;
+        const std::string lf = csv_trim(fields[0]);
+        if (!csv_number(lf, lv))
+            return error("load_csv: non-numeric label '" + lf + "' at line " + std::to_string(line_no));
+        if (lv < 0 || lv != std::floor(lv))
+            return error("load_csv: label must be a non-negative integer, got '" + fields[0] + "' at line " +
+                         std::to_string(line_no));
+        const uint64_t row_dim = fields.size() - 1;
+        if (c.first_line == 0) {
+            c.first_line = line_no;
+            c.dim = row_dim;
+        } else if (row_dim != c.dim) {
+            return error("load_csv: ragged row with " + std::to_string(row_dim) + " features (expected " +
+                         std::to_string(c.dim) + ") at line " + std::to_string(line_no));
+        }
+        for (size_t j = 1; j < fields.size(); ++j) {
+            double v = 0.0;
+            const std::string ff = csv_trim(fields[j]);
+            if (!csv_number(ff, v))
+                return error("load_csv: non-numeric feature '" + ff + "' at line " + std::to_string(line_no));
+            c.x.push_back(v);
+        }
+        c.y.push_back(static_cast<int32_t>(lv));
+        c.max_label = std::max(c.max_label, c.y.back());
+    }
+}
+
+}  // namespace
+
+HostData load_csv(const std::string& path, uint64_t* classes) {
+    std::ifstream is(path, std::ios::binary);
+    if (!is) fail("load_csv: cannot open '" + path + "'");
+    const std::string text((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+    // line starts (std::getline semantics: a final line without '\n' still counts)
+    std::vector<size_t> starts;
+    if (!text.empty()) starts.push_back(0);
+    for (size_t i = 0; i < text.size(); ++i)
+        if (text[i] == '\n' && i + 1 < text.size()) starts.push_back(i + 1);
+    const size_t nl = starts.size();
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nch = std::max<size_t>(1, std::min<size_t>(hw, nl / 4096 + 1));
+    std::vector<CsvChunk> ch(nch);
+    std::vector<std::thread> th;
+    for (size_t k = 0; k < nch; ++k)
+        th.emplace_back([&, k] { csv_parse_chunk(text.data(), starts, nl * k / nch, nl * (k + 1) / nch, text.size(), ch[k]); });
+    for (auto& t : th) t.join();
+    // the reference stops at the first failing line in file order; a chunk's first
+    // data row is checked against the file's first data row (global dim) first
+    uint64_t dim = 0;
+    for (const CsvChunk& c : ch) {
+        if (c.first_line && dim == 0) dim = c.dim;
+        if (c.first_line && c.dim != dim)
+            fail("load_csv: ragged row with " + std::to_string(c.dim) + " features (expected " + std::to_string(dim) +
+                 ") at line " + std::to_string(c.first_line));
+        if (c.err_line) fail(c.err);
+    }
+    HostData d;
+    d.d = dim;
+    int max_label = -1;
+    for (const CsvChunk& c : ch) {
+        d.x.insert(d.x.end(), c.x.begin(), c.x.end());
+        d.y.insert(d.y.end(), c.y.begin(), c.y.end());
+        max_label = std::max(max_label, c.max_label);
+    }
+    d.n = d.y.size();
+    if (d.n == 0) fail("load_csv: no data rows in '" + path + "'");
+    if (classes) *classes = static_cast<uint64_t>(max_label) + 1;
+    return d;
+}
+
+void save_csv(const std::string& path, const HostData& d) {
+    std::ofstream os(path, std::ios::trunc);
+    if (!os) fail("save_csv: cannot open '" + path + "' for writing");
+    char buf[32];
+    for (uint64_t i = 0; i < d.n; ++i) {
+        os << d.y[i];
+        for (uint64_t j = 0; j < d.d; ++j) {
+            std::snprintf(buf, sizeof(buf), "%.17g", d.x[i * d.d + j]);
+            os << ',' << buf;
+        }
+        os << '\n';
+    }
+    if (!os) fail("save_csv: write failed for '" + path + "'");
 }
 
 uint64_t param_count(const std::vector<uint64_t>& dims) {

@@ -20,6 +20,7 @@ struct Jump {
     uint64_t col[256][4];
 };
 Jump make_jump(uint64_t n);
+Jump jump_square(const Jump& j);  // T^2n from T^n
 
 class Rng {
 public:
@@ -70,6 +71,10 @@ struct HostData {
     uint64_t n = 0, d = 0;
 };
 HostData generate_synthetic(uint64_t classes, uint64_t dim, uint64_t per_class, double sep, uint64_t seed);
+// load_csv / save_csv (data.cpp:66-122): 'label,f1,...' rows, '#' comments and
+// blank lines skipped, errors naming the 1-based line; parsed on all host threads
+HostData load_csv(const std::string& path, uint64_t* classes);
+void save_csv(const std::string& path, const HostData& d);
 void split_cv(const HostData& all, double cv_fraction, uint64_t seed, HostData& train, HostData& cv);
 void feature_stats(const HostData& d, std::vector<double>& mean, std::vector<double>& sd);
 void standardize(HostData& d, const std::vector<double>& mean, const std::vector<double>& sd);

@@ -122,6 +122,13 @@ DeviceDataset::DeviceDataset(Context* c, const double* x, const int32_t* labels,
     CUDA_THROW(cudaMemcpy(y, labels, n * 4, cudaMemcpyHostToDevice));
 }
 
+DeviceDataset::DeviceDataset(Context* c, long n_, long d_, long classes_)
+    : ctx(c), n(n_), d(d_), ld(pad32(d_)), classes(classes_) {
+    CUDA_THROW(cudaSetDevice(c->device));
+    x32 = dalloc<float>(static_cast<size_t>(n * ld));
+    y = dalloc<int32_t>(n);
+}
+
 DeviceDataset::~DeviceDataset() {
     if (written) cudaEventDestroy(written);
     dfree(x32);

@@ -89,6 +89,7 @@ struct DeviceDataset {
     int32_t* y = nullptr;
     cudaEvent_t written = nullptr;  // last write_rows; steps of replicas bound here wait on it
     DeviceDataset(Context* c, const double* x, const int32_t* labels, long n, long d, long classes);
+    DeviceDataset(Context* c, long n, long d, long classes);  // zeroed device buffers (data.cu fills them)
     ~DeviceDataset();
     const void* features(Precision p);
     // overwrite rows [row0, row0+n) from host fp32 (+ labels); refreshes the bf16 copy
@@ -350,6 +351,11 @@ void debug_gemm(int prec, bool a_mn, bool b_mn, int M, int N, int K, int mode, i
 // non-blocking stream at priority level 0 (highest: the dz chain and whatever
 // gates it), 1 (concurrent side work) or 2 (lowest: background NG subspace updates)
 cudaStream_t make_stream(int level);
+// data.cu: generate_synthetic + split_cv + train-split standardize (data.cpp:124-242)
+// on the device; labels / row order bit-exact, features within fp32 rounding
+void generate_device(Context* ctx, uint64_t classes, uint64_t dim, uint64_t per_class, double sep, uint64_t seed,
+                     double cv_fraction, uint64_t split_seed, bool standardize, DeviceDataset** train,
+                     DeviceDataset** cv);
 void record_ext(cudaEvent_t e, cudaStream_t s);
 void wait_ext(cudaStream_t s, cudaEvent_t e);
 

@@ -193,6 +193,22 @@ def make_data(classes: int, dim: int, per_class: int, separation: float, seed: i
     return Dataset(tx[:a].copy(), ty[:a].copy(), classes), Dataset(cx[:b].copy(), cy[:b].copy(), classes)
 
 
+def load_csv(path: str) -> Dataset:
+    """load_csv (data.cpp:66-107) on the host threads; errors carry the reference's messages."""
+    n, d, k = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    check(lib().parnn_load_csv(path.encode(), None, None, 0, 0, C.byref(n), C.byref(d), C.byref(k)))
+    x = np.zeros((n.value, d.value))
+    y = np.zeros(n.value, np.int32)
+    check(lib().parnn_load_csv(path.encode(), ptr(x), ptr(y), n.value, d.value, C.byref(n), C.byref(d), C.byref(k)))
+    return Dataset(x, y, k.value)
+
+
+def save_csv(path: str, ds: Dataset) -> None:
+    """save_csv (data.cpp:109-122)."""
+    x, y = f64(ds.features), i32(ds.labels)
+    check(lib().parnn_save_csv(path.encode(), ptr(x), ptr(y), x.shape[0], x.shape[1] if x.ndim == 2 else 0))
+
+
 def param_count(dims) -> int:
     d = u64(dims)
     return int(lib().parnn_param_count(ptr(d), len(d)))
@@ -303,12 +319,40 @@ class Context:
 
 
 class DeviceDataset:
-    def __init__(self, ctx: Context, ds: Dataset):
+    def __init__(self, ctx: Context, ds: Dataset | None = None, handle=None):
+        if handle is None:
+            h = C.c_void_p()
+            x, y = f64(ds.features), i32(ds.labels)
+            classes = ds.num_classes or (int(y.max()) + 1 if y.size else 0)
+            check(lib().parnn_dataset_create(ctx.h, ptr(x), ptr(y), x.shape[0], x.shape[1], classes, C.byref(h)))
+        else:
+            h = handle
+        self.h, self.ctx = h, ctx
+        n, d, k = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(lib().parnn_dataset_info(self.h, C.byref(n), C.byref(d), C.byref(k)))
+        self.n, self.d, self.num_classes = n.value, d.value, k.value
+
+    @staticmethod
+    def generate(ctx: Context, classes: int, dim: int, per_class: int, separation: float, seed: int,
+                 cv_fraction: float = 0.10, split_seed: int = 0, standardize: bool = True):
+        """generate_synthetic + split_cv + standardize on the device (data.cpp:124-242):
+        returns (train, cv) device datasets."""
+        a, b = C.c_void_p(), C.c_void_p()
+        check(lib().parnn_dataset_generate(ctx.h, classes, dim, per_class, separation, seed, cv_fraction, split_seed,
+                                           int(standardize), C.byref(a), C.byref(b)))
+        return DeviceDataset(ctx, handle=a), DeviceDataset(ctx, handle=b)
+
+    @staticmethod
+    def load_csv(ctx: Context, path: str):
         h = C.c_void_p()
-        x, y = f64(ds.features), i32(ds.labels)
-        classes = ds.num_classes or (int(y.max()) + 1 if y.size else 0)
-        check(lib().parnn_dataset_create(ctx.h, ptr(x), ptr(y), x.shape[0], x.shape[1], classes, C.byref(h)))
-        self.h, self.ctx, self.n = h, ctx, x.shape[0]
+        check(lib().parnn_dataset_load_csv(ctx.h, path.encode(), C.byref(h)))
+        return DeviceDataset(ctx, handle=h)
+
+    def download(self) -> Dataset:
+        x = np.zeros((self.n, self.d), np.float32)
+        y = np.zeros(self.n, np.int32)
+        check(lib().parnn_dataset_download(self.h, ptr(x), ptr(y)))
+        return Dataset(x, y, self.num_classes)
 
     def write_rows(self, x, y, row0: int = 0):
         """Host fp32 rows -> device (the per-step H2D of the end-to-end path)."""
