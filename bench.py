@@ -50,7 +50,13 @@ OPT_DESC = {"ngsgd_lowrank": "ngsgd_lowrank: online low-rank Fisher NG-SGD (nort
             "sgd": "sgd: plain SGD"}
 METRIC = "training frames/sec (440-2048x6-8806 NG-SGD, minibatch 1024)"
 UNIT = "frames/s"
-SEPARATION = 8.0
+# Calibrated with scripts/calibrate_cfg2.py (SURVEY §8d "Calibrate s"; profiles/
+# r2_calibration.txt): at s = 20 and 128 frames per class the low-rank NG-SGD (lr 10,
+# exponential schedule over 6 epochs) takes the frame CE from ln 8806 = 9.08 to ~0.3
+# while plain SGD stays at ln 8806; s <= 16 learns only late, s >= 32 is separable
+# within 2 epochs; lr >= 20 diverges.
+SEPARATION = 20.0
+LR_INIT = 10.0
 
 
 def flops_per_frame(dims):
@@ -78,7 +84,7 @@ def workload_config(args, world):
         "parallelism": f"dp{world} model-averaging",
         "avg_frequency": args.avg_frequency,
         "data": (f"generate_synthetic({DIMS[-1]} classes x {args.per_class}, {DIMS[0]}-dim, s={SEPARATION:g}, "
-                 f"seed 1) -> split_cv(0.1, seed 2) -> standardize: {n_train} train frames"),
+                 f"seed 1) -> split_cv(0.1, seed 2) -> standardize (on the device): {n_train} train frames"),
         "l2": "inputs larger than L2: the resident training set is %.0f MB (bf16) and each step streams 160 MB of "
               "fp32 parameters" % (n_train * 440 * 2 / 1e6),
     }
@@ -196,12 +202,11 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # synthetic Switchboard-shaped frames (generate_synthetic + split + standardize, data.cpp:124-242);
-    # worker r trains on shard r of partition_data (parallel.cpp:61-77)
+    # synthetic Switchboard-shaped frames (generate_synthetic + split + standardize, data.cpp:124-242,
+    # generated on the device); worker r trains on shard r of partition_data (parallel.cpp:61-77)
     t0 = time.perf_counter()
-    train, _ = P.make_data(DIMS[-1], DIMS[0], args.per_class, SEPARATION, 1, 0.10, 2, True)
-    shards = P.partition_rows(train.size(), world, 0)
-    ds = P.DeviceDataset(ctx, train)
+    ds, cv_ds = P.DeviceDataset.generate(ctx, DIMS[-1], DIMS[0], args.per_class, SEPARATION, 1, 0.10, 2, True)
+    shards = P.partition_rows(ds.n, world, 0)
     gen_s = time.perf_counter() - t0
     m0 = P.init_random(DIMS, seed=7)
     rep = P.Replica(ctx, DIMS, precision=prec, optimizer=opt, minibatch=B, max_steps=W + K + 8)
@@ -212,7 +217,7 @@ def run_ours(args, rank, world, local_rank):
     need = W + K + 8
     rows = shards[rank][order.ravel().astype(np.int64)]
     rows = np.resize(rows, need * B)
-    lrs = np.full(need, 1e-3, np.float32)
+    lrs = np.full(need, LR_INIT * 0.01 ** 0.5, np.float32)  # the exponential schedule's mid-run rate
     rep.upload_epoch(rows, lrs)
     if W:
         P.run_steps([rep], W, args.avg_frequency, comm=comm, m_total=world)  # warm-up, averaging included
@@ -251,12 +256,13 @@ def run_ours(args, rank, world, local_rank):
         E = args.e2e_steps
         pins = [torch.empty((B, DIMS[0]), dtype=torch.float32, pin_memory=True) for _ in range(2)]
         pinys = [torch.empty((B,), dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        train = ds.download()  # host-resident frames (fp32, as on the device)
         stage = P.DeviceDataset(ctx, P.Dataset(train.features[:2 * B], train.labels[:2 * B], DIMS[-1]))
         rep_e = P.Replica(ctx, DIMS, precision=prec, optimizer=opt, minibatch=B, max_steps=E + 4)
         rep_e.set_params(m0.params)
         rep_e.bind(stage)
         rep_e.upload_epoch(np.concatenate([np.arange(B) + (i % 2) * B for i in range(E + 4)]),
-                           np.full(E + 4, 1e-3, np.float32))
+                           np.full(E + 4, LR_INIT * 0.01 ** 0.5, np.float32))
         avg_e = P.Averager([rep_e], comm=comm, m_total=world)
         src = torch.from_numpy(shards[rank][np.random.default_rng(3 + rank).integers(0, S, (E + 4, B))].astype(np.int64))
         # host-resident training frames in the device dataset's element type (fp32),
@@ -347,6 +353,25 @@ def run_ours(args, rank, world, local_rank):
                   "frac": g_fl / (g_ms / 1e3) / 1e12 / burst, "ms_per_step": g_ms,
                   "flops_per_step": g_fl, "kinds": gemm_kinds}
 
+    # ---- the metric's "final frame CE": train_parallel for a fixed number of epochs on
+    # the same data (train_loop semantics: per-epoch forced average, CV accuracy on
+    # rank 0 outside the wall time, exponential LR), low-rank NG-SGD and plain SGD
+    conv = None
+    if world == 1 and args.epochs > 0:
+        conv = {"epochs": args.epochs, "lr_init": LR_INIT, "schedule": "exponential", "minibatch": B,
+                "avg_frequency": args.avg_frequency}
+        m0c = P.init_random(DIMS, seed=7)
+        for name in ("ngsgd_lowrank", "sgd"):
+            o = P.TrainOptions(optimizer=P.OptimizerKind[name], lr_init=LR_INIT, epochs=args.epochs,
+                               precision=prec)
+            res = P.train_parallel(P.ParallelPlan(1, args.avg_frequency, B, 5), m0c, None, None, o, ctx=ctx,
+                                   device_data=(ds, cv_ds))
+            frames = sum((ds.n // B) * B for _ in res.metrics)
+            conv[name] = {"train_ce": [round(float(m.train_ce), 4) for m in res.metrics],
+                          "cv_accuracy": [round(float(m.cv_accuracy), 4) for m in res.metrics],
+                          "final_ce": float(res.metrics[-1].train_ce),
+                          "frames_per_s": frames / sum(m.wall_seconds for m in res.metrics)}
+
     cpu = None
     if world == 1 and not args.no_cpu:
         try:
@@ -393,6 +418,7 @@ def run_ours(args, rank, world, local_rank):
         "cpu_baseline": cpu,
         "ngsgd_kron_full": kron,
         "final_ce": float(ce[-1]),
+        "convergence": conv,
         "data_gen_seconds": gen_s,
         "regions_ms": {k: round(v[0], 4) for k, v in sorted(by_kind.items(), key=lambda kv: -kv[1][0])},
     })
@@ -447,7 +473,8 @@ def main():
     ap.add_argument("--no-kron", action="store_true", help="skip the kron-full NG-SGD side measurement")
     ap.add_argument("--minibatch", type=int, default=1024)
     ap.add_argument("--avg-frequency", type=int, default=4)
-    ap.add_argument("--per-class", type=int, default=24)
+    ap.add_argument("--per-class", type=int, default=128)
+    ap.add_argument("--epochs", type=int, default=6, help="epochs of the final-CE run (0 = skip)")
     ap.add_argument("--profile-steps", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=600)
     ap.add_argument("--no-e2e", action="store_true")
