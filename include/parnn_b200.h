@@ -291,6 +291,11 @@ int parnn_greedy_pretrain_rng(parnn_ctx* ctx, const uint64_t* dims, int ndims, c
                               int activation, uint64_t rng_state[4], double* rng_spare, int* rng_has_spare,
                               int precision, double* params_out);
 
+/* Device time (CUDA events around each layer's epoch loop) of the CD-1 steps
+ * of the last greedy_pretrain call on this thread, their count and their flop
+ * (10 v h b per step). Measurement aid: the reference has no counterpart. */
+int parnn_pretrain_last_stats(double* cd1_device_seconds, uint64_t* cd1_steps, double* cd1_flop);
+
 #ifdef __cplusplus
 }
 #endif

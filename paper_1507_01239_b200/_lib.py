@@ -110,6 +110,7 @@ SIGNATURES = [
     ("parnn_greedy_pretrain", c_int, [vp, vp, c_int, vp, c_u64, c_u64, c_f64, c_f64, c_u64, c_u64, c_int, vp]),
     ("parnn_greedy_pretrain_rng", c_int, [vp, vp, c_int, vp, c_u64, c_u64, c_f64, c_f64, c_u64, c_int, vp, vp, vp,
                                           c_int, vp]),
+    ("parnn_pretrain_last_stats", c_int, [vp, vp, vp]),
 ]
 
 _lib = None

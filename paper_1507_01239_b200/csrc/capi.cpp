@@ -755,4 +755,12 @@ int parnn_greedy_pretrain_rng(parnn_ctx* ctx, const uint64_t* dims, int nd, cons
     });
 }
 
+int parnn_pretrain_last_stats(double* cd1_device_seconds, uint64_t* cd1_steps, double* cd1_flop) {
+    return guarded([&] {
+        if (cd1_device_seconds) *cd1_device_seconds = g_pretrain_stats.cd1_seconds;
+        if (cd1_steps) *cd1_steps = g_pretrain_stats.cd1_steps;
+        if (cd1_flop) *cd1_flop = g_pretrain_stats.cd1_flop;
+    });
+}
+
 }  // extern "C"

@@ -22,11 +22,12 @@ void* upload(const float* h, long rows, long cols, long ld, bool f32) {
     CUDA_THROW(cudaMemset(d, 0, static_cast<size_t>(rows * ld) * es + 256));
     if (f32) {
         CUDA_THROW(cudaMemcpy2D(d, ld * 4, h, cols * 4, cols * 4, rows, cudaMemcpyHostToDevice));
+        CUDA_THROW(cudaStreamSynchronize(cudaStreamLegacy));
     } else {
         std::vector<bf16> t(static_cast<size_t>(rows * ld), __float2bfloat16_rn(0.f));
         for (long r = 0; r < rows; ++r)
             for (long c = 0; c < cols; ++c) t[r * ld + c] = __float2bfloat16_rn(h[r * cols + c]);
-        CUDA_THROW(cudaMemcpy(d, t.data(), t.size() * 2, cudaMemcpyHostToDevice));
+        pnb::upload(d, t.data(), t.size() * 2);
     }
     return d;
 }

@@ -634,12 +634,12 @@ void side_alloc(Replica& r, LrSide& sd, bool in, long dx, int want_rank, int lay
         sth[R + i] = e0;
     }
     sth[2 * R] = kEps;
-    CUDA_THROW(cudaMemcpy(sd.st, sth.data(), sth.size() * 8, cudaMemcpyHostToDevice));
+    upload(sd.st, sth.data(), sth.size() * 8);
     std::vector<float> w(R * sd.ldY, 0.f);
     const double se = std::sqrt(e0);
     for (int i = 0; i < R; ++i)
         for (long j = 0; j < sd.D; ++j) w[i * sd.ldY + j] = static_cast<float>(se * basis[i * sd.D + j]);
-    CUDA_THROW(cudaMemcpy(sd.YW + R * sd.ldY, w.data(), w.size() * 4, cudaMemcpyHostToDevice));
+    upload(sd.YW + R * sd.ldY, w.data(), w.size() * 4);
     if (!r.f32()) {
         lr_split_kernel<<<64, 256>>>(sd.YW + R * sd.ldY, R * sd.ldY, R * sd.ldY, static_cast<bf16*>(sd.wop));
         CUDA_THROW(cudaGetLastError());
@@ -758,8 +758,8 @@ void lr_debug_eig(int R, long D, double eta, double a, double alpha, const doubl
     double* dst = dalloc_d(ns);
     float* dg = falloc(4L * R * R);
     float* dm = falloc(2L * R * R);
-    CUDA_THROW(cudaMemcpy(dst, st_in, ns * 8, cudaMemcpyHostToDevice));
-    CUDA_THROW(cudaMemcpy(dg, gram, 16L * R * R, cudaMemcpyHostToDevice));
+    upload(dst, st_in, ns * 8);
+    upload(dg, gram, 16L * R * R);
     ensure_smem_attr(reinterpret_cast<const void*>(lr_eig_kernel), static_cast<int>(eig_smem(LR_MAX_RANK)));
     const int nblk = ((R + 7) & ~7) / 4;
     const int threads = std::max(64, 32 * (nblk / 2));

@@ -168,8 +168,8 @@ Averager::Averager(Context* c, const std::vector<Replica*>& r, Comm* cm, long m)
     CUDA_THROW(cudaMalloc(&d_src, k * sizeof(float*)));
     CUDA_THROW(cudaMalloc(&d_shadow, k * sizeof(bf16*)));
     CUDA_THROW(cudaMalloc(&d_null_shadow, sizeof(bf16*)));
-    CUDA_THROW(cudaMemcpy(d_src, src.data(), k * sizeof(float*), cudaMemcpyHostToDevice));
-    CUDA_THROW(cudaMemcpy(d_shadow, sh.data(), k * sizeof(bf16*), cudaMemcpyHostToDevice));
+    upload(d_src, src.data(), k * sizeof(float*));
+    upload(d_shadow, sh.data(), k * sizeof(bf16*));
     CUDA_THROW(cudaMemset(d_null_shadow, 0, sizeof(bf16*)));
     work = comm != nullptr || k > 1;
     if (work)
@@ -177,7 +177,7 @@ Averager::Averager(Context* c, const std::vector<Replica*>& r, Comm* cm, long m)
     if (comm && k > 1) {
         CUDA_THROW(cudaMalloc(&scratch, n * sizeof(float)));
         CUDA_THROW(cudaMalloc(&d_scratch_ptr, sizeof(float*)));
-        CUDA_THROW(cudaMemcpy(d_scratch_ptr, &scratch, sizeof(float*), cudaMemcpyHostToDevice));
+        upload(d_scratch_ptr, &scratch, sizeof(float*));
     }
 }
 

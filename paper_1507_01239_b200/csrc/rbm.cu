@@ -1,12 +1,15 @@
 // RBM CD-1 on device (pretrain.cpp:9-207).
 //
-// One update = 4 tcgen05 GEMMs + 3 small kernels:
+// One update = 4 tcgen05 GEMMs + 4 small kernels. The three M = b GEMMs run
+// split-K (EPI_PARTIAL) and each is followed by one reduction kernel that sums
+// the splits and applies the elementwise step:
 //   pos   = sigmoid(X W^T + hb)                      -> PN[0:b)   (hidden_probs)
-//   hs    = Bernoulli(pos)                           -> HS        (sample_bernoulli)
+//   hs    = Bernoulli(pos)    (same kernel)          -> HS        (sample_bernoulli)
 //   recon = hs W + vb  (sigmoid for bernoulli)       -> XR[b:2b)  (reconstruct_mean)
 //   -neg  = -sigmoid(recon W^T + hb)                 -> PN[b:2b)
 //   W    += lr/b * [pos; -neg]^T [X; recon]          one GEMM with K = 2b (cd1_apply)
-//   hb   += lr/b * colsum(PN),  vb += lr/b * colsum(X - recon)
+//   hb   += lr/b * colsum(PN),  vb += lr/b * colsum(X - recon)  (column sums
+//           taken by the reductions, folded by bias_finish_kernel)
 // Bernoulli draws: counter-based Philox4x32-10 keyed by (seed, element
 // counter) in row-major draw order, or threshold_half, or injected uniforms
 // (parity modes, pretrain.cpp:63-77).
@@ -62,73 +65,169 @@ __device__ __forceinline__ float tf<bf16>(bf16 v) {
     return __bfloat162float(v);
 }
 
-template <typename T>
-__global__ void sample_kernel(const T* __restrict__ pos, long ldp, long b, long h, T* __restrict__ hs, long ldh,
-                              int mode, uint64_t key, uint64_t counter, const double* __restrict__ u) {
-    const long total = b * h;
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-        const long r = i / h, c = i % h;
-        const float p = tf<T>(pos[r * ldp + c]);
-        bool on;
-        if (mode == 1) on = p > 0.5f;
-        else if (mode == 2) on = u[i] < static_cast<double>(p);
-        else on = philox_uniform(key, counter + static_cast<uint64_t>(i)) < p;
-        hs[r * ldh + c] = static_cast<T>(on ? 1.f : 0.f);
+// Split-K reductions with the CD-1 epilogues fused (pretrain.cpp:37-121). The
+// three M = b GEMMs of a step (b = 128 rows against a 2048-wide layer) have 8-16
+// output tiles: each runs split-K over ~128 CTAs writing fp32 partial tiles
+// (EPI_PARTIAL), and one of these kernels sums the splits and applies the
+// step's elementwise work. Block = 32 columns x 8 row groups over one chunk of
+// rows; its column sums go to colpart[chunk][col] (fixed order, deterministic)
+// and bias_finish_kernel folds them into the biases once all chunks are done.
+struct PartIn {
+    const float* p;  // split ks at p + ks * stride, element (r, c) at r * ld + c
+    long stride, ld;
+    int ks;
+};
+
+// the splits are summed in split order; the loads are read-only (nc) so the
+// unrolled batch of them is in flight together
+__device__ __forceinline__ float part_sum(const PartIn& in, long r, long c) {
+    const float* q = in.p + r * in.ld + c;
+    float a = __ldg(q);
+#pragma unroll 8
+    for (int k = 1; k < in.ks; ++k) a += __ldg(q + k * in.stride);
+    return a;
+}
+
+__device__ __forceinline__ float sigmoid_exact(float z) { return 1.f / (1.f + expf(-z)); }
+__device__ __forceinline__ double sigmoid_d(float z) { return 1.0 / (1.0 + exp(-static_cast<double>(z))); }
+
+struct Chunk {
+    long r0, r1;  // rows of this block
+    long j;       // column
+};
+
+__device__ __forceinline__ Chunk chunk_of(long b, long n) {
+    const long per = 8;  // one row per thread (grid.y = ceil(b / 8))
+    Chunk c;
+    c.r0 = blockIdx.y * per;
+    c.r1 = min(b, c.r0 + per);
+    c.j = blockIdx.x * 32L + threadIdx.x;
+    return c;
+}
+
+// column sum over the block's 8 row groups -> colpart[blockIdx.y][j]
+__device__ __forceinline__ void block_colsum(double acc, long j, long n, double* colpart, long ldc) {
+    __shared__ double red[8][33];
+    red[threadIdx.y][threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.y == 0 && j < n) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
+        colpart[blockIdx.y * ldc + j] = s;
     }
 }
 
-// Bias updates of a CD-1 step (pretrain.cpp:106-119): hb += s * colsum(PN) over
-// the 2b stacked rows [pos_h; -neg_h], vb += s * colsum(v - recon). A block is
-// 32 columns x 16 row groups: each thread sums every 16th row of its column
-// (independent loads in flight), then the 16 partials are added in a fixed order
-// (deterministic). One thread per column summing all rows serially was
-// latency-bound (80 us of a 2048 x 2048, b = 128 step).
+// pos = sigmoid(sum + hb) -> PN rows [0, b) (and fp32 rows of out32 when given);
+// hs = Bernoulli(pos) -> HS: mode 0 Philox keyed by (key, counter + r*h + c)
+// (the reference's row-major draw order), 1 threshold_half, 2 injected
+// uniforms, 3 hs = pos (mean-field pass of reconstruction_error), 4 no hs
+// (hidden_probs).
 template <typename T>
-__global__ void __launch_bounds__(512) bias_update_kernel(const T* __restrict__ pn, long ldh, long b, long h,
-                                                          float* __restrict__ hb, const T* __restrict__ xr, long ldv,
-                                                          long v, float* __restrict__ vb, float s) {
-    __shared__ float red[2][16][33];
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const long j = blockIdx.x * 32L + tx;
-    float ah = 0.f, av = 0.f;
+__global__ void __launch_bounds__(256) cd1_pos_kernel(PartIn in, long b, long h, const float* __restrict__ hb,
+                                                      T* __restrict__ pn, long ldh, T* __restrict__ hs, int mode,
+                                                      uint64_t key, uint64_t counter, const double* __restrict__ u,
+                                                      float* __restrict__ zp, float* __restrict__ out32, long ld32,
+                                                      const uint64_t* __restrict__ dctr) {
+    grid_dep_wait();
+    // graph-launched steps: counter = epoch base + step * b * h (dctr = {step, base})
+    if (dctr) counter = dctr[1] + dctr[0] * static_cast<uint64_t>(b) * static_cast<uint64_t>(h);
+    const Chunk c = chunk_of(b, h);
+    if (c.j < h) {
+        const float bias = hb[c.j];
+        for (long r = c.r0 + threadIdx.y; r < c.r1; r += 8) {
+            const float z = part_sum(in, r, c.j) + bias;
+            if (zp) zp[r * ldh + c.j] = z;
+            const T pv = static_cast<T>(sigmoid_exact(z));
+            const float p = tf<T>(pv);
+            pn[r * ldh + c.j] = pv;
+            if (out32) out32[r * ld32 + c.j] = p;
+            if (!hs) continue;
+            const long i = r * h + c.j;
+            float s;
+            if (mode == 3) s = p;
+            else if (mode == 1) s = p > 0.5f ? 1.f : 0.f;
+            else if (mode == 2) s = u[i] < static_cast<double>(p) ? 1.f : 0.f;
+            else s = philox_uniform(key, counter + static_cast<uint64_t>(i)) < p ? 1.f : 0.f;
+            hs[r * ldh + c.j] = static_cast<T>(s);
+        }
+    }
+}
+
+// recon = act(sum + vb) -> xr rows [b, 2b) (act: sigmoid, or identity for
+// Gaussian visibles); colpart <- column sums of (v - recon) over the block's rows.
+template <typename T>
+__global__ void __launch_bounds__(256) cd1_recon_kernel(PartIn in, long b, long v, const float* __restrict__ vb,
+                                                        bool gaussian, T* __restrict__ xr, long ldv, T* __restrict__ rec,
+                                                        double* __restrict__ colpart) {
+    grid_dep_wait();
+    const Chunk c = chunk_of(b, v);
+    double acc = 0.0;
+    if (c.j < v) {
+        const float bias = vb[c.j];
+        for (long r = c.r0 + threadIdx.y; r < c.r1; r += 8) {
+            const float z = part_sum(in, r, c.j) + bias;
+            const T x = static_cast<T>(gaussian ? z : sigmoid_exact(z));
+            rec[r * ldv + c.j] = x;
+            if (colpart) acc += static_cast<double>(tf<T>(xr[r * ldv + c.j])) - (gaussian ? z : sigmoid_d(z));
+        }
+    }
+    grid_dep_launch();
+    if (colpart) block_colsum(acc, c.j, v, colpart, ldv);
+}
+
+// -neg = -sigmoid(sum + hb) -> PN rows [b, 2b); colpart <- column sums of
+// (pos - neg). pos and neg are close once the RBM reconstructs well, so their
+// difference is taken in fp64 from the two pre-activations (zp: the pos pass's,
+// kept by cd1_pos_kernel) rather than from the rounded probabilities.
+template <typename T>
+__global__ void __launch_bounds__(256) cd1_neg_kernel(PartIn in, long b, long h, const float* __restrict__ hb,
+                                                      const float* __restrict__ zp, T* __restrict__ pn, long ldh,
+                                                      double* __restrict__ colpart) {
+    grid_dep_wait();
+    const Chunk c = chunk_of(b, h);
+    double acc = 0.0;
+    if (c.j < h) {
+        const float bias = hb[c.j];
+        for (long r = c.r0 + threadIdx.y; r < c.r1; r += 8) {
+            const float z = part_sum(in, r, c.j) + bias;
+            pn[(b + r) * ldh + c.j] = static_cast<T>(-sigmoid_exact(z));
+            acc += sigmoid_d(zp[r * ldh + c.j]) - sigmoid_d(z);
+        }
+    }
+    grid_dep_launch();
+    block_colsum(acc, c.j, h, colpart, ldh);
+}
+
+// hb += s * sum (pos - neg), vb += s * sum (v - recon)   (pretrain.cpp:106-119)
+__global__ void bias_finish_kernel(const double* __restrict__ cpn, int chunks_h, long h, long ldh,
+                                   float* __restrict__ hb, const double* __restrict__ cvis, int chunks_v, long v,
+                                   long ldv, float* __restrict__ vb, double s, uint64_t* __restrict__ dctr) {
+    grid_dep_wait();
+    const long j = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (dctr && j == 0) dctr[0] += 1;  // the step is done: the next one reads its rows / counter
     if (j < h) {
-#pragma unroll 4
-        for (long i = ty; i < 2 * b; i += 16) ah += tf<T>(pn[i * ldh + j]);
+        double a = 0.0;
+        for (int k = 0; k < chunks_h; ++k) a += cpn[k * ldh + j];
+        hb[j] = static_cast<float>(hb[j] + s * a);
     }
     if (j < v) {
-#pragma unroll 4
-        for (long i = ty; i < b; i += 16) av += tf<T>(xr[i * ldv + j]) - tf<T>(xr[(b + i) * ldv + j]);
-    }
-    red[0][ty][tx] = ah;
-    red[1][ty][tx] = av;
-    __syncthreads();
-    if (ty < 2) {  // ty 0: hidden bias, ty 1: visible bias
-        float acc = 0.f;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) acc += red[ty][k][tx];
-        if (ty == 0 && j < h) hb[j] += s * acc;
-        if (ty == 1 && j < v) vb[j] += s * acc;
+        double a = 0.0;
+        for (int k = 0; k < chunks_v; ++k) a += cvis[k * ldv + j];
+        vb[j] = static_cast<float>(vb[j] + s * a);
     }
 }
 
 template <typename T>
 __global__ void load_rows_kernel(const float* __restrict__ src, long lds, const uint32_t* __restrict__ rows, long b,
-                                 long d, T* __restrict__ dst, long ldd) {
+                                 long d, T* __restrict__ dst, long ldd, const uint64_t* __restrict__ dstep) {
+    grid_dep_wait();
+    if (dstep) rows += dstep[0] * b;  // graph-launched steps: this step's slice of the shuffled order
     const long total = b * ldd;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
         const long r = i / ldd, c = i % ldd;
         const long sr = rows ? rows[r] : r;
         dst[i] = static_cast<T>(c < d ? src[sr * lds + c] : 0.f);
-    }
-}
-
-template <typename T>
-__global__ void store_rows_kernel(const T* __restrict__ src, long lds, long b, long d, float* __restrict__ dst,
-                                  long ldd) {
-    const long total = b * ldd;
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-        const long r = i / ldd, c = i % ldd;
-        dst[i] = c < d ? tf<T>(src[r * lds + c]) : 0.f;
     }
 }
 
@@ -148,12 +247,6 @@ __global__ void sqerr_kernel(const T* __restrict__ xr, long ldv, long B, long b,
         __syncthreads();
     }
     if (threadIdx.x == 0) out[blockIdx.x] += sh[0];
-}
-
-template <typename T>
-__global__ void copy_rows_kernel(const T* __restrict__ src, long lds, long b, long d, T* __restrict__ dst, long ldd) {
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < b * d; i += (long)gridDim.x * blockDim.x)
-        dst[(i / d) * ldd + (i % d)] = src[(i / d) * lds + (i % d)];
 }
 
 int grid_of(long total) { return (int)std::max<long>(1, std::min<long>((total + 255) / 256, 148L * 8)); }
@@ -181,11 +274,16 @@ RbmDevice::RbmDevice(Context* c, long visible, long hidden, bool g, long batch, 
     CUDA_THROW(cudaMemset(HS, 0, B * ldh * es));
     u_dev = dalloc<double>(B * h);
     red = dalloc<double>(1024);
+    const long chunks = (B + 7) / 8;
+    colp = dalloc<double>(chunks * (ldh + ldv));
+    ZP = dalloc<float>(B * ldh);
+    dctr = dalloc<uint64_t>(2);
 }
 
 RbmDevice::~RbmDevice() {
     if (stream) cudaStreamSynchronize(stream);
-    for (void* p : {(void*)W, (void*)Ws, (void*)vb, (void*)hb, XR, PN, HS, (void*)u_dev, (void*)red})
+    for (void* p : {(void*)W, (void*)Ws, (void*)vb, (void*)hb, XR, PN, HS, (void*)u_dev, (void*)red, (void*)part,
+                    (void*)colp, (void*)ZP, (void*)dctr})
         if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
 }
@@ -196,9 +294,9 @@ void RbmDevice::set_params(const double* p) {
         for (long c = 0; c < v; ++c) w[r * ldv + c] = static_cast<float>(p[r * v + c]);
     for (long j = 0; j < v; ++j) b1[j] = static_cast<float>(p[h * v + j]);
     for (long j = 0; j < h; ++j) b2[j] = static_cast<float>(p[h * v + v + j]);
-    CUDA_THROW(cudaMemcpy(W, w.data(), w.size() * 4, cudaMemcpyHostToDevice));
-    CUDA_THROW(cudaMemcpy(vb, b1.data(), b1.size() * 4, cudaMemcpyHostToDevice));
-    CUDA_THROW(cudaMemcpy(hb, b2.data(), b2.size() * 4, cudaMemcpyHostToDevice));
+    upload(W, w.data(), w.size() * 4);
+    upload(vb, b1.data(), b1.size() * 4);
+    upload(hb, b2.data(), b2.size() * 4);
     if (Ws) launch_f32_to_bf16_rows(W, ldv, h, v, Ws, stream);
     CUDA_THROW(cudaStreamSynchronize(stream));
 }
@@ -215,6 +313,37 @@ void RbmDevice::get_params(double* p) {
     for (long j = 0; j < h; ++j) p[h * v + v + j] = b2[j];
 }
 
+namespace {
+// split-K factor of an M = b CD-1 GEMM with BN = 128 tiles: about one CTA per SM,
+// at least two k-blocks per split (gemm_plan rounds it so no split is empty)
+int cd1_ksplit(int prec, long M, long N, long K, int sms) {
+    const long tiles = ((M + 127) / 128) * ((N + 127) / 128);
+    const long nk = (K + (prec ? 31 : 63)) / (prec ? 32 : 64);
+    return static_cast<int>(std::max<long>(1, std::min<long>(sms / tiles, nk / 2)));
+}
+
+int row_chunks(long b) { return static_cast<int>((b + 7) / 8); }  // grid.y of the reductions: a row per thread
+
+// Launch with programmatic stream serialization: the kernel is scheduled while
+// its predecessor drains and waits for it in griddepcontrol.wait (every kernel
+// launched this way starts with grid_dep_wait()).
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_THROW(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+}
+
+PartIn part_of(const GemmPlan& g) { return PartIn{g.ep.out32, g.ep.split_stride, g.ep.ld_out32, g.ep.ksplit}; }
+}  // namespace
+
 void RbmDevice::plan(long b) {
     if (b == planned_b) return;
     if (b > B) throw std::runtime_error("cd1_gibbs: batch larger than the RBM's buffers");
@@ -224,24 +353,25 @@ void RbmDevice::plan(long b) {
     char* xr = static_cast<char*>(XR);
     char* pn = static_cast<char*>(PN);
     const int sms = ctx->num_sms;
-    GemmEpi e;
-    e.mode = EPI_FWD_ACT;
-    e.act = 0;
-    e.bias = hb;
-    e.out = pn;
-    e.ld_out = ldh;
-    gemm_plan(g_pos, prec, false, xr, ldv, false, Wop, ldv, (int)b, (int)h, (int)v, e, sms);
-    GemmEpi r;
-    r.mode = EPI_FWD_ACT;
-    r.act = gaussian ? 2 : 0;  // reconstruct_mean: linear for gaussian visibles
-    r.bias = vb;
-    r.out = xr + b * ldv * es;
-    r.ld_out = ldv;
-    gemm_plan(g_recon, prec, false, HS, ldh, true, Wop, ldv, (int)b, (int)v, (int)h, r, sms);
-    GemmEpi n = e;
-    n.out_scale = -1.f;
-    n.out = pn + b * ldh * es;
-    gemm_plan(g_neg, prec, false, xr + b * ldv * es, ldv, false, Wop, ldv, (int)b, (int)h, (int)v, n, sms);
+    const int kp = cd1_ksplit(prec, b, h, v, sms), kr = cd1_ksplit(prec, b, v, h, sms);
+    const size_t need = std::max(static_cast<size_t>(kp) * b * ldh, static_cast<size_t>(kr) * b * ldv);
+    if (need > part_n) {
+        if (part) CUDA_THROW(cudaFree(part));
+        CUDA_THROW(cudaMalloc(&part, need * 4));
+        part_n = need;
+    }
+    auto split = [&](GemmPlan& g, bool b_mn, const void* A, long lda, int N, int K, int ks, long ld) {
+        GemmEpi e;
+        e.mode = EPI_PARTIAL;
+        e.out32 = part;
+        e.ld_out32 = ld;
+        e.split_stride = b * ld;
+        e.ksplit = ks;
+        gemm_plan(g, prec, false, A, lda, b_mn, Wop, ldv, static_cast<int>(b), N, K, e, sms, 128);
+    };
+    split(g_pos, false, xr, ldv, static_cast<int>(h), static_cast<int>(v), kp, ldh);             // X W^T
+    split(g_recon, true, HS, ldh, static_cast<int>(v), static_cast<int>(h), kr, ldv);            // hs W
+    split(g_neg, false, xr + b * ldv * es, ldv, static_cast<int>(h), static_cast<int>(v), kp, ldh);  // recon W^T
     GemmEpi u;
     u.mode = EPI_AXPY;
     u.out32 = W;
@@ -249,33 +379,66 @@ void RbmDevice::plan(long b) {
     u.shadow = Ws;
     u.ld_shadow = ldv;
     gemm_plan(g_upd, prec, true, pn, ldh, true, xr, ldv, (int)h, (int)v, (int)(2 * b), u, sms);
+    ch_h = ch_v = row_chunks(b);
     planned_b = b;
 }
 
+namespace {
+template <typename T>
+void launch_pos(RbmDevice& r, long rows, int mode, uint64_t seed, uint64_t counter, float* out32, long ld32,
+                const uint64_t* dctr = nullptr) {
+    const dim3 grid(static_cast<unsigned>((r.h + 31) / 32), r.ch_h), block(32, 8);
+    launch_pdl(cd1_pos_kernel<T>, grid, block, r.stream, part_of(r.g_pos), rows, r.h, r.hb, static_cast<T*>(r.PN),
+               r.ldh, mode == 4 ? nullptr : static_cast<T*>(r.HS), mode, seed, counter, r.u_dev,
+               mode < 3 ? r.ZP : nullptr, out32, ld32, dctr);
+}
+
+template <typename T>
+void launch_recon(RbmDevice& r, long rows, double* colpart) {
+    const dim3 grid(static_cast<unsigned>((r.v + 31) / 32), r.ch_v), block(32, 8);
+    T* xr = static_cast<T*>(r.XR);
+    launch_pdl(cd1_recon_kernel<T>, grid, block, r.stream, part_of(r.g_recon), rows, r.v, r.vb, r.gaussian, xr, r.ldv,
+               xr + r.planned_b * r.ldv, colpart);
+}
+
+// one CD-1 update (pretrain.cpp:79-121): 3 split-K GEMMs each followed by its
+// fused reduction, the rank-2b weight update, the bias update
+template <typename T>
+// dctr: graph-captured steps read the Philox counter from {step, base} and the
+// last kernel advances the step
+void run_cd1(RbmDevice& r, long b, double lr, int sampling, uint64_t seed, uint64_t counter,
+             uint64_t* dctr = nullptr) {
+    cudaStream_t s = r.stream;
+    double* cpn = r.colp;
+    double* cvis = cpn + r.ch_h * r.ldh;
+    gemm_launch(r.g_pos, s);
+    launch_pos<T>(r, b, sampling, seed, counter, nullptr, 0, dctr);
+    gemm_launch(r.g_recon, s);
+    launch_recon<T>(r, b, cvis);
+    gemm_launch(r.g_neg, s);
+    const dim3 grid(static_cast<unsigned>((r.h + 31) / 32), r.ch_h), block(32, 8);
+    launch_pdl(cd1_neg_kernel<T>, grid, block, s, part_of(r.g_neg), b, r.h, r.hb, r.ZP, static_cast<T*>(r.PN), r.ldh,
+               cpn);
+    const double scale = lr / static_cast<double>(b);
+    r.g_upd.ep.alpha = static_cast<float>(scale);
+    gemm_launch(r.g_upd, s);
+    const long wmax = std::max(r.v, r.h);
+    launch_pdl(bias_finish_kernel, dim3(static_cast<unsigned>((wmax + 255) / 256)), dim3(256), s, cpn, r.ch_h, r.h,
+               r.ldh, r.hb, cvis, r.ch_v, r.v, r.ldv, r.vb, scale, dctr);
+    CUDA_THROW(cudaGetLastError());
+}
+}  // namespace
+
 void RbmDevice::cd1(long b, double lr, int sampling, uint64_t seed, uint64_t counter) {
     plan(b);
-    cudaStream_t s = stream;
-    const bool F = f32();
-    gemm_launch(g_pos, s);
-    if (F)
-        sample_kernel<float><<<grid_of(b * h), 256, 0, s>>>(static_cast<float*>(PN), ldh, b, h, static_cast<float*>(HS),
-                                                            ldh, sampling, seed, counter, u_dev);
-    else
-        sample_kernel<bf16><<<grid_of(b * h), 256, 0, s>>>(static_cast<bf16*>(PN), ldh, b, h, static_cast<bf16*>(HS),
-                                                           ldh, sampling, seed, counter, u_dev);
-    gemm_launch(g_recon, s);
-    gemm_launch(g_neg, s);
-    const float scale = static_cast<float>(lr / static_cast<double>(b));
-    g_upd.ep.alpha = scale;
-    gemm_launch(g_upd, s);
-    const long wmax = std::max(v, h);
-    const dim3 bgrid(static_cast<unsigned>((wmax + 31) / 32)), bblock(32, 16);
-    if (F)
-        bias_update_kernel<float><<<bgrid, bblock, 0, s>>>(static_cast<float*>(PN), ldh, b, h, hb,
-                                                           static_cast<float*>(XR), ldv, v, vb, scale);
-    else
-        bias_update_kernel<bf16><<<bgrid, bblock, 0, s>>>(static_cast<bf16*>(PN), ldh, b, h, hb,
-                                                          static_cast<bf16*>(XR), ldv, v, vb, scale);
+    if (f32()) run_cd1<float>(*this, b, lr, sampling, seed, counter);
+    else run_cd1<bf16>(*this, b, lr, sampling, seed, counter);
+}
+
+void RbmDevice::hidden_probs_rows(long rows, float* out32, long ld32) {
+    gemm_launch(g_pos, stream);
+    if (f32()) launch_pos<float>(*this, rows, 4, 0, 0, out32, ld32);
+    else launch_pos<bf16>(*this, rows, 4, 0, 0, out32, ld32);
     CUDA_THROW(cudaGetLastError());
 }
 
@@ -288,9 +451,11 @@ void upload_rows(RbmDevice& r, const double* x, long b, long d, long ld, void* d
     CUDA_THROW(cudaMalloc(&tmp, hbuf.size() * 4));
     CUDA_THROW(cudaMemcpyAsync(tmp, hbuf.data(), hbuf.size() * 4, cudaMemcpyHostToDevice, r.stream));
     if (r.f32())
-        load_rows_kernel<float><<<grid_of(b * ld), 256, 0, r.stream>>>(tmp, ld, nullptr, b, d, static_cast<float*>(dst), ld);
+        load_rows_kernel<float><<<grid_of(b * ld), 256, 0, r.stream>>>(tmp, ld, nullptr, b, d, static_cast<float*>(dst), ld,
+                                                                        nullptr);
     else
-        load_rows_kernel<bf16><<<grid_of(b * ld), 256, 0, r.stream>>>(tmp, ld, nullptr, b, d, static_cast<bf16*>(dst), ld);
+        load_rows_kernel<bf16><<<grid_of(b * ld), 256, 0, r.stream>>>(tmp, ld, nullptr, b, d, static_cast<bf16*>(dst), ld,
+                                                                       nullptr);
     CUDA_THROW(cudaStreamSynchronize(r.stream));
     cudaFree(tmp);
 }
@@ -309,28 +474,24 @@ void RbmDevice::cd1_host(const double* batch, long b, double lr, int sampling, u
 }
 
 void RbmDevice::hidden_probs_host(const double* x, long n, double* out) {
-    const size_t es = f32() ? 4 : 2;
     std::vector<float> tmp(B * ldh);
     float* d32 = nullptr;
     CUDA_THROW(cudaMalloc(&d32, B * ldh * 4));
+    plan(B);
     for (long c0 = 0; c0 < n; c0 += B) {
         const long cb = std::min(B, n - c0);
         upload_rows(*this, x + c0 * v, cb, v, ldv, XR);
-        plan(B);
-        gemm_launch(g_pos, stream);
-        if (f32())
-            store_rows_kernel<float><<<grid_of(cb * ldh), 256, 0, stream>>>(static_cast<float*>(PN), ldh, cb, h, d32, ldh);
-        else
-            store_rows_kernel<bf16><<<grid_of(cb * ldh), 256, 0, stream>>>(static_cast<bf16*>(PN), ldh, cb, h, d32, ldh);
+        hidden_probs_rows(cb, d32, ldh);
         CUDA_THROW(cudaMemcpyAsync(tmp.data(), d32, cb * ldh * 4, cudaMemcpyDeviceToHost, stream));
         CUDA_THROW(cudaStreamSynchronize(stream));
         for (long i = 0; i < cb; ++i)
             for (long j = 0; j < h; ++j) out[(c0 + i) * h + j] = tmp[i * ldh + j];
     }
-    (void)es;
     cudaFree(d32);
 }
 
+// pretrain.cpp:127-136: mean-field pass (hs = pos), squared error of the
+// reconstruction over the first cb rows
 double RbmDevice::reconstruction_error_host(const double* x, long n) {
     if (n <= 0) throw std::runtime_error("reconstruction_error: empty batch");
     CUDA_THROW(cudaMemsetAsync(red, 0, 8 * 64, stream));
@@ -340,14 +501,14 @@ double RbmDevice::reconstruction_error_host(const double* x, long n) {
         upload_rows(*this, x + c0 * v, cb, v, ldv, XR);
         gemm_launch(g_pos, stream);
         if (f32()) {
-            copy_rows_kernel<float><<<grid_of(cb * h), 256, 0, stream>>>(static_cast<float*>(PN), ldh, cb, h,
-                                                                         static_cast<float*>(HS), ldh);
+            launch_pos<float>(*this, cb, 3, 0, 0, nullptr, 0);
             gemm_launch(g_recon, stream);
+            launch_recon<float>(*this, cb, nullptr);
             sqerr_kernel<float><<<64, 256, 0, stream>>>(static_cast<float*>(XR), ldv, B, cb, v, red);
         } else {
-            copy_rows_kernel<bf16><<<grid_of(cb * h), 256, 0, stream>>>(static_cast<bf16*>(PN), ldh, cb, h,
-                                                                        static_cast<bf16*>(HS), ldh);
+            launch_pos<bf16>(*this, cb, 3, 0, 0, nullptr, 0);
             gemm_launch(g_recon, stream);
+            launch_recon<bf16>(*this, cb, nullptr);
             sqerr_kernel<bf16><<<64, 256, 0, stream>>>(static_cast<bf16*>(XR), ldv, B, cb, v, red);
         }
     }
@@ -364,9 +525,12 @@ double RbmDevice::reconstruction_error_host(const double* x, long n) {
 // the b*h Bernoulli draws the reference takes from that same stream per batch
 // are skipped with an xoshiro256** GF(2) jump, while the device draws its own
 // counter-based Philox uniforms.
+thread_local PretrainStats g_pretrain_stats;
+
 void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* data, long n, uint64_t epochs,
                      double lr_g, double lr_b, long batch, host::Rng& rng, uint64_t philox_seed, Precision prec,
                      double* out) {
+    g_pretrain_stats = PretrainStats();
     if (dims.size() < 2) throw std::runtime_error("greedy_pretrain: need at least 2 dims");
     if (batch <= 0) throw std::runtime_error("greedy_pretrain: batch size must be >= 1");
     if (n <= 0) throw std::runtime_error("cd1_gibbs: empty batch");
@@ -378,7 +542,7 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
         for (long i = 0; i < n; ++i)
             for (long j = 0; j < d0; ++j) hx[i * ld0 + j] = static_cast<float>(data[i * d0 + j]);
         CUDA_THROW(cudaMalloc(&X, hx.size() * 4));
-        CUDA_THROW(cudaMemcpy(X, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice));
+        upload(X, hx.data(), hx.size() * 4);
     }
     uint32_t* d_idx = nullptr;
     CUDA_THROW(cudaMalloc(&d_idx, n * 4));
@@ -396,24 +560,68 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
         const host::Jump skip = host::make_jump(static_cast<uint64_t>(bs) * static_cast<uint64_t>(h));
         const long ldx = pad32(v);
         std::vector<uint32_t> idx(n);
+        // The epoch's CD-1 steps run as CUDA graphs of kGraphSteps steps (and
+        // single-step graphs for the remainder): launched one kernel at a time the
+        // step is bound by host launch submission (~3.7 us per launch against
+        // ~0.6 us per graph node). The steps read their slice of the shuffled
+        // order and their Philox counter from rbm.dctr = {step, base}.
+        rbm.plan(bs);
+        const long steps = n / bs;
+        constexpr long kGraphSteps = 32;
+        auto capture = [&](long nsteps) {
+            cudaGraph_t g = nullptr;
+            cudaGraphExec_t ge = nullptr;
+            CUDA_THROW(cudaStreamBeginCapture(rbm.stream, cudaStreamCaptureModeThreadLocal));
+            for (long k = 0; k < nsteps; ++k) {
+                const dim3 gr(static_cast<unsigned>(grid_of(bs * ldx))), t(256);
+                if (rbm.f32()) {
+                    launch_pdl(load_rows_kernel<float>, gr, t, rbm.stream, X, ldx, d_idx, bs, v,
+                               static_cast<float*>(rbm.XR), ldx, static_cast<const uint64_t*>(rbm.dctr));
+                    run_cd1<float>(rbm, bs, lr, 0, philox_seed, 0, rbm.dctr);
+                } else {
+                    launch_pdl(load_rows_kernel<bf16>, gr, t, rbm.stream, X, ldx, d_idx, bs, v,
+                               static_cast<bf16*>(rbm.XR), ldx, static_cast<const uint64_t*>(rbm.dctr));
+                    run_cd1<bf16>(rbm, bs, lr, 0, philox_seed, 0, rbm.dctr);
+                }
+            }
+            CUDA_THROW(cudaStreamEndCapture(rbm.stream, &g));
+            CUDA_THROW(cudaGraphInstantiate(&ge, g, 0));
+            CUDA_THROW(cudaGraphDestroy(g));
+            return ge;
+        };
+        cudaGraphExec_t gbig = steps >= kGraphSteps ? capture(kGraphSteps) : nullptr;
+        cudaGraphExec_t gone = steps % kGraphSteps ? capture(1) : nullptr;
+        uint64_t hctr[2];
+        cudaEvent_t t0, t1;
+        CUDA_THROW(cudaEventCreate(&t0));
+        CUDA_THROW(cudaEventCreate(&t1));
+        CUDA_THROW(cudaEventRecord(t0, rbm.stream));
         for (uint64_t ep = 0; ep < epochs; ++ep) {
             std::vector<uint64_t> order(n);
             for (long i = 0; i < n; ++i) order[i] = static_cast<uint64_t>(i);
             rng.shuffle(order);  // feature_batches (pretrain.cpp:141-158)
+            CUDA_THROW(cudaStreamSynchronize(rbm.stream));  // idx / hctr of the previous epoch are free
             for (long i = 0; i < n; ++i) idx[i] = static_cast<uint32_t>(order[i]);
+            hctr[0] = 0;
+            hctr[1] = counter;
             CUDA_THROW(cudaMemcpyAsync(d_idx, idx.data(), n * 4, cudaMemcpyHostToDevice, rbm.stream));
-            for (long b = 0; b < n / bs; ++b) {
-                if (rbm.f32())
-                    load_rows_kernel<float><<<grid_of(bs * ldx), 256, 0, rbm.stream>>>(
-                        X, ldx, d_idx + b * bs, bs, v, static_cast<float*>(rbm.XR), ldx);
-                else
-                    load_rows_kernel<bf16><<<grid_of(bs * ldx), 256, 0, rbm.stream>>>(
-                        X, ldx, d_idx + b * bs, bs, v, static_cast<bf16*>(rbm.XR), ldx);
-                rbm.cd1(bs, lr, 0, philox_seed, counter);
-                counter += static_cast<uint64_t>(bs) * static_cast<uint64_t>(h);
-                rng.jump(skip);
-            }
+            CUDA_THROW(cudaMemcpyAsync(rbm.dctr, hctr, sizeof(hctr), cudaMemcpyHostToDevice, rbm.stream));
+            for (long k = 0; k + kGraphSteps <= steps; k += kGraphSteps) CUDA_THROW(cudaGraphLaunch(gbig, rbm.stream));
+            for (long k = 0; k < steps % kGraphSteps; ++k) CUDA_THROW(cudaGraphLaunch(gone, rbm.stream));
+            counter += static_cast<uint64_t>(steps) * static_cast<uint64_t>(bs) * static_cast<uint64_t>(h);
+            for (long k = 0; k < steps; ++k) rng.jump(skip);  // the reference's b*h sample_bernoulli draws
         }
+        CUDA_THROW(cudaEventRecord(t1, rbm.stream));
+        CUDA_THROW(cudaStreamSynchronize(rbm.stream));
+        float ms = 0.f;
+        CUDA_THROW(cudaEventElapsedTime(&ms, t0, t1));  // device span of the epochs (host shuffles overlap it)
+        g_pretrain_stats.cd1_seconds += ms * 1e-3;
+        g_pretrain_stats.cd1_steps += static_cast<uint64_t>(steps) * epochs;
+        g_pretrain_stats.cd1_flop += 10.0 * v * h * static_cast<double>(bs) * steps * epochs;
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        if (gbig) CUDA_THROW(cudaGraphExecDestroy(gbig));
+        if (gone) CUDA_THROW(cudaGraphExecDestroy(gone));
         // next layer input: hidden probabilities over the whole data (pretrain.cpp:190)
         const long ldh = pad32(h);
         float* Xn = nullptr;
@@ -423,17 +631,11 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
             const long cb = std::min(bs, n - c0);
             if (rbm.f32())
                 load_rows_kernel<float><<<grid_of(cb * ldx), 256, 0, rbm.stream>>>(X + c0 * ldx, ldx, nullptr, cb, v,
-                                                                                static_cast<float*>(rbm.XR), ldx);
+                                                                                static_cast<float*>(rbm.XR), ldx, nullptr);
             else
                 load_rows_kernel<bf16><<<grid_of(cb * ldx), 256, 0, rbm.stream>>>(X + c0 * ldx, ldx, nullptr, cb, v,
-                                                                               static_cast<bf16*>(rbm.XR), ldx);
-            gemm_launch(rbm.g_pos, rbm.stream);
-            if (rbm.f32())
-                store_rows_kernel<float><<<grid_of(cb * ldh), 256, 0, rbm.stream>>>(static_cast<float*>(rbm.PN), ldh, cb,
-                                                                                 h, Xn + c0 * ldh, ldh);
-            else
-                store_rows_kernel<bf16><<<grid_of(cb * ldh), 256, 0, rbm.stream>>>(static_cast<bf16*>(rbm.PN), ldh, cb, h,
-                                                                                Xn + c0 * ldh, ldh);
+                                                                               static_cast<bf16*>(rbm.XR), ldx, nullptr);
+            rbm.hidden_probs_rows(cb, Xn + c0 * ldh, ldh);
         }
         CUDA_THROW(cudaStreamSynchronize(rbm.stream));
         cudaFree(X);

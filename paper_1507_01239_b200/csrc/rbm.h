@@ -23,6 +23,12 @@ struct RbmDevice {
     void* HS = nullptr;  // [B x ldh] op dtype: hidden samples
     double* u_dev = nullptr;  // injected uniforms [B x h]
     double* red = nullptr;    // reduction scratch
+    float* part = nullptr;    // split-K partial tiles of the M = b GEMMs
+    size_t part_n = 0;
+    double* colp = nullptr;   // per-row-chunk column sums: pos - neg [ch_h x ldh], v - recon [ch_v x ldv]
+    float* ZP = nullptr;      // [B x ldh] pre-activations of the pos pass (for the fp64 pos - neg)
+    uint64_t* dctr = nullptr; // {step, Philox counter base} of graph-launched CD-1 steps
+    int ch_h = 1, ch_v = 1;   // row chunks (grid.y) of the h- and v-wide reductions
     long planned_b = -1;
     GemmPlan g_pos, g_recon, g_neg, g_upd;
 
@@ -36,9 +42,20 @@ struct RbmDevice {
     void cd1(long b, double lr, int sampling, uint64_t seed, uint64_t counter);
     void cd1_host(const double* batch, long b, double lr, int sampling, uint64_t seed, uint64_t counter,
                   const double* u);
+    // hidden probabilities of the first `rows` rows in XR -> out32 (fp32, ld32)
+    void hidden_probs_rows(long rows, float* out32, long ld32);
     void hidden_probs_host(const double* x, long n, double* out);
     double reconstruction_error_host(const double* x, long n);
 };
+
+// Device time of the last greedy_pretrain's CD-1 epochs on this thread (events
+// around each layer's epoch loop), its step count and 10 v h b flop per step.
+struct PretrainStats {
+    double cd1_seconds = 0.0;
+    uint64_t cd1_steps = 0;
+    double cd1_flop = 0.0;
+};
+extern thread_local PretrainStats g_pretrain_stats;
 
 // rng: the caller's generator, advanced exactly as the reference advances it;
 // philox_seed keys the device Bernoulli draws.

@@ -118,8 +118,8 @@ DeviceDataset::DeviceDataset(Context* c, const double* x, const int32_t* labels,
                                      " out of range [0, " + std::to_string(classes) + ")");
     x32 = dalloc<float>(h.size());
     y = dalloc<int32_t>(n);
-    CUDA_THROW(cudaMemcpy(x32, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
-    CUDA_THROW(cudaMemcpy(y, labels, n * 4, cudaMemcpyHostToDevice));
+    upload(x32, h.data(), h.size() * 4);
+    upload(y, labels, n * 4);
 }
 
 DeviceDataset::DeviceDataset(Context* c, long n_, long d_, long classes_)
@@ -287,7 +287,7 @@ void Replica::set_params(const double* flat) {
     CUDA_THROW(cudaSetDevice(ctx->device));
     CUDA_THROW(cudaStreamSynchronize(stream));
     CUDA_THROW(cudaStreamSynchronize(ctx->avg));
-    CUDA_THROW(cudaMemcpy(params, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    upload(params, h.data(), h.size() * 4);
     sync_shadow(stream);
     CUDA_THROW(cudaStreamSynchronize(stream));
 }
@@ -333,12 +333,12 @@ void Replica::set_ng_state(const double* f, long t) {
             std::vector<float> h(static_cast<size_t>(n * ld), 0.f);
             for (long i = 0; i < n; ++i)
                 for (long j = 0; j < n; ++j) h[i * ld + j] = static_cast<float>(f[pos++]);
-            CUDA_THROW(cudaMemcpy(side == 0 ? r_in[l] : r_out[l], h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+            upload(side == 0 ? r_in[l] : r_out[l], h.data(), h.size() * 4);
         }
     }
     ng_t = t;
     long tt = t;
-    CUDA_THROW(cudaMemcpy(reinterpret_cast<char*>(scal) + 8 * (16 * (L + 1) + 500), &tt, 8, cudaMemcpyHostToDevice));
+    upload(reinterpret_cast<char*>(scal) + 8 * (16 * (L + 1) + 500), &tt, 8);
 }
 
 void Replica::bind(DeviceDataset* ds) {
@@ -1075,7 +1075,7 @@ double Replica::accuracy(DeviceDataset* ds) {
         eval_rows = dalloc<uint32_t>(ds->n);
         std::vector<uint32_t> h(ds->n);
         for (long i = 0; i < ds->n; ++i) h[i] = static_cast<uint32_t>(i);
-        CUDA_THROW(cudaMemcpy(eval_rows, h.data(), ds->n * 4, cudaMemcpyHostToDevice));
+        upload(eval_rows, h.data(), ds->n * 4);
         eval_rows_n = ds->n;
     }
     uint32_t* rows = eval_rows;

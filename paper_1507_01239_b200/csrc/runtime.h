@@ -25,6 +25,14 @@ namespace pnb {
 
 using bf16 = __nv_bfloat16;
 
+// Blocking host -> device upload. cudaMemcpy from pageable memory may return
+// before its DMA has landed, and the legacy stream it runs on does not order
+// the non-blocking streams every kernel here is launched on: wait for it.
+inline void upload(void* dst, const void* src, size_t bytes) {
+    CUDA_THROW(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    CUDA_THROW(cudaStreamSynchronize(cudaStreamLegacy));
+}
+
 struct GemmPlan {
     CUtensorMap ta, tb;
     dim3 grid;

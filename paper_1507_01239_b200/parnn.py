@@ -679,6 +679,14 @@ def greedy_pretrain(dims, data, opts: PretrainOptions = PretrainOptions(), activ
     return MlpModel(list(map(int, dims)), Activation(activation), out)
 
 
+def pretrain_last_stats() -> dict:
+    """Device time of the last greedy_pretrain's CD-1 epochs on this thread
+    (CUDA events around each layer's epoch loop), step count and flop."""
+    sec, steps, flop = C.c_double(), C.c_uint64(), C.c_double()
+    check(lib().parnn_pretrain_last_stats(C.byref(sec), C.byref(steps), C.byref(flop)))
+    return {"cd1_device_seconds": sec.value, "cd1_steps": steps.value, "cd1_flop": flop.value}
+
+
 # ------------------------------------------------------------ test hooks
 EPI = {"fwd_act": 0, "fwd_linear": 1, "grad": 2, "grad_sgd": 3, "actgrad": 4, "ema": 5, "axpy": 6, "sub": 7,
        "partial": 8, "resid": 9}
