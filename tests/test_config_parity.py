@@ -125,3 +125,75 @@ def test_config2_one_period_vs_oracle(ctx, opt):
     assert max(lr_) < 1e-4, lr_
     assert rel(p - p0, ref - p0) < 2e-3
     assert np.abs(ce - rce).max() <= 1e-5 * np.abs(rce).max()
+
+
+# ---------------------------------------------------------------- NG-SGD runs
+def _ng_golden(name):
+    return dict(np.load(os.path.join(ROOT, "tests", "golden", name)))
+
+
+def _cfg1_ng_opts(g, **kw):
+    return P.TrainOptions(optimizer=P.OptimizerKind.ngsgd, lr_init=float(g.get("lr_init", 2.0)),
+                          epochs=int(g.get("epochs", 1)), precision=FP32, **kw)
+
+
+def test_config1_kron_ng_trajectory_matches_reference(ctx):
+    """Kron-full NG-SGD (optimizer.cpp:79-157) through a whole epoch (35 steps,
+    9 averaging events) of the config-1 network on 9000 frames, fp32 mode,
+    against the compiled reference (golden_cfg1_ng_small.npz): the epoch metrics
+    and 64 Rademacher projections of the parameter delta within 1e-4."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("mk", os.path.join(ROOT, "tests", "golden", "make_golden_cfg1_ng.py"))
+    mk = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mk)
+    g = _ng_golden("golden_cfg1_ng_small.npz")
+    tr, cv = P.make_data(1000, 440, 10, 16.0, 7, 0.10, 2, True)
+    m0 = P.init_random(CFG1_DIMS, seed=1)
+    res = P.train_parallel(P.ParallelPlan(1, 4, 256, 5), m0, tr, cv, _cfg1_ng_opts({"lr_init": 2.0, "epochs": 1}),
+                           ctx=ctx)
+    m, ref = res.metrics[0], g["met"][0]
+    assert (m.lr, m.avg_events) == (ref[1], ref[6])
+    assert abs(m.train_ce - ref[2]) <= 1e-5 * ref[2] and abs(m.cv_accuracy - ref[3]) <= 1e-9
+    d = (res.model.params - m0.params).astype(np.float32)
+    proj = mk.rng_projection(d.size) @ d
+    assert rel(proj, g["proj"]) < 1e-4, rel(proj, g["proj"])
+    assert abs(np.linalg.norm(res.model.params - m0.params) - float(g["delta_norm"])) < 1e-4 * float(g["delta_norm"])
+
+
+@pytest.fixture(scope="module")
+def cfg1_ng_runs(ctx):
+    """Config 1 (100 frames per class, 2 epochs, lr 2.0) with the kron-full NG
+    and with low-rank NG-SGD at update lag 1 and 4 (fp32 mode)."""
+    g = _ng_golden("golden_cfg1_ng.npz")
+    tr, cv = P.make_data(1000, 440, 100, float(g["separation"]), 7, 0.10, 2, True)
+    m0 = P.init_random(CFG1_DIMS, seed=1)
+    plan = P.ParallelPlan(1, 4, 256, 5)
+    out = {"golden": g}
+    for key, opt, lag in (("kron", P.OptimizerKind.ngsgd, 1), ("lag1", P.OptimizerKind.ngsgd_lowrank, 1),
+                          ("lag4", P.OptimizerKind.ngsgd_lowrank, 4)):
+        o = P.TrainOptions(optimizer=opt, lr_init=float(g["lr_init"]), epochs=int(g["epochs"]), precision=FP32,
+                           ng_update_lag=lag)
+        out[key] = P.train_parallel(plan, m0, tr, cv, o, ctx=ctx).metrics
+    return out
+
+
+def test_config1_kron_ng_full_run_matches_reference(cfg1_ng_runs):
+    """The whole 2-epoch config-1 kron-full NG run (702 steps) against the
+    compiled reference: per-epoch train CE within 0.1%, CV accuracy within 0.01."""
+    ref = cfg1_ng_runs["golden"]["met"]
+    for m, r in zip(cfg1_ng_runs["kron"], ref):
+        assert abs(m.train_ce - r[2]) <= 1e-3 * r[2], (m.train_ce, r[2])
+        assert abs(m.cv_accuracy - r[3]) <= 0.01
+
+
+def test_lowrank_update_lag_1_vs_4_config1(cfg1_ng_runs):
+    """Low-rank NG-SGD with the Fisher subspace refreshed immediately (lag 1,
+    Povey 2014) and 4 steps stale (lag 4, the B200 default that overlaps the
+    refresh with later steps): final train CE within 1% of each other, and no
+    worse than the reference's kron-full NG on the same run (+5%)."""
+    ce1, ce4 = cfg1_ng_runs["lag1"][-1].train_ce, cfg1_ng_runs["lag4"][-1].train_ce
+    ref = float(cfg1_ng_runs["golden"]["met"][-1][2])
+    assert abs(ce1 - ce4) <= 0.01 * ce1, (ce1, ce4)
+    assert max(ce1, ce4) <= 1.05 * ref, (ce1, ce4, ref)
+    for m in cfg1_ng_runs["lag1"] + cfg1_ng_runs["lag4"]:
+        assert m.cv_accuracy >= 0.99
