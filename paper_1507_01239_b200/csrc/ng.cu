@@ -135,8 +135,8 @@ __device__ __forceinline__ void trailing_update(float* S, int c0) {
 //
 // 256 threads; 4 panels of 32 columns. Per panel:
 //   A. warp 0 factors the 32x32 diagonal sub-block D: lane i keeps row i in
-//      registers; each step broadcasts column k through shared memory
-//      (one store, eight 16-byte broadcast loads) — the serial chain is short;
+//      registers, the 32 column steps fully unrolled; pivot and L[c][k]
+//      arrive by warp shuffle;
 //   B. rows below solve x D^T = a by forward substitution (one thread per row,
 //      D broadcast from shared memory);
 //   C. all 8 warps apply the rank-32 trailing update with register-tiled
@@ -150,7 +150,6 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(float* __restrict__ a, l
     extern __shared__ float sm[];
     float* S = sm;                 // [NB][LDS]  A -> L
     float* V = sm + NB * LDS;      // [NB][LDS]  L^-1
-    float* col = V + NB * LDS;     // [32] column broadcast (16-byte aligned)
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     PNB_CLK(0);
     {
@@ -174,25 +173,15 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(float* __restrict__ a, l
     for (int p = 0; p < NB / 32; ++p) {
         const int c0 = 32 * p;
         if (warp == 0) {
+            // lane i holds row i of the block; the column steps are unrolled so
+            // every register index is static, the pivot and L[c][k] come from the
+            // owning lanes by shuffle (no shared-memory round trips on the chain)
             float d[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c) d[c] = S[(c0 + lane) * LDS + c0 + c];
-#pragma unroll 1
+#pragma unroll
             for (int k = 0; k < 32; ++k) {
-                // dk = d[k] for a runtime k: 5-level select tree (depth 5, not a 32-long chain)
-                float s16[16], s8[8], s4[4], s2[2];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) s16[i] = (k & 16) ? d[i + 16] : d[i];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) s8[i] = (k & 8) ? s16[i + 8] : s16[i];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) s4[i] = (k & 4) ? s8[i + 4] : s8[i];
-#pragma unroll
-                for (int i = 0; i < 2; ++i) s2[i] = (k & 2) ? s4[i + 2] : s4[i];
-                const float dk = (k & 1) ? s2[1] : s2[0];
-                if (lane == k) col[32] = dk;
-                __syncwarp();
-                const float piv = col[32];
+                const float piv = __shfl_sync(0xffffffffu, d[k], k);
                 if (lane == 0 && c0 + k < b && (!(piv > 0.f) || !isfinite(piv))) {
                     if (atomicCAS(&err->chol_failed, 0, 1) == 0) {
                         err->chol_index = static_cast<int>(j + c0 + k);
@@ -201,23 +190,13 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(float* __restrict__ a, l
                 }
                 const float rs = rsqrtf(piv);  // 1/L_kk
                 const float lkk = piv * rs;
-                const float lik = lane > k ? dk * rs : (lane == k ? lkk : 0.f);
-                col[lane] = lik;
-                __syncwarp();
-                float cv[32];
+                const float lik = lane > k ? d[k] * rs : (lane == k ? lkk : 0.f);
+                d[k] = lik;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 f = reinterpret_cast<const float4*>(col)[q];
-                    cv[4 * q] = f.x; cv[4 * q + 1] = f.y; cv[4 * q + 2] = f.z; cv[4 * q + 3] = f.w;
+                for (int c = k + 1; c < 32; ++c) {
+                    // rows c <= lane: a_ic -= L_ik L_ck (columns above the diagonal are dropped)
+                    d[c] = fmaf(-lik, __shfl_sync(0xffffffffu, lik, c), d[c]);
                 }
-                // branch-free (select) updates: divergent predicated branches
-                // here cost ~30 cycles of reconvergence each
-#pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const float w = (c > k && c <= lane) ? lik : 0.f;
-                    d[c] = (c == k) ? lik : fmaf(-w, cv[c], d[c]);
-                }
-                __syncwarp();
             }
 #pragma unroll
             for (int c = 0; c < 32; ++c) S[(c0 + lane) * LDS + c0 + c] = c <= lane ? d[c] : 0.f;
@@ -251,18 +230,21 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(float* __restrict__ a, l
     // D. inverses of the four 32x32 diagonal sub-blocks, one warp each:
     //    lane owns column `lane`; x_i = (e - sum_{q<i} D[i][q] x_q) / D[i][i]
     if (warp < NB / 32) {
+        // right-looking: once x_i is known every later row's partial sum takes its
+        // term (independent FMAs) instead of a serial dot product per row
         const int c0 = 32 * warp;
-        float x[32];
+        float acc[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = (i == lane) ? 1.f : 0.f;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-            const float* dr = S + (c0 + i) * LDS + c0;
-            float acc = (i == lane) ? 1.f : 0.f;
+            const float xi = acc[i] / S[(c0 + i) * LDS + c0 + i];
+            acc[i] = xi;
 #pragma unroll
-            for (int q = 0; q < i; ++q) acc -= dr[q] * x[q];
-            x[i] = acc / dr[i];
+            for (int r = i + 1; r < 32; ++r) acc[r] = fmaf(-S[(c0 + r) * LDS + c0 + i], xi, acc[r]);
         }
 #pragma unroll
-        for (int i = 0; i < 32; ++i) V[(c0 + i) * LDS + c0 + lane] = x[i];
+        for (int i = 0; i < 32; ++i) V[(c0 + i) * LDS + c0 + lane] = acc[i];
     }
     __syncthreads();
     PNB_CLK(10);
