@@ -324,9 +324,18 @@ def run_ours(args, rank, world, local_rank):
     burst = pk["bf16_tflops"]
     sustained = pk.get("bf16_tflops_sustained", burst)
     achieved = (d_fl / d_n) / (d_ms / d_n / 1e3) / 1e12 if d_fl > 0 else None
-    # algorithmic bytes of one dW launch (avg over layers): fp32 W read + write, bf16 shadow
-    # write, and the two bf16 operands (B x dout, B x (din + 1))
-    dw_bytes = sum(10.0 * o * (i + 1) + 2.0 * B * (o + i + 1) for i, o in zip(DIMS[:-1], DIMS[1:])) / (len(DIMS) - 1)
+    # algorithmic bytes per launch of the dominant kind (avg over layers)
+    pairs = list(zip(DIMS[:-1], DIMS[1:]))
+    alg_bytes = {
+        # dW + SGD: fp32 W read + write, bf16 shadow write, the two bf16 operands (B x dout, B x (din + 1))
+        "gemm_dw_sgd": sum(10.0 * o * (i + 1) + 2.0 * B * (o + i + 1) for i, o in pairs) / len(pairs),
+        # forward: bf16 X (B x din) and W (dout x din) read, bf16 activations (B x dout) written;
+        # the output layer writes fp32 logits
+        "gemm_fwd": sum(2.0 * B * i + 2.0 * o * i + (4.0 if k == len(pairs) - 1 else 2.0) * B * o
+                        for k, (i, o) in enumerate(pairs)) / len(pairs),
+        # dA: bf16 dZ (B x dout) and W read, bf16 dA (B x din) written
+        "gemm_da": sum(2.0 * B * o + 2.0 * o * i + 2.0 * B * i for i, o in pairs[1:]) / max(1, len(pairs) - 1),
+    }
     # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "dominant_traffic.json")
@@ -340,7 +349,7 @@ def run_ours(args, rank, world, local_rank):
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
                 "frac": (achieved / burst) if achieved else None, "traffic": traffic,
                 "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
-                "algorithmic_bytes_per_launch": dw_bytes,
+                "algorithmic_bytes_per_launch": alg_bytes.get(dom),
                 "peak_source": f"{how} bf16_tflops (burst: each launch is timed alone in the eager profile)",
                 "launches_per_step": d_n, "ms_per_step": d_ms,
                 "note": ("tcgen05 GEMM region, algorithmic flops (2MNK per launch) / CUDA-event time of the region "
@@ -397,6 +406,40 @@ def run_ours(args, rank, world, local_rank):
                 "note": "like-for-like: the same NG-SGD algorithm as the reference arm (bf16 operands here)"}
         rk.close()
 
+    # ---- the kron-full NG in fp32 mode (3xTF32 everywhere: the mode pinned to the
+    # compiled reference over whole config-1 runs, tests/test_config_parity.py)
+    kron32 = None
+    if world == 1 and not args.no_kron:
+        rk = P.Replica(ctx, DIMS, precision=P.Precision.fp32, optimizer=P.OptimizerKind.ngsgd, minibatch=B,
+                       max_steps=8)
+        rk.set_params(m0.params)
+        rk.bind(ds)
+        rk.upload_epoch(rows[:8 * B], lrs[:8])
+        rk.step(2)
+        rk.sync()
+        kms32 = rk.time_steps(4) / 4
+        kron32 = {"optimizer": OPT_DESC["ngsgd"], "precision": "fp32 (3xTF32 operands and solves)",
+                  "value": B / (kms32 / 1e3), "unit": UNIT, "ms_per_step": kms32, "steps": 4,
+                  "timing": "CUDA events on the replica stream, graph launches"}
+        rk.close()
+
+    # ---- config-4 CD-1 pretraining (greedy_pretrain, pretrain.cpp:162-207) at the
+    # config's layer shapes: device time of the graph-launched CD-1 epochs
+    cd1 = None
+    if world == 1 and not args.no_cd1:
+        xs = np.random.default_rng(0).standard_normal((16384, DIMS[0]))
+        cdims = [DIMS[0], 2048, 2048, 2048, 10]
+        cd1 = {"workload": "greedy_pretrain 440-2048-2048-2048 (3 RBMs: 1 Gaussian-Bernoulli 440x2048, 2 Bernoulli "
+                           "2048x2048) on 16384 frames x 2 epochs, batch 128",
+               "flop_note": "10 v h flop per frame per RBM (SURVEY 8(d))"}
+        for pn in ("bf16", "tf32"):
+            pr = P.Precision[pn]
+            P.greedy_pretrain(cdims[:3], xs[:2048], P.PretrainOptions(1), seed=1, precision=pr, ctx=ctx)
+            P.greedy_pretrain(cdims, xs, P.PretrainOptions(2), seed=3, precision=pr, ctx=ctx)
+            st = P.pretrain_last_stats()
+            cd1[pn] = {"value": st["cd1_flop"] / st["cd1_device_seconds"] / 1e12, "unit": "TFLOP/s",
+                       "us_per_step": st["cd1_device_seconds"] / st["cd1_steps"] * 1e6, "steps": st["cd1_steps"]}
+
     kps = rep.kernels_per_step()
     events = -(-K // args.avg_frequency)
     avg_kernels = 0 if world == 1 else (len(DIMS) - 1) * (2 if prec == P.Precision.bf16 else 1)
@@ -417,6 +460,8 @@ def run_ours(args, rank, world, local_rank):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "ngsgd_kron_full": kron,
+        "ngsgd_kron_full_fp32": kron32,
+        "cd1_pretrain": cd1,
         "final_ce": float(ce[-1]),
         "convergence": conv,
         "data_gen_seconds": gen_s,
@@ -479,6 +524,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=600)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cd1", action="store_true", help="skip the config-4 CD-1 pretraining measurement")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn(sys.argv[1:], args.gpus))
