@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--precision", choices=["bf16", "tf32", "fp32"], default="tf32")
     ap.add_argument("--workers", type=int, default=1)
     ap.add_argument("--lr-init", type=float, default=0.32)
+    ap.add_argument("--separation", type=float, default=8.0)
     ap.add_argument("--dims", default="440,2048,2048,2048,2048,2048,2048,8806")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -45,7 +46,7 @@ def main():
     prec = P.Precision[args.precision]
 
     t0 = time.perf_counter()
-    train, cv = P.make_data(dims[-1], dims[0], args.per_class, 8.0, 1, 0.10, 2, True)
+    train, cv = P.make_data(dims[-1], dims[0], args.per_class, args.separation, 1, 0.10, 2, True)
     gen_s = time.perf_counter() - t0
     ctx = P.Context(0)
     opts = P.PretrainOptions()
@@ -55,6 +56,7 @@ def main():
     t0 = time.perf_counter()
     pre = P.greedy_pretrain(dims, train.features, opts, seed=11, precision=prec, ctx=ctx)
     pre_s = time.perf_counter() - t0
+    cd1_st = P.pretrain_last_stats()
     n = train.size()
     n_eff = n // opts.batch_size * opts.batch_size
     rbm_layers = list(zip(dims[:-2], dims[1:-1]))
@@ -67,6 +69,10 @@ def main():
         "pretrain_frames_per_s_per_layer": n_eff * opts.epochs * len(rbm_layers) / pre_s,
         "pretrain_tflops": flop / pre_s / 1e12,
         "pretrain_flop_note": "10 d_v d_h flop per frame per RBM (SURVEY 8(d))",
+        "pretrain_cd1_device_seconds": cd1_st["cd1_device_seconds"],
+        "pretrain_cd1_tflops_device": cd1_st["cd1_flop"] / cd1_st["cd1_device_seconds"] / 1e12,
+        "pretrain_cd1_us_per_step": cd1_st["cd1_device_seconds"] / cd1_st["cd1_steps"] * 1e6,
+        "separation": args.separation, "lr_init": args.lr_init,
     }
 
     topts = P.TrainOptions(optimizer=P.OptimizerKind.ngsgd_lowrank, lr_schedule=P.LrVariant.exponential,

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--per-class", type=int, default=128)
     ap.add_argument("--epochs", type=int, default=1)
     ap.add_argument("--lr-init", type=float, default=0.32)
+    ap.add_argument("--separation", type=float, default=8.0)
     ap.add_argument("--optimizer", choices=["ngsgd_lowrank", "ngsgd", "sgd"], default="ngsgd_lowrank")
     ap.add_argument("--precision", choices=["bf16", "tf32", "fp32"], default="bf16")
     ap.add_argument("--dims", default="440,2048,2048,2048,2048,2048,2048,8806")
@@ -46,7 +47,7 @@ def main():
     opts = P.TrainOptions(optimizer=P.OptimizerKind[args.optimizer], lr_schedule=P.LrVariant.exponential,
                           lr_init=args.lr_init, epochs=args.epochs, precision=P.Precision[args.precision])
     t0 = time.perf_counter()
-    base = S.RunConfig(dims=dims, per_class=args.per_class, separation=8.0, plan=P.ParallelPlan(args.workers, 4, 1024, 0),
+    base = S.RunConfig(dims=dims, per_class=args.per_class, separation=args.separation, plan=P.ParallelPlan(args.workers, 4, 1024, 0),
                        opts=opts)
     S._data(base)  # generate once (shared by every cell)
     gen_s = time.perf_counter() - t0
@@ -71,6 +72,7 @@ def main():
         f.write("\n".join([header] + lines) + "\n")
     info = {"workers": args.workers, "dims": dims, "per_class": args.per_class, "epochs": args.epochs,
             "optimizer": args.optimizer, "precision": args.precision, "lr_init": args.lr_init,
+            "separation": args.separation, "avg_frequencies": ks, "minibatches": bs,
             "data_gen_seconds": gen_s, "total_seconds": time.perf_counter() - t0,
             "note": "all workers are virtual replicas on one B200; frames_per_s = frames / training wall time"}
     with open(os.path.join(args.out, "info.json"), "w") as f:
