@@ -19,7 +19,7 @@ void* upload(const float* h, long rows, long cols, long ld, bool f32) {
     void* d = nullptr;
     const size_t es = f32 ? 4 : 2;
     CUDA_THROW(cudaMalloc(&d, static_cast<size_t>(rows * ld) * es + 256));
-    CUDA_THROW(cudaMemset(d, 0, static_cast<size_t>(rows * ld) * es + 256));
+    zero(d, static_cast<size_t>(rows * ld) * es + 256);
     if (f32) {
         CUDA_THROW(cudaMemcpy2D(d, ld * 4, h, cols * 4, cols * 4, rows, cudaMemcpyHostToDevice));
         CUDA_THROW(cudaStreamSynchronize(cudaStreamLegacy));

@@ -36,7 +36,7 @@ constexpr int LDS = NB + 1;  // padded shared-memory row
 float* dalloc_f(size_t n) {
     void* p = nullptr;
     CUDA_THROW(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(float)));
-    CUDA_THROW(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(float)));
+    zero(p, std::max<size_t>(n, 1) * sizeof(float));
     return static_cast<float*>(p);
 }
 

@@ -35,19 +35,19 @@ constexpr double kTiny = 1e-30;
 float* falloc(size_t n) {
     void* p = nullptr;
     CUDA_THROW(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(float)));
-    CUDA_THROW(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(float)));
+    zero(p, std::max<size_t>(n, 1) * sizeof(float));
     return static_cast<float*>(p);
 }
 double* dalloc_d(size_t n) {
     void* p = nullptr;
     CUDA_THROW(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(double)));
-    CUDA_THROW(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(double)));
+    zero(p, std::max<size_t>(n, 1) * sizeof(double));
     return static_cast<double*>(p);
 }
 void* valloc(size_t bytes) {
     void* p = nullptr;
     CUDA_THROW(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
-    CUDA_THROW(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+    zero(p, std::max<size_t>(bytes, 16));
     return p;
 }
 

@@ -170,7 +170,7 @@ Averager::Averager(Context* c, const std::vector<Replica*>& r, Comm* cm, long m)
     CUDA_THROW(cudaMalloc(&d_null_shadow, sizeof(bf16*)));
     upload(d_src, src.data(), k * sizeof(float*));
     upload(d_shadow, sh.data(), k * sizeof(bf16*));
-    CUDA_THROW(cudaMemset(d_null_shadow, 0, sizeof(bf16*)));
+    zero(d_null_shadow, sizeof(bf16*));
     work = comm != nullptr || k > 1;
     if (work)
         for (Replica* p : reps) p->precapture_gates();

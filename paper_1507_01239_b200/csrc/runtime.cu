@@ -17,7 +17,7 @@ T* dalloc(size_t n) {
     void* p = nullptr;
     if (n == 0) n = 1;
     CUDA_THROW(cudaMalloc(&p, n * sizeof(T)));
-    CUDA_THROW(cudaMemset(p, 0, n * sizeof(T)));
+    zero(p, n * sizeof(T));
     return static_cast<T*>(p);
 }
 

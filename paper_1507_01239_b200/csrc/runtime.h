@@ -32,6 +32,11 @@ inline void upload(void* dst, const void* src, size_t bytes) {
     CUDA_THROW(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
     CUDA_THROW(cudaStreamSynchronize(cudaStreamLegacy));
 }
+// Blocking zero fill (cudaMemset is asynchronous on the legacy stream; same hazard).
+inline void zero(void* dst, size_t bytes) {
+    CUDA_THROW(cudaMemset(dst, 0, bytes));
+    CUDA_THROW(cudaStreamSynchronize(cudaStreamLegacy));
+}
 
 struct GemmPlan {
     CUtensorMap ta, tb;
