@@ -152,9 +152,6 @@ void gemm_plan(GemmPlan& p, int prec, bool a_mn, const void* A, long lda, bool b
         fn = te ? gemm_pick_bf16_t(bn, a_mn, b_mn, &p.smem) : gemm_pick_bf16_r(bn, a_mn, b_mn, &p.smem);
     p.fn = reinterpret_cast<void*>(fn);
     p.bn = bn_eff;
-    if (ep.coop && (p.mc != 1 || ep.mode != EPI_PARTIAL || static_cast<long>(p.grid.x) != p.tiles || p.tiles > num_sms))
-        throw std::runtime_error("gemm: cooperative split-K needs single-CTA tiles, EPI_PARTIAL and one work item "
-                                 "per SM");
     p.threads = split ? 448 : 320;  // GemmSmem::kThreads
 }
 
@@ -180,7 +177,6 @@ dim3 gemm_launch_grid(const GemmPlan& p) {
     // the persistent kernel covers every tile with any grid (tile = blockIdx + k * gridDim;
     // CTA pairs: pair = blockIdx / 2 + k * gridDim / 2, so the grid stays even)
     if (p.mc == 3) return p.grid;  // one tile per cluster: the grid cannot shrink
-    if (p.ep.coop) return p.grid;  // cooperative split-K: every work item's CTA must be resident
     if (g_grid_cap > 0 && static_cast<int>(p.grid.x) > g_grid_cap)
         return dim3(p.mc == 2 ? std::max(2, g_grid_cap & ~1) : g_grid_cap, 1, 1);
     return p.grid;

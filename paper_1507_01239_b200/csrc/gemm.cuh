@@ -24,7 +24,6 @@
 
 #include <type_traits>
 
-#include "cd1_epi.cuh"
 #include "ptx.cuh"
 
 namespace pnb {
@@ -88,9 +87,6 @@ struct GemmEpi {
     int ksplit = 1;         // split-K factor (set by gemm_plan; every split non-empty)
     long split_stride = 0;  // PARTIAL: floats between the per-split outputs
     double* part = nullptr; // RESID: [gridDim.x][2] per-CTA {sum aux^2, sum out^2}
-    // PARTIAL with a device Cd1Epi: the splits of each tile reduce in-kernel and
-    // apply the CD-1 epilogue (cd1_epi.cuh); one work item per CTA
-    const void* coop = nullptr;
 };
 
 // Kernel parameters: NP problems (1, or up to kGroupMax for a grouped launch).
@@ -1011,14 +1007,6 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
             }
         }
         if (bad && ep.flag) atomicOr(ep.flag, 1u << ep.flag_bit);
-        if constexpr (MC == 1 && NP == 1) {
-            if (ep.coop) {  // cooperative split-K (one work item per CTA: tile w0)
-                const TileInfo ti = select(w0);
-                cd1_coop_finish<T>(static_cast<const Cd1Epi*>(ep.coop), ep.out32, ep.split_stride, ep.ld_out32,
-                                   ep.ksplit, M, N, BN, ti.m0, ti.n0, ti.ks, w0 % tiles_mn, w0 % tiles_m,
-                                   static_cast<int>(threadIdx.x) - 64, reinterpret_cast<double*>(smem));
-            }
-        }
         if (ep.mode == EPI_RESID) {
             // deterministic per-CTA sums: fixed tile order, fixed reduction tree
             __shared__ float red[2][8];

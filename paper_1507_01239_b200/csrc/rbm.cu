@@ -31,7 +31,30 @@ T* dalloc(size_t n) {
     return static_cast<T*>(p);
 }
 
-// philox_uniform: cd1_epi.cuh (shared with the in-GEMM CD-1 epilogue)
+__device__ __forceinline__ uint32_t mulhilo(uint32_t a, uint32_t b, uint32_t& hi) {
+    const uint64_t p = static_cast<uint64_t>(a) * b;
+    hi = static_cast<uint32_t>(p >> 32);
+    return static_cast<uint32_t>(p);
+}
+
+// Philox4x32-10 (Salmon et al. 2011), first output word -> uniform in [0,1).
+__device__ __forceinline__ float philox_uniform(uint64_t key, uint64_t ctr) {
+    uint32_t c0 = static_cast<uint32_t>(ctr), c1 = static_cast<uint32_t>(ctr >> 32), c2 = 0x5EED, c3 = 0xC0FFEE;
+    uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t hi0, hi1;
+        const uint32_t lo0 = mulhilo(0xD2511F53u, c0, hi0);
+        const uint32_t lo1 = mulhilo(0xCD9E8D57u, c2, hi1);
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return static_cast<float>(c0 >> 8) * (1.0f / 16777216.0f);
+}
 
 template <typename T>
 __device__ __forceinline__ float tf(T v) {
@@ -252,8 +275,7 @@ RbmDevice::RbmDevice(Context* c, long visible, long hidden, bool g, long batch, 
     u_dev = dalloc<double>(B * h);
     red = dalloc<double>(1024);
     const long chunks = (B + 7) / 8;
-    colp_n = static_cast<size_t>(chunks) * (ldh + ldv);
-    colp = dalloc<double>(colp_n);
+    colp = dalloc<double>(chunks * (ldh + ldv));
     ZP = dalloc<float>(B * ldh);
     dctr = dalloc<uint64_t>(2);
 }
@@ -261,8 +283,7 @@ RbmDevice::RbmDevice(Context* c, long visible, long hidden, bool g, long batch, 
 RbmDevice::~RbmDevice() {
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : {(void*)W, (void*)Ws, (void*)vb, (void*)hb, XR, PN, HS, (void*)u_dev, (void*)red, (void*)part,
-                    (void*)colp, (void*)ZP, (void*)dctr,
-                    (void*)d_cd1, (void*)ctrs})
+                    (void*)colp, (void*)ZP, (void*)dctr})
         if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
 }
@@ -358,88 +379,15 @@ void RbmDevice::plan(long b) {
     u.shadow = Ws;
     u.ld_shadow = ldv;
     gemm_plan(g_upd, prec, true, pn, ldh, true, xr, ldv, (int)h, (int)v, (int)(2 * b), u, sms);
-    // cooperative split-K: the row chunks of the fp64 column sums are (tile row, split)
-    const long tm = (b + 127) / 128;
-    ch_h = static_cast<int>(tm * g_neg.ep.ksplit);
-    ch_v = static_cast<int>(tm * g_recon.ep.ksplit);
-    const size_t need_c = std::max<size_t>(static_cast<size_t>(ch_h) * ldh + static_cast<size_t>(ch_v) * ldv,
-                                           static_cast<size_t>(row_chunks(B)) * (ldh + ldv));
-    if (need_c > colp_n) {
-        if (colp) CUDA_THROW(cudaFree(colp));
-        colp = dalloc<double>(need_c);
-        colp_n = need_c;
-    }
-    coop = coop_enabled() && static_cast<long>(g_pos.tiles) <= sms && static_cast<long>(g_recon.tiles) <= sms;
-    if (coop) {
-        const long tiles = std::max(g_pos.tiles / g_pos.ep.ksplit, g_recon.tiles / g_recon.ep.ksplit);
-        if (tiles > ctr_tiles) {
-            if (ctrs) CUDA_THROW(cudaFree(ctrs));
-            ctrs = dalloc<unsigned>(6 * tiles);
-            ctr_tiles = tiles;
-        }
-        Cd1Epi c[3];
-        for (int k = 0; k < 3; ++k) {
-            c[k].kind = k;
-            c[k].b = b;
-            c[k].pn = pn;
-            c[k].hs = HS;
-            c[k].ldh = ldh;
-            c[k].zp = ZP;
-            c[k].x = xr;
-            c[k].rec = xr + b * ldv * es;
-            c[k].ldv = ldv;
-            c[k].gaussian = gaussian ? 1 : 0;
-            c[k].ctr = ctrs + 2 * ctr_tiles * k;
-            c[k].u = u_dev;
-        }
-        c[CD1_POS].bias = hb;
-        c[CD1_NEG].bias = hb;
-        c[CD1_RECON].bias = vb;
-        c[CD1_NEG].colpart = colp;
-        c[CD1_NEG].ldc = ldh;
-        c[CD1_RECON].colpart = colp + static_cast<size_t>(ch_h) * ldh;
-        c[CD1_RECON].ldc = ldv;
-        for (int k = 0; k < 3; ++k) h_cd1[k] = c[k];
-        if (!d_cd1) CUDA_THROW(cudaMalloc(&d_cd1, 3 * sizeof(Cd1Epi)));
-        upload(d_cd1, h_cd1, sizeof(h_cd1));
-        cd1_sent_mode = -1;
-        g_pos.ep.coop = d_cd1 + CD1_POS;
-        g_recon.ep.coop = d_cd1 + CD1_RECON;
-        g_neg.ep.coop = d_cd1 + CD1_NEG;
-    }
+    ch_h = ch_v = row_chunks(b);
     planned_b = b;
-}
-
-// PARNN_CD1_COOP=0 falls back to the separate reduction kernels (A/B aid)
-bool RbmDevice::coop_enabled() {
-    static const bool on = [] {
-        const char* v = std::getenv("PARNN_CD1_COOP");
-        return !(v && v[0] == '0');
-    }();
-    return on;
-}
-
-// the per-call fields of the POS epilogue (sampling mode, Philox key / counter or
-// the graph's device counter); a no-op when unchanged
-void RbmDevice::set_sampling(int mode, uint64_t seed, uint64_t counter, const uint64_t* dc) {
-    if (!coop) return;
-    if (mode == cd1_sent_mode && seed == h_cd1[CD1_POS].key && counter == h_cd1[CD1_POS].counter &&
-        dc == h_cd1[CD1_POS].dctr)
-        return;
-    h_cd1[CD1_POS].mode = mode;
-    h_cd1[CD1_POS].key = seed;
-    h_cd1[CD1_POS].counter = counter;
-    h_cd1[CD1_POS].dctr = dc;
-    CUDA_THROW(cudaMemcpyAsync(d_cd1, h_cd1, sizeof(Cd1Epi), cudaMemcpyHostToDevice, stream));
-    CUDA_THROW(cudaStreamSynchronize(stream));  // h_cd1 may change again before a pageable copy lands
-    cd1_sent_mode = mode;
 }
 
 namespace {
 template <typename T>
 void launch_pos(RbmDevice& r, long rows, int mode, uint64_t seed, uint64_t counter, float* out32, long ld32,
                 const uint64_t* dctr = nullptr) {
-    const dim3 grid(static_cast<unsigned>((r.h + 31) / 32), row_chunks(rows)), block(32, 8);
+    const dim3 grid(static_cast<unsigned>((r.h + 31) / 32), r.ch_h), block(32, 8);
     launch_pdl(cd1_pos_kernel<T>, grid, block, r.stream, part_of(r.g_pos), rows, r.h, r.hb, static_cast<T*>(r.PN),
                r.ldh, mode == 4 ? nullptr : static_cast<T*>(r.HS), mode, seed, counter, r.u_dev,
                mode < 3 ? r.ZP : nullptr, out32, ld32, dctr);
@@ -447,7 +395,7 @@ void launch_pos(RbmDevice& r, long rows, int mode, uint64_t seed, uint64_t count
 
 template <typename T>
 void launch_recon(RbmDevice& r, long rows, double* colpart) {
-    const dim3 grid(static_cast<unsigned>((r.v + 31) / 32), row_chunks(rows)), block(32, 8);
+    const dim3 grid(static_cast<unsigned>((r.v + 31) / 32), r.ch_v), block(32, 8);
     T* xr = static_cast<T*>(r.XR);
     launch_pdl(cd1_recon_kernel<T>, grid, block, r.stream, part_of(r.g_recon), rows, r.v, r.vb, r.gaussian, xr, r.ldv,
                xr + r.planned_b * r.ldv, colpart);
@@ -462,47 +410,33 @@ void run_cd1(RbmDevice& r, long b, double lr, int sampling, uint64_t seed, uint6
              uint64_t* dctr = nullptr) {
     cudaStream_t s = r.stream;
     double* cpn = r.colp;
-    int chh = r.ch_h, chv = r.ch_v;
-    if (r.coop) {
-        // the splits of each tile reduce inside the GEMM (cd1_epi.cuh): no reduction launches
-        gemm_launch(r.g_pos, s);
-        gemm_launch(r.g_recon, s);
-        gemm_launch(r.g_neg, s);
-    } else {
-        chh = chv = row_chunks(b);
-        double* cvis = cpn + chh * r.ldh;
-        r.g_pos.ep.coop = r.g_recon.ep.coop = r.g_neg.ep.coop = nullptr;
-        gemm_launch(r.g_pos, s);
-        launch_pos<T>(r, b, sampling, seed, counter, nullptr, 0, dctr);
-        gemm_launch(r.g_recon, s);
-        launch_recon<T>(r, b, cvis);
-        gemm_launch(r.g_neg, s);
-        const dim3 grid(static_cast<unsigned>((r.h + 31) / 32), chh), block(32, 8);
-        launch_pdl(cd1_neg_kernel<T>, grid, block, s, part_of(r.g_neg), b, r.h, r.hb, r.ZP, static_cast<T*>(r.PN),
-                   r.ldh, cpn);
-    }
-    double* cvis = cpn + chh * r.ldh;
+    double* cvis = cpn + r.ch_h * r.ldh;
+    gemm_launch(r.g_pos, s);
+    launch_pos<T>(r, b, sampling, seed, counter, nullptr, 0, dctr);
+    gemm_launch(r.g_recon, s);
+    launch_recon<T>(r, b, cvis);
+    gemm_launch(r.g_neg, s);
+    const dim3 grid(static_cast<unsigned>((r.h + 31) / 32), r.ch_h), block(32, 8);
+    launch_pdl(cd1_neg_kernel<T>, grid, block, s, part_of(r.g_neg), b, r.h, r.hb, r.ZP, static_cast<T*>(r.PN), r.ldh,
+               cpn);
     const double scale = lr / static_cast<double>(b);
     r.g_upd.ep.alpha = static_cast<float>(scale);
     gemm_launch(r.g_upd, s);
     const long wmax = std::max(r.v, r.h);
-    launch_pdl(bias_finish_kernel, dim3(static_cast<unsigned>((wmax + 255) / 256)), dim3(256), s, cpn, chh, r.h,
-               r.ldh, r.hb, cvis, chv, r.v, r.ldv, r.vb, scale, dctr);
+    launch_pdl(bias_finish_kernel, dim3(static_cast<unsigned>((wmax + 255) / 256)), dim3(256), s, cpn, r.ch_h, r.h,
+               r.ldh, r.hb, cvis, r.ch_v, r.v, r.ldv, r.vb, scale, dctr);
     CUDA_THROW(cudaGetLastError());
 }
 }  // namespace
 
 void RbmDevice::cd1(long b, double lr, int sampling, uint64_t seed, uint64_t counter) {
     plan(b);
-    set_sampling(sampling, seed, counter, nullptr);
     if (f32()) run_cd1<float>(*this, b, lr, sampling, seed, counter);
     else run_cd1<bf16>(*this, b, lr, sampling, seed, counter);
 }
 
 void RbmDevice::hidden_probs_rows(long rows, float* out32, long ld32) {
-    GemmPlan g = g_pos;  // plain split-K + the reduction kernel (mode 4: no samples)
-    g.ep.coop = nullptr;
-    gemm_launch(g, stream);
+    gemm_launch(g_pos, stream);
     if (f32()) launch_pos<float>(*this, rows, 4, 0, 0, out32, ld32);
     else launch_pos<bf16>(*this, rows, 4, 0, 0, out32, ld32);
     CUDA_THROW(cudaGetLastError());
@@ -562,20 +496,18 @@ double RbmDevice::reconstruction_error_host(const double* x, long n) {
     if (n <= 0) throw std::runtime_error("reconstruction_error: empty batch");
     CUDA_THROW(cudaMemsetAsync(red, 0, 8 * 64, stream));
     plan(B);
-    GemmPlan gp = g_pos, gr = g_recon;  // plain split-K + the reduction kernels
-    gp.ep.coop = gr.ep.coop = nullptr;
     for (long c0 = 0; c0 < n; c0 += B) {
         const long cb = std::min(B, n - c0);
         upload_rows(*this, x + c0 * v, cb, v, ldv, XR);
-        gemm_launch(gp, stream);
+        gemm_launch(g_pos, stream);
         if (f32()) {
             launch_pos<float>(*this, cb, 3, 0, 0, nullptr, 0);
-            gemm_launch(gr, stream);
+            gemm_launch(g_recon, stream);
             launch_recon<float>(*this, cb, nullptr);
             sqerr_kernel<float><<<64, 256, 0, stream>>>(static_cast<float*>(XR), ldv, B, cb, v, red);
         } else {
             launch_pos<bf16>(*this, cb, 3, 0, 0, nullptr, 0);
-            gemm_launch(gr, stream);
+            gemm_launch(g_recon, stream);
             launch_recon<bf16>(*this, cb, nullptr);
             sqerr_kernel<bf16><<<64, 256, 0, stream>>>(static_cast<bf16*>(XR), ldv, B, cb, v, red);
         }
@@ -634,7 +566,6 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
         // ~0.6 us per graph node). The steps read their slice of the shuffled
         // order and their Philox counter from rbm.dctr = {step, base}.
         rbm.plan(bs);
-        rbm.set_sampling(0, philox_seed, 0, rbm.dctr);  // the graphs read the Philox counter from dctr
         const long steps = n / bs;
         constexpr long kGraphSteps = 32;
         auto capture = [&](long nsteps) {

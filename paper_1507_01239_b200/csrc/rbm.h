@@ -28,14 +28,7 @@ struct RbmDevice {
     double* colp = nullptr;   // per-row-chunk column sums: pos - neg [ch_h x ldh], v - recon [ch_v x ldv]
     float* ZP = nullptr;      // [B x ldh] pre-activations of the pos pass (for the fp64 pos - neg)
     uint64_t* dctr = nullptr; // {step, Philox counter base} of graph-launched CD-1 steps
-    size_t colp_n = 0;
-    int ch_h = 1, ch_v = 1;   // row chunks of the column sums (cooperative split-K: tile rows x splits)
-    bool coop = false;        // the M = b GEMMs reduce their splits in-kernel (cd1_epi.cuh)
-    Cd1Epi* d_cd1 = nullptr;  // device epilogue descriptors: POS, RECON, NEG
-    Cd1Epi h_cd1[3];
-    int cd1_sent_mode = -1;
-    unsigned* ctrs = nullptr;  // per-tile arrival / departure counters, 2 per tile per GEMM
-    long ctr_tiles = 0;
+    int ch_h = 1, ch_v = 1;   // row chunks (grid.y) of the h- and v-wide reductions
     long planned_b = -1;
     GemmPlan g_pos, g_recon, g_neg, g_upd;
 
@@ -45,8 +38,6 @@ struct RbmDevice {
     void set_params(const double* p);  // [W, v_bias, h_bias]
     void get_params(double* p);
     void plan(long b);
-    static bool coop_enabled();
-    void set_sampling(int mode, uint64_t seed, uint64_t counter, const uint64_t* dctr);
     // one CD-1 update on the b rows already in XR[0:b)
     void cd1(long b, double lr, int sampling, uint64_t seed, uint64_t counter);
     void cd1_host(const double* batch, long b, double lr, int sampling, uint64_t seed, uint64_t counter,
