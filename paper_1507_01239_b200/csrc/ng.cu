@@ -400,14 +400,61 @@ void ensure_diag_attr() {
 
 float* linv_blk(NgFactor& f, long j) { return f.linv + (j / NB) * NB * NB; }
 
+// Trailing updates in super-blocks of G 128-column blocks: a block updates the next
+// block column with every panel of its super-block so far (look-ahead, K = (pos+1)
+// x 128); the super-block's last block also applies all G panels at once (K = 128 G)
+// to the rest of the trailing matrix. 1/G as many bulk updates, each with G times
+// the K: the fp32 read-modify-write of the trailing matrix (the early blocks'
+// critical path) is paid once per super-block. PARNN_NG_SUPER=G (1 = per block).
+int ng_super() {  // blocks per super-block (1 = one bulk update per block)
+    static const int g = [] {
+        const char* v = std::getenv("PARNN_NG_SUPER");
+        return v ? std::max(1, std::atoi(v)) : 2;
+    }();
+    return g;
+}
+
 void build_factor(NgFactor& f, int sms) {
     f.panel.clear();
     f.col.clear();
     f.rest.clear();
+    const int G = ng_super();
+    const bool sup = G > 1;
     for (long j = 0; j < f.n; j += NB) {
         const long b = std::min<long>(NB, f.n - j), below = f.n - j - b;
+        const int pos = static_cast<int>((j / NB) % G);  // position in the super-block
+        const bool last = pos == G - 1;
         GemmPlan pp, cp, rp;
-        if (below > 0) {
+        if (below > 0 && sup) {
+            float* a21 = f.a + (j + b) * f.ld + j;
+            GemmEpi e;  // A21 <- A21 L_jj^-T, in place
+            e.mode = EPI_GRAD;
+            e.alpha = 1.f;
+            e.out32 = a21;
+            e.ld_out32 = f.ld;
+            gemm_plan(pp, PREC_FP32, false, a21, f.ld, false, linv_blk(f, j), NB, (int)below, (int)b, (int)b, e, sms,
+                      128);
+            // the super-block's panels so far (columns j - pos*128 .. j + b): none of them has
+            // reached block column j+1 yet, and at the super-block's end none has reached the rest
+            const long k0 = j - pos * NB, kk = pos * NB + b;
+            float* p21 = f.a + (j + b) * f.ld + k0;
+            const long bn1 = std::min<long>(NB, below);
+            GemmEpi c;
+            c.mode = EPI_SUB;
+            c.out32 = f.a + (j + b) * f.ld + (j + b);
+            c.ld_out32 = f.ld;
+            gemm_plan(cp, PREC_FP32, false, p21, f.ld, false, p21, f.ld, (int)below, (int)bn1, (int)kk, c, sms);
+            const long rest = below - bn1;
+            if (last && rest > 0) {
+                float* p31 = p21 + bn1 * f.ld;
+                GemmEpi u;
+                u.mode = EPI_SUB;
+                u.lower = 1;
+                u.out32 = f.a + (j + b + bn1) * f.ld + (j + b + bn1);
+                u.ld_out32 = f.ld;
+                gemm_plan(rp, PREC_FP32, false, p31, f.ld, false, p31, f.ld, (int)rest, (int)rest, (int)kk, u, sms);
+            }
+        } else if (below > 0) {
             float* a21 = f.a + (j + b) * f.ld + j;
             GemmEpi e;  // A21 <- A21 L_jj^-T, in place (one N tile: BN = 128 >= b)
             e.mode = EPI_GRAD;
