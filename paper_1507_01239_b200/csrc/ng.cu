@@ -493,6 +493,8 @@ void build_solve(NgFactor& f, NgSolve& sv, float* x, long ldx, long c, int sms) 
     sv.fupd.clear();
     sv.bdiag.clear();
     sv.bupd.clear();
+    sv.bnext.clear();
+    sv.bpair.clear();
     for (long i0 = 0; i0 < f.n; i0 += NB) {
         const long b = std::min<long>(NB, f.n - i0), rest = f.n - i0 - b;
         float* xi = x + i0 * ldx;
@@ -519,10 +521,29 @@ void build_solve(NgFactor& f, NgSolve& sv, float* x, long ldx, long c, int sms) 
             u.ld_out32 = ldx;
             gemm_plan(bu, PREC_FP32, true, f.a + i0 * f.ld, f.ld, true, xi, ldx, (int)i0, (int)c, (int)b, u, sms);
         }
+        GemmPlan bn, bp;
+        if (i0 >= NB) {
+            GemmEpi u;  // X_{i-1} -= L_{i,i-1}^T X_i
+            u.mode = EPI_SUB;
+            u.out32 = x + (i0 - NB) * ldx;
+            u.ld_out32 = ldx;
+            gemm_plan(bn, PREC_FP32, true, f.a + i0 * f.ld + (i0 - NB), f.ld, true, xi, ldx, NB, (int)c, (int)b, u,
+                      sms);
+            if (i0 >= 2 * NB) {
+                GemmEpi w;  // X_{<i-1} -= L_{{i-1,i},<i-1}^T [X_{i-1}; X_i]
+                w.mode = EPI_SUB;
+                w.out32 = x;
+                w.ld_out32 = ldx;
+                gemm_plan(bp, PREC_FP32, true, f.a + (i0 - NB) * f.ld, f.ld, true, x + (i0 - NB) * ldx, ldx,
+                          (int)(i0 - NB), (int)c, (int)(NB + b), w, sms);
+            }
+        }
         sv.fdiag.push_back(fd);
         sv.fupd.push_back(fu);
         sv.bdiag.push_back(bd);
         sv.bupd.push_back(bu);
+        sv.bnext.push_back(bn);
+        sv.bpair.push_back(bp);
     }
 }
 
@@ -571,9 +592,20 @@ void solve_forward(NgFactor& f, NgSolve& sv, cudaStream_t s, bool conc) {
     }
 }
 
+// Backward sweep in block pairs (ng_super() > 1): bdiag(i), the pair's small
+// update of block i-1, bdiag(i-1), then ONE update of every row above the pair with
+// K = 256 -- half as many of the large read-modify-writes of X.
 void solve_backward(NgSolve& sv, cudaStream_t s) {
-    for (size_t i = sv.bdiag.size(); i-- > 0;) {
+    const bool pairs = ng_super() > 1;
+    for (long i = static_cast<long>(sv.bdiag.size()) - 1; i >= 0; --i) {
         gemm_launch(sv.bdiag[i], s);
+        if (pairs && i >= 1) {
+            gemm_launch(sv.bnext[i], s);
+            gemm_launch(sv.bdiag[i - 1], s);
+            if (sv.bpair[i].M > 0) gemm_launch(sv.bpair[i], s);
+            --i;
+            continue;
+        }
         if (sv.bupd[i].M > 0) gemm_launch(sv.bupd[i], s);
     }
 }

@@ -131,6 +131,9 @@ struct NgFactor {
 };
 struct NgSolve {  // X <- S^-1 X for one fixed right-hand-side buffer
     std::vector<GemmPlan> fdiag, fupd, bdiag, bupd;  // per block
+    // backward sweep in block pairs (i, i-1): X_{i-1} -= L_{i,i-1}^T X_i (bnext), then
+    // X_{<i-1} -= L_{{i-1,i},<i-1}^T X_{i-1,i} with K = 256 (bpair); indexed by i
+    std::vector<GemmPlan> bnext, bpair;
 };
 struct NgLayer {
     NgFactor out, in;
