@@ -495,6 +495,8 @@ void build_solve(NgFactor& f, NgSolve& sv, float* x, long ldx, long c, int sms) 
     sv.bupd.clear();
     sv.bnext.clear();
     sv.bpair.clear();
+    sv.fnext.clear();
+    sv.fpair.clear();
     for (long i0 = 0; i0 < f.n; i0 += NB) {
         const long b = std::min<long>(NB, f.n - i0), rest = f.n - i0 - b;
         float* xi = x + i0 * ldx;
@@ -544,6 +546,26 @@ void build_solve(NgFactor& f, NgSolve& sv, float* x, long ldx, long c, int sms) 
         sv.bupd.push_back(bu);
         sv.bnext.push_back(bn);
         sv.bpair.push_back(bp);
+        GemmPlan fn, fp;
+        if (rest > 0) {
+            const long b1 = std::min<long>(NB, rest);
+            GemmEpi u;  // X_{i+1} -= L_{i+1,i} X_i
+            u.mode = EPI_SUB;
+            u.out32 = x + (i0 + b) * ldx;
+            u.ld_out32 = ldx;
+            gemm_plan(fn, PREC_FP32, false, f.a + (i0 + b) * f.ld + i0, f.ld, true, xi, ldx, (int)b1, (int)c, (int)b,
+                      u, sms);
+            if (rest > b1) {
+                GemmEpi w;  // X_{>i+1} -= L_{>i+1,{i,i+1}} [X_i; X_{i+1}]
+                w.mode = EPI_SUB;
+                w.out32 = x + (i0 + b + b1) * ldx;
+                w.ld_out32 = ldx;
+                gemm_plan(fp, PREC_FP32, false, f.a + (i0 + b + b1) * f.ld + i0, f.ld, true, xi, ldx,
+                          (int)(rest - b1), (int)c, (int)(b + b1), w, sms);
+            }
+        }
+        sv.fnext.push_back(fn);
+        sv.fpair.push_back(fp);
     }
 }
 
@@ -584,10 +606,22 @@ void cholesky(Replica& r, int l, NgFactor& f, DevErr* err, cudaStream_t fs, cuda
 }
 
 // Forward solve block by block, each block as soon as its column of L is final.
+// In block pairs as well (ng_super() > 1): fdiag(i), the pair's small update of
+// block i+1, fdiag(i+1), one K = 256 update of every row below the pair.
 void solve_forward(NgFactor& f, NgSolve& sv, cudaStream_t s, bool conc) {
-    for (size_t i = 0; i < sv.fdiag.size(); ++i) {
+    const bool pairs = ng_super() > 1;
+    const size_t nb = sv.fdiag.size();
+    for (size_t i = 0; i < nb; ++i) {
         if (conc) CUDA_THROW(cudaStreamWaitEvent(s, f.ev_panel[i], 0));
         gemm_launch(sv.fdiag[i], s);
+        if (pairs && i + 1 < nb) {
+            gemm_launch(sv.fnext[i], s);
+            if (conc) CUDA_THROW(cudaStreamWaitEvent(s, f.ev_panel[i + 1], 0));
+            gemm_launch(sv.fdiag[i + 1], s);
+            if (sv.fpair[i].M > 0) gemm_launch(sv.fpair[i], s);
+            ++i;
+            continue;
+        }
         if (sv.fupd[i].M > 0) gemm_launch(sv.fupd[i], s);
     }
 }

@@ -134,6 +134,9 @@ struct NgSolve {  // X <- S^-1 X for one fixed right-hand-side buffer
     // backward sweep in block pairs (i, i-1): X_{i-1} -= L_{i,i-1}^T X_i (bnext), then
     // X_{<i-1} -= L_{{i-1,i},<i-1}^T X_{i-1,i} with K = 256 (bpair); indexed by i
     std::vector<GemmPlan> bnext, bpair;
+    // forward sweep in block pairs (i, i+1): X_{i+1} -= L_{i+1,i} X_i (fnext), then
+    // X_{>i+1} -= L_{>i+1,{i,i+1}} X_{i,i+1} with K = 256 (fpair); indexed by i
+    std::vector<GemmPlan> fnext, fpair;
 };
 struct NgLayer {
     NgFactor out, in;
