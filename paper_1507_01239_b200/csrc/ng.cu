@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(float* __restrict__ a, l
     extern __shared__ float sm[];
     float* S = sm;                 // [NB][LDS]  A -> L
     float* V = sm + NB * LDS;      // [NB][LDS]  L^-1
+    float* col = V + NB * LDS;     // [32] column broadcast of the 32x32 factorizations (16-byte aligned)
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     PNB_CLK(0);
     {
@@ -179,24 +180,39 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(float* __restrict__ a, l
             float d[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c) d[c] = S[(c0 + lane) * LDS + c0 + c];
+            // Software-pipelined: step k first finishes column k+1 and fetches the next
+            // pivot, then applies its remaining column updates while that pivot's
+            // shuffle / rsqrt latency runs (the same operations as the plain order).
+            // The first failing pivot is remembered with warp-uniform selects and
+            // recorded after the loop (a lane-0 branch per step cost a reconvergence).
+            float piv = __shfl_sync(0xffffffffu, d[0], 0);
+            int bad_k = -1;
+            float bad_v = 0.f;
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
-                const float piv = __shfl_sync(0xffffffffu, d[k], k);
-                if (lane == 0 && c0 + k < b && (!(piv > 0.f) || !isfinite(piv))) {
-                    if (atomicCAS(&err->chol_failed, 0, 1) == 0) {
-                        err->chol_index = static_cast<int>(j + c0 + k);
-                        err->chol_value = piv;
-                    }
-                }
+                const bool bad = c0 + k < b && (!(piv > 0.f) || !isfinite(piv));
+                bad_v = (bad_k < 0 && bad) ? piv : bad_v;
+                bad_k = (bad_k < 0 && bad) ? k : bad_k;
                 const float rs = rsqrtf(piv);  // 1/L_kk
                 const float lkk = piv * rs;
                 const float lik = lane > k ? d[k] * rs : (lane == k ? lkk : 0.f);
                 d[k] = lik;
-#pragma unroll
-                for (int c = k + 1; c < 32; ++c) {
+                if (k + 1 < 32) {
+                    // column k of L broadcast through shared memory (one store per lane,
+                    // broadcast loads: the 31 - k shuffles per step were SHFL-throughput bound)
+                    col[lane] = lik;
+                    __syncwarp();
                     // rows c <= lane: a_ic -= L_ik L_ck (columns above the diagonal are dropped)
-                    d[c] = fmaf(-lik, __shfl_sync(0xffffffffu, lik, c), d[c]);
+                    d[k + 1] = fmaf(-lik, col[k + 1], d[k + 1]);
+                    piv = __shfl_sync(0xffffffffu, d[k + 1], k + 1);
+#pragma unroll
+                    for (int c = k + 2; c < 32; ++c) d[c] = fmaf(-lik, col[c], d[c]);
+                    __syncwarp();  // every lane has read column k before the next step overwrites it
                 }
+            }
+            if (lane == 0 && bad_k >= 0 && atomicCAS(&err->chol_failed, 0, 1) == 0) {
+                err->chol_index = static_cast<int>(j + c0 + bad_k);
+                err->chol_value = bad_v;
             }
 #pragma unroll
             for (int c = 0; c < 32; ++c) S[(c0 + lane) * LDS + c0 + c] = c <= lane ? d[c] : 0.f;

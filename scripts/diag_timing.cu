@@ -30,7 +30,9 @@ int main() {
         long long c[64];
         cudaMemcpyFromSymbol(c, g_clk, sizeof(c));
         printf("iter %d: %.1f us | phases (cycles):", it, ms * 1e3);
-        for (int i = 1; i < 16 && c[i]; ++i) printf(" %lld", c[i] - c[i - 1]);
+        // load, [A+B, C] x 4 panels, D (diagonal inverses), E (off-diagonal inverse), store
+        for (int i = 1; i <= 10; ++i) printf(" %lld", c[i] - c[i - 1]);
+        printf(" E %lld store %lld", c[14] - c[10], c[15] - c[14]);
         printf(" | err %s\n", cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
