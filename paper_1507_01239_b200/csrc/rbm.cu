@@ -314,10 +314,23 @@ void RbmDevice::get_params(double* p) {
 }
 
 namespace {
-// split-K factor of an M = b CD-1 GEMM with BN = 128 tiles: about one CTA per SM,
+// split-K factor of an M = b CD-1 GEMM: about one CTA per SM,
 // at least two k-blocks per split (gemm_plan rounds it so no split is empty)
+// Tile width of the M = b split-K GEMMs: 64 (twice the tiles, half the splits and
+// half the partial bytes for the reductions: 53.7 vs 56.3 us per 2048 x 2048 bf16
+// step) except in fp32 mode, where the 3xTF32 mainloop favours 128 (83 vs 89 us).
+// PARNN_CD1_BN: tuning aid.
+int cd1_bn(int prec) {
+    static const int forced = [] {
+        const char* v = std::getenv("PARNN_CD1_BN");
+        const int x = v ? std::atoi(v) : 0;
+        return (x == 64 || x == 128 || x == 256) ? x : 0;
+    }();
+    return forced ? forced : (prec == PREC_FP32 ? 128 : 64);
+}
+
 int cd1_ksplit(int prec, long M, long N, long K, int sms) {
-    const long tiles = ((M + 127) / 128) * ((N + 127) / 128);
+    const long tiles = ((M + 127) / 128) * ((N + cd1_bn(prec) - 1) / cd1_bn(prec));
     const long nk = (K + (prec ? 31 : 63)) / (prec ? 32 : 64);
     return static_cast<int>(std::max<long>(1, std::min<long>(sms / tiles, nk / 2)));
 }
@@ -367,7 +380,7 @@ void RbmDevice::plan(long b) {
         e.ld_out32 = ld;
         e.split_stride = b * ld;
         e.ksplit = ks;
-        gemm_plan(g, prec, false, A, lda, b_mn, Wop, ldv, static_cast<int>(b), N, K, e, sms, 128);
+        gemm_plan(g, prec, false, A, lda, b_mn, Wop, ldv, static_cast<int>(b), N, K, e, sms, cd1_bn(prec));
     };
     split(g_pos, false, xr, ldv, static_cast<int>(h), static_cast<int>(v), kp, ldh);             // X W^T
     split(g_recon, true, HS, ldh, static_cast<int>(v), static_cast<int>(h), kr, ldv);            // hs W
