@@ -1048,7 +1048,11 @@ void Replica::check_errors() {
     // Reference order: ng_precondition (Cholesky) throws before sgd_step's checks.
     if (e.chol_failed) {
         std::ostringstream os;
-        os << "cholesky_solve: non-positive-definite pivot " << e.chol_value << " at index " << e.chol_index;
+        os << "cholesky_solve: non-positive-definite pivot ";
+        // the reference (x86, glibc) prints its NaN pivots as -nan (the default NaN is negative)
+        if (std::isnan(e.chol_value)) os << "-nan";
+        else os << e.chol_value;
+        os << " at index " << e.chol_index;
         throw std::runtime_error(os.str());
     }
     const unsigned bits = f[1] | f[0];
