@@ -131,10 +131,26 @@ __global__ void __launch_bounds__(256) softmax_ce_reg_kernel(const float* __rest
 #pragma unroll
     for (int k = 0; k < kVec; ++k) {
         const long j = 4 * (threadIdx.x + 256L * k);
-        const float p[4] = {v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv};
+        float p[4] = {v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv};
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-            if (j + e < C) dr[j + e] = static_cast<T>(j + e == lab ? p[e] - 1.f : p[e]);
+            if (j + e == lab) p[e] -= 1.f;
+        if (j + 3 < C) {
+            // one vector store per 4 outputs (rows are 64-byte aligned, j is a multiple of 4)
+            if constexpr (sizeof(T) == 2) {
+                const __nv_bfloat162 a = __floats2bfloat162_rn(p[0], p[1]), b = __floats2bfloat162_rn(p[2], p[3]);
+                uint2 w;
+                w.x = *reinterpret_cast<const unsigned*>(&a);
+                w.y = *reinterpret_cast<const unsigned*>(&b);
+                *reinterpret_cast<uint2*>(dr + j) = w;
+            } else {
+                *reinterpret_cast<float4*>(dr + j) = make_float4(p[0], p[1], p[2], p[3]);
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (j + e < C) dr[j + e] = static_cast<T>(p[e]);
+        }
     }
     if (threadIdx.x == 0) ce_rows[i] = logf(s) + m - z[i * ldz + lab];
 }
