@@ -9,11 +9,14 @@ parallel.cpp:195-214):
 * the per-layer buckets: averaging every step through the bucketed,
   event-gated path trains to exactly the same bits as an average issued only
   after every replica's step has finished;
-* contribution-count errors carry the reference's message.
+* contribution-count errors carry the reference's message;
+* averaging after every step with plain SGD equals one replica on the
+  concatenated batch (gradient averaging).
 """
 import numpy as np
 import pytest
 
+from conftest import rel
 from oracle import parnn_oracle as O
 from paper_1507_01239_b200 import parnn as P
 
@@ -133,3 +136,44 @@ def test_time_average_reports_bytes(ctx):
     ms, nbytes = P.time_average(reps, iters=5)
     assert ms > 0
     assert nbytes >= 4 * reps[0].P  # fp32 bytes of the padded parameter layout
+
+
+def test_averaging_every_step_equals_gradient_averaging(ctx):
+    """SPEC.md:404 / SURVEY §8(c): with plain SGD and averaging after every step
+    (K = 1), m replicas that start from the same parameters and each take one
+    batch of B frames equal ONE replica stepping on the concatenated m*B frames
+    (the average of m SGD updates is the SGD update of the batch-mean gradient).
+    Config-1 layer widths, m = 4, B = 64, 5 steps, fp32 mode: the parameter
+    deltas agree to fp32 rounding (the two sides sum in different orders)."""
+    dims = [440, 512, 512, 1000]
+    m, B, T = 4, 64, 5
+    tr, _ = P.make_data(1000, 440, 4, 16.0, 7, 0.10, 2, True)
+    ds = P.DeviceDataset(ctx, tr)
+    p0 = P.init_random(dims, seed=1).params
+    rng = np.random.default_rng(5)
+    rows = rng.integers(0, tr.size(), (T, m, B))
+    lrs = np.full(T, 0.5, np.float32)
+    reps = []
+    for r in range(m):
+        rep = P.Replica(ctx, dims, precision=P.Precision.fp32, optimizer=P.OptimizerKind.sgd, minibatch=B,
+                        max_steps=T)
+        rep.set_params(p0)
+        rep.bind(ds)
+        rep.upload_epoch(rows[:, r, :].ravel(), lrs)
+        reps.append(rep)
+    P.run_steps(reps, T, 1)
+    for rep in reps:
+        rep.sync()
+    avg = reps[0].get_params()
+    for rep in reps[1:]:
+        assert np.array_equal(rep.get_params(), avg)  # every replica holds the average
+    one = P.Replica(ctx, dims, precision=P.Precision.fp32, optimizer=P.OptimizerKind.sgd, minibatch=m * B, max_steps=T)
+    one.set_params(p0)
+    one.bind(ds)
+    one.upload_epoch(rows.reshape(T, m * B).ravel(), lrs)
+    one.step(T)
+    one.sync()
+    big = one.get_params()
+    assert rel(avg - p0, big - p0) < 1e-5, rel(avg - p0, big - p0)
+    for rep in reps + [one]:
+        rep.close()
