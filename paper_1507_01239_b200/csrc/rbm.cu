@@ -128,10 +128,11 @@ __global__ void __launch_bounds__(256) cd1_pos_kernel(PartIn in, long b, long h,
                                                       T* __restrict__ pn, long ldh, T* __restrict__ hs, int mode,
                                                       uint64_t key, uint64_t counter, const double* __restrict__ u,
                                                       float* __restrict__ zp, float* __restrict__ out32, long ld32,
-                                                      const uint64_t* __restrict__ dctr) {
+                                                      const uint64_t* __restrict__ dctr, long koff) {
     grid_dep_wait();
-    // graph-launched steps: counter = epoch base + step * b * h (dctr = {step, base})
-    if (dctr) counter = dctr[1] + dctr[0] * static_cast<uint64_t>(b) * static_cast<uint64_t>(h);
+    // graph-launched steps: counter = epoch base + step * b * h, step = graph base + koff
+    // (dctr = {graph base step, counter base})
+    if (dctr) counter = dctr[1] + (dctr[0] + koff) * static_cast<uint64_t>(b) * static_cast<uint64_t>(h);
     const Chunk c = chunk_of(b, h);
     if (c.j < h) {
         const float bias = hb[c.j];
@@ -202,10 +203,11 @@ __global__ void __launch_bounds__(256) cd1_neg_kernel(PartIn in, long b, long h,
 // hb += s * sum (pos - neg), vb += s * sum (v - recon)   (pretrain.cpp:106-119)
 __global__ void bias_finish_kernel(const double* __restrict__ cpn, int chunks_h, long h, long ldh,
                                    float* __restrict__ hb, const double* __restrict__ cvis, int chunks_v, long v,
-                                   long ldv, float* __restrict__ vb, double s, uint64_t* __restrict__ dctr) {
+                                   long ldv, float* __restrict__ vb, double s, uint64_t* __restrict__ dctr,
+                                   long inc) {
     grid_dep_wait();
     const long j = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (dctr && j == 0) dctr[0] += 1;  // the step is done: the next one reads its rows / counter
+    if (dctr && inc && j == 0) dctr[0] += inc;  // the graph's last step: advance the graph base step
     if (j < h) {
         double a = 0.0;
         for (int k = 0; k < chunks_h; ++k) a += cpn[k * ldh + j];
@@ -220,9 +222,10 @@ __global__ void bias_finish_kernel(const double* __restrict__ cpn, int chunks_h,
 
 template <typename T>
 __global__ void load_rows_kernel(const float* __restrict__ src, long lds, const uint32_t* __restrict__ rows, long b,
-                                 long d, T* __restrict__ dst, long ldd, const uint64_t* __restrict__ dstep) {
+                                 long d, T* __restrict__ dst, long ldd, const uint64_t* __restrict__ dstep,
+                                 long koff) {
     grid_dep_wait();
-    if (dstep) rows += dstep[0] * b;  // graph-launched steps: this step's slice of the shuffled order
+    if (dstep) rows += (dstep[0] + koff) * b;  // graph-launched steps: this step's slice of the shuffled order
     const long total = b * ldd;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
         const long r = i / ldd, c = i % ldd;
@@ -268,6 +271,9 @@ RbmDevice::RbmDevice(Context* c, long visible, long hidden, bool g, long batch, 
     hb = dalloc<float>(ldh);
     CUDA_THROW(cudaMalloc(&XR, 2 * B * ldv * es));
     zero(XR, 2 * B * ldv * es);
+    CUDA_THROW(cudaMalloc(&XRs[1], 2 * B * ldv * es));
+    zero(XRs[1], 2 * B * ldv * es);
+    XRs[0] = XR;
     CUDA_THROW(cudaMalloc(&PN, 2 * B * ldh * es));
     zero(PN, 2 * B * ldh * es);
     CUDA_THROW(cudaMalloc(&HS, B * ldh * es));
@@ -282,8 +288,8 @@ RbmDevice::RbmDevice(Context* c, long visible, long hidden, bool g, long batch, 
 
 RbmDevice::~RbmDevice() {
     if (stream) cudaStreamSynchronize(stream);
-    for (void* p : {(void*)W, (void*)Ws, (void*)vb, (void*)hb, XR, PN, HS, (void*)u_dev, (void*)red, (void*)part,
-                    (void*)colp, (void*)ZP, (void*)dctr})
+    for (void* p : {(void*)W, (void*)Ws, (void*)vb, (void*)hb, XRs[0], XRs[1], PN, HS, (void*)u_dev, (void*)red,
+                    (void*)part, (void*)colp, (void*)ZP, (void*)dctr})
         if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
 }
@@ -363,47 +369,63 @@ void RbmDevice::plan(long b) {
     const bool F = f32();
     const size_t es = F ? 4 : 2;
     const void* Wop = F ? static_cast<const void*>(W) : static_cast<const void*>(Ws);
-    char* xr = static_cast<char*>(XR);
-    char* pn = static_cast<char*>(PN);
-    const int sms = ctx->num_sms;
-    const int kp = cd1_ksplit(prec, b, h, v, sms), kr = cd1_ksplit(prec, b, v, h, sms);
-    const size_t need = std::max(static_cast<size_t>(kp) * b * ldh, static_cast<size_t>(kr) * b * ldv);
-    if (need > part_n) {
-        if (part) CUDA_THROW(cudaFree(part));
-        CUDA_THROW(cudaMalloc(&part, need * 4));
-        part_n = need;
+    // one plan set per XR buffer (graph-launched epochs alternate them)
+    for (int sl = 1; sl >= 0; --sl) {
+        XR = XRs[sl];
+        char* xr = static_cast<char*>(XR);
+        char* pn = static_cast<char*>(PN);
+        const int sms = ctx->num_sms;
+        const int kp = cd1_ksplit(prec, b, h, v, sms), kr = cd1_ksplit(prec, b, v, h, sms);
+        const size_t need = std::max(static_cast<size_t>(kp) * b * ldh, static_cast<size_t>(kr) * b * ldv);
+        if (need > part_n) {
+            if (part) CUDA_THROW(cudaFree(part));
+            CUDA_THROW(cudaMalloc(&part, need * 4));
+            part_n = need;
+        }
+        auto split = [&](GemmPlan& g, bool b_mn, const void* A, long lda, int N, int K, int ks, long ld) {
+            GemmEpi e;
+            e.mode = EPI_PARTIAL;
+            e.out32 = part;
+            e.ld_out32 = ld;
+            e.split_stride = b * ld;
+            e.ksplit = ks;
+            gemm_plan(g, prec, false, A, lda, b_mn, Wop, ldv, static_cast<int>(b), N, K, e, sms, cd1_bn(prec));
+        };
+        split(g_pos, false, xr, ldv, static_cast<int>(h), static_cast<int>(v), kp, ldh);             // X W^T
+        split(g_recon, true, HS, ldh, static_cast<int>(v), static_cast<int>(h), kr, ldv);            // hs W
+        split(g_neg, false, xr + b * ldv * es, ldv, static_cast<int>(h), static_cast<int>(v), kp, ldh);  // recon W^T
+        GemmEpi u;
+        u.mode = EPI_AXPY;
+        u.out32 = W;
+        u.ld_out32 = ldv;
+        u.shadow = Ws;
+        u.ld_shadow = ldv;
+        gemm_plan(g_upd, prec, true, pn, ldh, true, xr, ldv, (int)h, (int)v, (int)(2 * b), u, sms);
+        slot_plans[sl][0] = g_pos;
+        slot_plans[sl][1] = g_recon;
+        slot_plans[sl][2] = g_neg;
+        slot_plans[sl][3] = g_upd;
     }
-    auto split = [&](GemmPlan& g, bool b_mn, const void* A, long lda, int N, int K, int ks, long ld) {
-        GemmEpi e;
-        e.mode = EPI_PARTIAL;
-        e.out32 = part;
-        e.ld_out32 = ld;
-        e.split_stride = b * ld;
-        e.ksplit = ks;
-        gemm_plan(g, prec, false, A, lda, b_mn, Wop, ldv, static_cast<int>(b), N, K, e, sms, cd1_bn(prec));
-    };
-    split(g_pos, false, xr, ldv, static_cast<int>(h), static_cast<int>(v), kp, ldh);             // X W^T
-    split(g_recon, true, HS, ldh, static_cast<int>(v), static_cast<int>(h), kr, ldv);            // hs W
-    split(g_neg, false, xr + b * ldv * es, ldv, static_cast<int>(h), static_cast<int>(v), kp, ldh);  // recon W^T
-    GemmEpi u;
-    u.mode = EPI_AXPY;
-    u.out32 = W;
-    u.ld_out32 = ldv;
-    u.shadow = Ws;
-    u.ld_shadow = ldv;
-    gemm_plan(g_upd, prec, true, pn, ldh, true, xr, ldv, (int)h, (int)v, (int)(2 * b), u, sms);
     ch_h = ch_v = row_chunks(b);
     planned_b = b;
+}
+
+void RbmDevice::use_slot(int sl) {
+    XR = XRs[sl];
+    g_pos = slot_plans[sl][0];
+    g_recon = slot_plans[sl][1];
+    g_neg = slot_plans[sl][2];
+    g_upd = slot_plans[sl][3];
 }
 
 namespace {
 template <typename T>
 void launch_pos(RbmDevice& r, long rows, int mode, uint64_t seed, uint64_t counter, float* out32, long ld32,
-                const uint64_t* dctr = nullptr) {
+                const uint64_t* dctr = nullptr, long koff = 0) {
     const dim3 grid(static_cast<unsigned>((r.h + 31) / 32), r.ch_h), block(32, 8);
     launch_pdl(cd1_pos_kernel<T>, grid, block, r.stream, part_of(r.g_pos), rows, r.h, r.hb, static_cast<T*>(r.PN),
                r.ldh, mode == 4 ? nullptr : static_cast<T*>(r.HS), mode, seed, counter, r.u_dev,
-               mode < 3 ? r.ZP : nullptr, out32, ld32, dctr);
+               mode < 3 ? r.ZP : nullptr, out32, ld32, dctr, koff);
 }
 
 template <typename T>
@@ -417,15 +439,15 @@ void launch_recon(RbmDevice& r, long rows, double* colpart) {
 // one CD-1 update (pretrain.cpp:79-121): 3 split-K GEMMs each followed by its
 // fused reduction, the rank-2b weight update, the bias update
 template <typename T>
-// dctr: graph-captured steps read the Philox counter from {step, base} and the
-// last kernel advances the step
+// dctr: graph-captured step koff of a graph reads its Philox counter from {graph
+// base step, counter base}; the graph's last step advances the base by inc
 void run_cd1(RbmDevice& r, long b, double lr, int sampling, uint64_t seed, uint64_t counter,
-             uint64_t* dctr = nullptr) {
+             uint64_t* dctr = nullptr, long koff = 0, long inc = 0) {
     cudaStream_t s = r.stream;
     double* cpn = r.colp;
     double* cvis = cpn + r.ch_h * r.ldh;
     gemm_launch(r.g_pos, s);
-    launch_pos<T>(r, b, sampling, seed, counter, nullptr, 0, dctr);
+    launch_pos<T>(r, b, sampling, seed, counter, nullptr, 0, dctr, koff);
     gemm_launch(r.g_recon, s);
     launch_recon<T>(r, b, cvis);
     gemm_launch(r.g_neg, s);
@@ -437,7 +459,7 @@ void run_cd1(RbmDevice& r, long b, double lr, int sampling, uint64_t seed, uint6
     gemm_launch(r.g_upd, s);
     const long wmax = std::max(r.v, r.h);
     launch_pdl(bias_finish_kernel, dim3(static_cast<unsigned>((wmax + 255) / 256)), dim3(256), s, cpn, r.ch_h, r.h,
-               r.ldh, r.hb, cvis, r.ch_v, r.v, r.ldv, r.vb, scale, dctr);
+               r.ldh, r.hb, cvis, r.ch_v, r.v, r.ldv, r.vb, scale, dctr, inc);
     CUDA_THROW(cudaGetLastError());
 }
 }  // namespace
@@ -465,10 +487,10 @@ void upload_rows(RbmDevice& r, const double* x, long b, long d, long ld, void* d
     CUDA_THROW(cudaMemcpyAsync(tmp, hbuf.data(), hbuf.size() * 4, cudaMemcpyHostToDevice, r.stream));
     if (r.f32())
         load_rows_kernel<float><<<grid_of(b * ld), 256, 0, r.stream>>>(tmp, ld, nullptr, b, d, static_cast<float*>(dst), ld,
-                                                                        nullptr);
+                                                                        nullptr, 0);
     else
         load_rows_kernel<bf16><<<grid_of(b * ld), 256, 0, r.stream>>>(tmp, ld, nullptr, b, d, static_cast<bf16*>(dst), ld,
-                                                                       nullptr);
+                                                                       nullptr, 0);
     CUDA_THROW(cudaStreamSynchronize(r.stream));
     cudaFree(tmp);
 }
@@ -581,22 +603,42 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
         rbm.plan(bs);
         const long steps = n / bs;
         constexpr long kGraphSteps = 32;
+        // Two XR buffers: step k gathers its batch into buffer k % 2 on a side stream,
+        // so the gather overlaps step k-1 (it waits only for step k-2, the last reader
+        // of that buffer) and leaves the step's dependent chain.
+        cudaStream_t side = nullptr;
+        CUDA_THROW(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        cudaEvent_t ev_begin, ev_load[2], ev_done[2], ev_side;
+        for (cudaEvent_t* e : {&ev_begin, &ev_load[0], &ev_load[1], &ev_done[0], &ev_done[1], &ev_side})
+            CUDA_THROW(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         auto capture = [&](long nsteps) {
             cudaGraph_t g = nullptr;
             cudaGraphExec_t ge = nullptr;
             CUDA_THROW(cudaStreamBeginCapture(rbm.stream, cudaStreamCaptureModeThreadLocal));
+            CUDA_THROW(cudaEventRecord(ev_begin, rbm.stream));
+            CUDA_THROW(cudaStreamWaitEvent(side, ev_begin, 0));
             for (long k = 0; k < nsteps; ++k) {
+                const int slot = static_cast<int>(k & 1);
+                if (k >= 2) CUDA_THROW(cudaStreamWaitEvent(side, ev_done[slot], 0));  // step k-2 read this buffer
                 const dim3 gr(static_cast<unsigned>(grid_of(bs * ldx))), t(256);
-                if (rbm.f32()) {
-                    launch_pdl(load_rows_kernel<float>, gr, t, rbm.stream, X, ldx, d_idx, bs, v,
-                               static_cast<float*>(rbm.XR), ldx, static_cast<const uint64_t*>(rbm.dctr));
-                    run_cd1<float>(rbm, bs, lr, 0, philox_seed, 0, rbm.dctr);
-                } else {
-                    launch_pdl(load_rows_kernel<bf16>, gr, t, rbm.stream, X, ldx, d_idx, bs, v,
-                               static_cast<bf16*>(rbm.XR), ldx, static_cast<const uint64_t*>(rbm.dctr));
-                    run_cd1<bf16>(rbm, bs, lr, 0, philox_seed, 0, rbm.dctr);
-                }
+                if (rbm.f32())
+                    launch_pdl(load_rows_kernel<float>, gr, t, side, X, ldx, d_idx, bs, v,
+                               static_cast<float*>(rbm.XRs[slot]), ldx, static_cast<const uint64_t*>(rbm.dctr), k);
+                else
+                    launch_pdl(load_rows_kernel<bf16>, gr, t, side, X, ldx, d_idx, bs, v,
+                               static_cast<bf16*>(rbm.XRs[slot]), ldx, static_cast<const uint64_t*>(rbm.dctr), k);
+                CUDA_THROW(cudaEventRecord(ev_load[slot], side));
+                CUDA_THROW(cudaStreamWaitEvent(rbm.stream, ev_load[slot], 0));
+                rbm.use_slot(slot);
+                if (rbm.f32())
+                    run_cd1<float>(rbm, bs, lr, 0, philox_seed, 0, rbm.dctr, k, k + 1 == nsteps ? nsteps : 0);
+                else
+                    run_cd1<bf16>(rbm, bs, lr, 0, philox_seed, 0, rbm.dctr, k, k + 1 == nsteps ? nsteps : 0);
+                CUDA_THROW(cudaEventRecord(ev_done[slot], rbm.stream));
             }
+            rbm.use_slot(0);
+            CUDA_THROW(cudaEventRecord(ev_side, side));  // join the side stream back
+            CUDA_THROW(cudaStreamWaitEvent(rbm.stream, ev_side, 0));
             CUDA_THROW(cudaStreamEndCapture(rbm.stream, &g));
             CUDA_THROW(cudaGraphInstantiate(&ge, g, 0));
             CUDA_THROW(cudaGraphDestroy(g));
@@ -635,6 +677,8 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
         cudaEventDestroy(t1);
         if (gbig) CUDA_THROW(cudaGraphExecDestroy(gbig));
         if (gone) CUDA_THROW(cudaGraphExecDestroy(gone));
+        for (cudaEvent_t e : {ev_begin, ev_load[0], ev_load[1], ev_done[0], ev_done[1], ev_side}) cudaEventDestroy(e);
+        cudaStreamDestroy(side);
         // next layer input: hidden probabilities over the whole data (pretrain.cpp:190)
         const long ldh = pad32(h);
         float* Xn = nullptr;
@@ -644,10 +688,10 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
             const long cb = std::min(bs, n - c0);
             if (rbm.f32())
                 load_rows_kernel<float><<<grid_of(cb * ldx), 256, 0, rbm.stream>>>(X + c0 * ldx, ldx, nullptr, cb, v,
-                                                                                static_cast<float*>(rbm.XR), ldx, nullptr);
+                                                                                static_cast<float*>(rbm.XR), ldx, nullptr, 0);
             else
                 load_rows_kernel<bf16><<<grid_of(cb * ldx), 256, 0, rbm.stream>>>(X + c0 * ldx, ldx, nullptr, cb, v,
-                                                                               static_cast<bf16*>(rbm.XR), ldx, nullptr);
+                                                                               static_cast<bf16*>(rbm.XR), ldx, nullptr, 0);
             rbm.hidden_probs_rows(cb, Xn + c0 * ldh, ldh);
         }
         CUDA_THROW(cudaStreamSynchronize(rbm.stream));

@@ -18,7 +18,8 @@ struct RbmDevice {
     bf16* Ws = nullptr;  // bf16 operand copy
     float* vb = nullptr;
     float* hb = nullptr;
-    void* XR = nullptr;  // [2B x ldv] op dtype: batch rows, then reconstruction rows
+    void* XR = nullptr;  // [2B x ldv] op dtype: batch rows, then reconstruction rows (= XRs[slot])
+    void* XRs[2] = {nullptr, nullptr};  // two buffers: the next batch gathers while a step runs
     void* PN = nullptr;  // [2B x ldh] op dtype: pos probs, then -neg probs
     void* HS = nullptr;  // [B x ldh] op dtype: hidden samples
     double* u_dev = nullptr;  // injected uniforms [B x h]
@@ -30,7 +31,8 @@ struct RbmDevice {
     uint64_t* dctr = nullptr; // {step, Philox counter base} of graph-launched CD-1 steps
     int ch_h = 1, ch_v = 1;   // row chunks (grid.y) of the h- and v-wide reductions
     long planned_b = -1;
-    GemmPlan g_pos, g_recon, g_neg, g_upd;
+    GemmPlan g_pos, g_recon, g_neg, g_upd;  // the current buffer's plans
+    GemmPlan slot_plans[2][4];
 
     RbmDevice(Context* c, long visible, long hidden, bool gaussian, long batch, Precision p);
     ~RbmDevice();
@@ -38,6 +40,7 @@ struct RbmDevice {
     void set_params(const double* p);  // [W, v_bias, h_bias]
     void get_params(double* p);
     void plan(long b);
+    void use_slot(int sl);  // XR and the plans of buffer sl
     // one CD-1 update on the b rows already in XR[0:b)
     void cd1(long b, double lr, int sampling, uint64_t seed, uint64_t counter);
     void cd1_host(const double* batch, long b, double lr, int sampling, uint64_t seed, uint64_t counter,
