@@ -447,6 +447,11 @@ void run_cd1(RbmDevice& r, long b, double lr, int sampling, uint64_t seed, uint6
     double* cpn = r.colp;
     double* cvis = cpn + r.ch_h * r.ldh;
     gemm_launch(r.g_pos, s);
+    if (r.bias_side && r.bias_pending) {
+        // the previous step's bias update (side stream) lands before this step reads hb
+        CUDA_THROW(cudaStreamWaitEvent(s, r.ev_bias, 0));
+        r.bias_pending = false;
+    }
     launch_pos<T>(r, b, sampling, seed, counter, nullptr, 0, dctr, koff);
     gemm_launch(r.g_recon, s);
     launch_recon<T>(r, b, cvis);
@@ -455,11 +460,22 @@ void run_cd1(RbmDevice& r, long b, double lr, int sampling, uint64_t seed, uint6
     launch_pdl(cd1_neg_kernel<T>, grid, block, s, part_of(r.g_neg), b, r.h, r.hb, r.ZP, static_cast<T*>(r.PN), r.ldh,
                cpn);
     const double scale = lr / static_cast<double>(b);
+    const long wmax = std::max(r.v, r.h);
+    const dim3 bgrid(static_cast<unsigned>((wmax + 255) / 256)), bblock(256);
+    if (r.bias_side) {
+        // graph-launched steps: the bias update runs beside the weight update
+        CUDA_THROW(cudaEventRecord(r.ev_neg, s));
+        CUDA_THROW(cudaStreamWaitEvent(r.bias_side, r.ev_neg, 0));
+        launch_pdl(bias_finish_kernel, bgrid, bblock, r.bias_side, cpn, r.ch_h, r.h, r.ldh, r.hb, cvis, r.ch_v, r.v,
+                   r.ldv, r.vb, scale, dctr, inc);
+        CUDA_THROW(cudaEventRecord(r.ev_bias, r.bias_side));
+        r.bias_pending = true;
+    }
     r.g_upd.ep.alpha = static_cast<float>(scale);
     gemm_launch(r.g_upd, s);
-    const long wmax = std::max(r.v, r.h);
-    launch_pdl(bias_finish_kernel, dim3(static_cast<unsigned>((wmax + 255) / 256)), dim3(256), s, cpn, r.ch_h, r.h,
-               r.ldh, r.hb, cvis, r.ch_v, r.v, r.ldv, r.vb, scale, dctr, inc);
+    if (!r.bias_side)
+        launch_pdl(bias_finish_kernel, bgrid, bblock, s, cpn, r.ch_h, r.h, r.ldh, r.hb, cvis, r.ch_v, r.v, r.ldv, r.vb,
+                   scale, dctr, inc);
     CUDA_THROW(cudaGetLastError());
 }
 }  // namespace
@@ -611,9 +627,13 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
         cudaEvent_t ev_begin, ev_load[2], ev_done[2], ev_side;
         for (cudaEvent_t* e : {&ev_begin, &ev_load[0], &ev_load[1], &ev_done[0], &ev_done[1], &ev_side})
             CUDA_THROW(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        CUDA_THROW(cudaEventCreateWithFlags(&rbm.ev_neg, cudaEventDisableTiming));
+        CUDA_THROW(cudaEventCreateWithFlags(&rbm.ev_bias, cudaEventDisableTiming));
         auto capture = [&](long nsteps) {
             cudaGraph_t g = nullptr;
             cudaGraphExec_t ge = nullptr;
+            rbm.bias_side = side;  // the bias updates run on the side stream too
+            rbm.bias_pending = false;
             CUDA_THROW(cudaStreamBeginCapture(rbm.stream, cudaStreamCaptureModeThreadLocal));
             CUDA_THROW(cudaEventRecord(ev_begin, rbm.stream));
             CUDA_THROW(cudaStreamWaitEvent(side, ev_begin, 0));
@@ -637,6 +657,8 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
                 CUDA_THROW(cudaEventRecord(ev_done[slot], rbm.stream));
             }
             rbm.use_slot(0);
+            rbm.bias_side = nullptr;
+            rbm.bias_pending = false;
             CUDA_THROW(cudaEventRecord(ev_side, side));  // join the side stream back
             CUDA_THROW(cudaStreamWaitEvent(rbm.stream, ev_side, 0));
             CUDA_THROW(cudaStreamEndCapture(rbm.stream, &g));
@@ -677,7 +699,10 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
         cudaEventDestroy(t1);
         if (gbig) CUDA_THROW(cudaGraphExecDestroy(gbig));
         if (gone) CUDA_THROW(cudaGraphExecDestroy(gone));
-        for (cudaEvent_t e : {ev_begin, ev_load[0], ev_load[1], ev_done[0], ev_done[1], ev_side}) cudaEventDestroy(e);
+        for (cudaEvent_t e : {ev_begin, ev_load[0], ev_load[1], ev_done[0], ev_done[1], ev_side, rbm.ev_neg,
+                              rbm.ev_bias})
+            cudaEventDestroy(e);
+        rbm.ev_neg = rbm.ev_bias = nullptr;
         cudaStreamDestroy(side);
         // next layer input: hidden probabilities over the whole data (pretrain.cpp:190)
         const long ldh = pad32(h);

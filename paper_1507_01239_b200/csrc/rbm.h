@@ -33,6 +33,10 @@ struct RbmDevice {
     long planned_b = -1;
     GemmPlan g_pos, g_recon, g_neg, g_upd;  // the current buffer's plans
     GemmPlan slot_plans[2][4];
+    // graph capture only: the bias update on this stream beside the weight update
+    cudaStream_t bias_side = nullptr;
+    cudaEvent_t ev_neg = nullptr, ev_bias = nullptr;
+    bool bias_pending = false;
 
     RbmDevice(Context* c, long visible, long hidden, bool gaussian, long batch, Precision p);
     ~RbmDevice();
