@@ -263,7 +263,7 @@ RbmDevice::RbmDevice(Context* c, long visible, long hidden, bool g, long batch, 
                                  std::to_string(h) + ")");
     if (B <= 0) throw std::runtime_error("cd1_gibbs: empty batch");
     CUDA_THROW(cudaSetDevice(c->device));
-    CUDA_THROW(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    stream = make_stream(0);  // the CD-1 chain; the graphs' side stream (batch gathers, bias updates) is low
     const size_t es = f32() ? 4 : 2;
     W = dalloc<float>(h * ldv);
     if (!f32()) Ws = dalloc<bf16>(h * ldv);
@@ -623,7 +623,7 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
         // so the gather overlaps step k-1 (it waits only for step k-2, the last reader
         // of that buffer) and leaves the step's dependent chain.
         cudaStream_t side = nullptr;
-        CUDA_THROW(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        side = make_stream(2);
         cudaEvent_t ev_begin, ev_load[2], ev_done[2], ev_side;
         for (cudaEvent_t* e : {&ev_begin, &ev_load[0], &ev_load[1], &ev_done[0], &ev_done[1], &ev_side})
             CUDA_THROW(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
