@@ -587,16 +587,31 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
     if (n <= 0) throw std::runtime_error("cd1_gibbs: empty batch");
     const long bs = std::min(batch, n);
     long d0 = dims[0], ld0 = pad32(d0);
+    // device buffers, streams, events and graphs are released on every exit path
+    struct Owned {
+        std::vector<void*> mem;
+        std::vector<cudaStream_t> streams;
+        std::vector<cudaEvent_t> events;
+        std::vector<cudaGraphExec_t> graphs;
+        ~Owned() {
+            for (auto g : graphs) cudaGraphExecDestroy(g);
+            for (auto e : events) cudaEventDestroy(e);
+            for (auto st : streams) cudaStreamDestroy(st);
+            for (void* m : mem) cudaFree(m);
+        }
+    } own;
     float* X = nullptr;
     {
         std::vector<float> hx(n * ld0, 0.f);
         for (long i = 0; i < n; ++i)
             for (long j = 0; j < d0; ++j) hx[i * ld0 + j] = static_cast<float>(data[i * d0 + j]);
         CUDA_THROW(cudaMalloc(&X, hx.size() * 4));
+        own.mem.push_back(X);
         upload(X, hx.data(), hx.size() * 4);
     }
     uint32_t* d_idx = nullptr;
     CUDA_THROW(cudaMalloc(&d_idx, n * 4));
+    own.mem.push_back(d_idx);
     long pos = 0;
     uint64_t counter = 0;
     const size_t L = dims.size() - 1;
@@ -622,13 +637,17 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
         // Two XR buffers: step k gathers its batch into buffer k % 2 on a side stream,
         // so the gather overlaps step k-1 (it waits only for step k-2, the last reader
         // of that buffer) and leaves the step's dependent chain.
-        cudaStream_t side = nullptr;
-        side = make_stream(2);
+        cudaStream_t side = make_stream(2);
+        own.streams.push_back(side);
         cudaEvent_t ev_begin, ev_load[2], ev_done[2], ev_side;
-        for (cudaEvent_t* e : {&ev_begin, &ev_load[0], &ev_load[1], &ev_done[0], &ev_done[1], &ev_side})
+        for (cudaEvent_t* e : {&ev_begin, &ev_load[0], &ev_load[1], &ev_done[0], &ev_done[1], &ev_side}) {
             CUDA_THROW(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+            own.events.push_back(*e);
+        }
         CUDA_THROW(cudaEventCreateWithFlags(&rbm.ev_neg, cudaEventDisableTiming));
+        own.events.push_back(rbm.ev_neg);
         CUDA_THROW(cudaEventCreateWithFlags(&rbm.ev_bias, cudaEventDisableTiming));
+        own.events.push_back(rbm.ev_bias);
         auto capture = [&](long nsteps) {
             cudaGraph_t g = nullptr;
             cudaGraphExec_t ge = nullptr;
@@ -662,8 +681,10 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
             CUDA_THROW(cudaEventRecord(ev_side, side));  // join the side stream back
             CUDA_THROW(cudaStreamWaitEvent(rbm.stream, ev_side, 0));
             CUDA_THROW(cudaStreamEndCapture(rbm.stream, &g));
-            CUDA_THROW(cudaGraphInstantiate(&ge, g, 0));
-            CUDA_THROW(cudaGraphDestroy(g));
+            const cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
+            cudaGraphDestroy(g);
+            CUDA_THROW(ie);
+            own.graphs.push_back(ge);
             return ge;
         };
         cudaGraphExec_t gbig = steps >= kGraphSteps ? capture(kGraphSteps) : nullptr;
@@ -697,17 +718,12 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
         g_pretrain_stats.cd1_flop += 10.0 * v * h * static_cast<double>(bs) * steps * epochs;
         cudaEventDestroy(t0);
         cudaEventDestroy(t1);
-        if (gbig) CUDA_THROW(cudaGraphExecDestroy(gbig));
-        if (gone) CUDA_THROW(cudaGraphExecDestroy(gone));
-        for (cudaEvent_t e : {ev_begin, ev_load[0], ev_load[1], ev_done[0], ev_done[1], ev_side, rbm.ev_neg,
-                              rbm.ev_bias})
-            cudaEventDestroy(e);
-        rbm.ev_neg = rbm.ev_bias = nullptr;
-        cudaStreamDestroy(side);
+        rbm.ev_neg = rbm.ev_bias = nullptr;  // released with the other per-layer objects at exit
         // next layer input: hidden probabilities over the whole data (pretrain.cpp:190)
         const long ldh = pad32(h);
         float* Xn = nullptr;
         CUDA_THROW(cudaMalloc(&Xn, n * ldh * 4));
+        own.mem.push_back(Xn);
         rbm.plan(bs);
         for (long c0 = 0; c0 < n; c0 += bs) {
             const long cb = std::min(bs, n - c0);
@@ -720,6 +736,8 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
             rbm.hidden_probs_rows(cb, Xn + c0 * ldh, ldh);
         }
         CUDA_THROW(cudaStreamSynchronize(rbm.stream));
+        // the previous layer's input is no longer needed (at config 4: 8 GB per layer)
+        own.mem.erase(std::find(own.mem.begin(), own.mem.end(), static_cast<void*>(X)));
         cudaFree(X);
         X = Xn;
         rbm.get_params(p.data());
@@ -730,8 +748,6 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
     const double r = std::sqrt(6.0 / static_cast<double>(di + dout));
     for (long i = 0; i < di * dout; ++i) out[pos++] = rng.uniform(-r, r);
     for (long j = 0; j < dout; ++j) out[pos++] = 0.0;
-    cudaFree(X);
-    cudaFree(d_idx);
 }
 
 }  // namespace pnb
