@@ -687,8 +687,12 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
             own.graphs.push_back(ge);
             return ge;
         };
-        cudaGraphExec_t gbig = steps >= kGraphSteps ? capture(kGraphSteps) : nullptr;
-        cudaGraphExec_t gone = steps % kGraphSteps ? capture(1) : nullptr;
+        // PARNN_CD1_GRAPH=0: the same steps launched one kernel at a time on the chain
+        // stream (test reference for the graphs; read per call)
+        const char* gv = std::getenv("PARNN_CD1_GRAPH");
+        const bool graphs = !(gv && gv[0] == '0');
+        cudaGraphExec_t gbig = graphs && steps >= kGraphSteps ? capture(kGraphSteps) : nullptr;
+        cudaGraphExec_t gone = graphs && steps % kGraphSteps ? capture(1) : nullptr;
         uint64_t hctr[2];
         cudaEvent_t t0, t1;
         CUDA_THROW(cudaEventCreate(&t0));
@@ -704,8 +708,25 @@ void greedy_pretrain(Context* ctx, const std::vector<long>& dims, const double* 
             hctr[1] = counter;
             CUDA_THROW(cudaMemcpyAsync(d_idx, idx.data(), n * 4, cudaMemcpyHostToDevice, rbm.stream));
             CUDA_THROW(cudaMemcpyAsync(rbm.dctr, hctr, sizeof(hctr), cudaMemcpyHostToDevice, rbm.stream));
-            for (long k = 0; k + kGraphSteps <= steps; k += kGraphSteps) CUDA_THROW(cudaGraphLaunch(gbig, rbm.stream));
-            for (long k = 0; k < steps % kGraphSteps; ++k) CUDA_THROW(cudaGraphLaunch(gone, rbm.stream));
+            if (graphs) {
+                for (long k = 0; k + kGraphSteps <= steps; k += kGraphSteps)
+                    CUDA_THROW(cudaGraphLaunch(gbig, rbm.stream));
+                for (long k = 0; k < steps % kGraphSteps; ++k) CUDA_THROW(cudaGraphLaunch(gone, rbm.stream));
+            } else {
+                for (long k = 0; k < steps; ++k) {
+                    const dim3 gr(static_cast<unsigned>(grid_of(bs * ldx))), t(256);
+                    const uint64_t ck = counter + static_cast<uint64_t>(k) * bs * static_cast<uint64_t>(h);
+                    if (rbm.f32()) {
+                        launch_pdl(load_rows_kernel<float>, gr, t, rbm.stream, X, ldx, d_idx + k * bs, bs, v,
+                                   static_cast<float*>(rbm.XR), ldx, static_cast<const uint64_t*>(nullptr), 0L);
+                        run_cd1<float>(rbm, bs, lr, 0, philox_seed, ck);
+                    } else {
+                        launch_pdl(load_rows_kernel<bf16>, gr, t, rbm.stream, X, ldx, d_idx + k * bs, bs, v,
+                                   static_cast<bf16*>(rbm.XR), ldx, static_cast<const uint64_t*>(nullptr), 0L);
+                        run_cd1<bf16>(rbm, bs, lr, 0, philox_seed, ck);
+                    }
+                }
+            }
             counter += static_cast<uint64_t>(steps) * static_cast<uint64_t>(bs) * static_cast<uint64_t>(h);
             for (long k = 0; k < steps; ++k) rng.jump(skip);  // the reference's b*h sample_bernoulli draws
         }

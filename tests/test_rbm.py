@@ -181,3 +181,20 @@ def test_cd1_philox_draws_are_bernoulli(ctx):
         p = 1 / (1 + np.exp(-hb[:v]))
         assert np.all(np.abs(f - p) < 5 * np.sqrt(p * (1 - p) / b) + 1e-6)
     assert not np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("prec", [P.Precision.bf16, P.Precision.fp32])
+def test_greedy_pretrain_graphs_match_stream_launches(ctx, prec, monkeypatch):
+    """The graph-launched epochs (32-step graphs with double-buffered batch rows
+    gathered on a side stream and the bias update beside the weight update, plus
+    single-step graphs for the remainder) give bit-identical parameters to the
+    same CD-1 steps launched one kernel at a time (PARNN_CD1_GRAPH=0)."""
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((4500, 64))  # 35 steps of 128 per epoch: one 32-step graph + 3 single steps
+    dims = [64, 96, 80, 10]
+    opts = P.PretrainOptions(epochs=2)
+    a = P.greedy_pretrain(dims, x, opts, seed=9, precision=prec, ctx=ctx).params
+    monkeypatch.setenv("PARNN_CD1_GRAPH", "0")
+    b = P.greedy_pretrain(dims, x, opts, seed=9, precision=prec, ctx=ctx).params
+    assert np.array_equal(a, b)
+    assert np.all(np.isfinite(a))
