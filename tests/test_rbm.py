@@ -198,3 +198,32 @@ def test_greedy_pretrain_graphs_match_stream_launches(ctx, prec, monkeypatch):
     b = P.greedy_pretrain(dims, x, opts, seed=9, precision=prec, ctx=ctx).params
     assert np.array_equal(a, b)
     assert np.all(np.isfinite(a))
+
+
+@pytest.mark.parametrize("prec", [P.Precision.fp32, P.Precision.bf16])
+@pytest.mark.parametrize("v,h,b,gauss", [(300, 200, 37, False), (77, 130, 5, True), (129, 257, 128, False)])
+def test_cd1_ragged_shapes(ctx, v, h, b, gauss, prec):
+    """Ragged widths and batches (not multiples of 8 / 32 / 64, a partial row
+    chunk, b < 8): one CD-1 step with margin-safe injected uniforms against the
+    oracle (fp32 1e-5; bf16 with its own tolerance)."""
+    rng = np.random.default_rng(v + h + b)
+    W = f32(rng.normal(0, 0.05, (h, v)))
+    vb = f32(rng.normal(0, 0.05, v))
+    hb = f32(rng.normal(0, 0.05, h))
+    x = f32(rng.standard_normal((b, v)) if gauss else rng.random((b, v)))
+    p0 = np.concatenate([W.ravel(), vb, hb])
+    st = O.Rbm(W.copy(), vb.copy(), hb.copy(), gauss)
+    p = O.hidden_probs(st, x)
+    u = rng.random(p.shape)
+    margin = 1e-4 if prec == P.Precision.fp32 else 3e-2
+    near = np.abs(u - p) < margin
+    u[near] = np.clip(np.where(p[near] > 0.5, p[near] - 2 * margin, p[near] + 2 * margin), 0.0, 0.999999)
+    r = P.Rbm(ctx, v, h, gauss, batch=128, precision=prec)
+    r.set_params(p0)
+    r.cd1(x, 0.1, sampling="uniforms", uniforms=u.ravel())
+    pos, hs, rec, neg = O.cd1_gibbs(st, x, lambda q: (u < q).astype(float))
+    ref = O.cd1_apply(st, x, pos, rec, neg, 0.1)
+    got = r.get_params()
+    refp = np.concatenate([ref.W.ravel(), ref.vb, ref.hb])
+    errs = blocks_rel(got, refp, p0, v, h)
+    assert max(errs) < TOL[prec], errs
