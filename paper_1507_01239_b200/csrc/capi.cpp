@@ -316,8 +316,8 @@ int parnn_replica_create(parnn_ctx* ctx, const uint64_t* dims, int nd, int act, 
     return guarded([&] {
         need(ctx, "replica");
         if (decay <= 0.0 || decay >= 1.0)
-            throw std::runtime_error("ng_init: decay must be in (0,1), got " + std::to_string(decay));
-        if (smoothing <= 0.0) throw std::runtime_error("ng_init: smoothing must be positive, got " + std::to_string(smoothing));
+            throw std::runtime_error("ng_init: decay must be in (0,1), got " + host::fmt_num(decay));
+        if (smoothing <= 0.0) throw std::runtime_error("ng_init: smoothing must be positive, got " + host::fmt_num(smoothing));
         if (opt < 0 || opt > 2) throw std::runtime_error("replica: unknown optimizer " + std::to_string(opt));
         auto* p = new parnn_replica;
         p->r.reset(new Replica(ctx->c.get(), to_dims(dims, nd), act, static_cast<Precision>(prec),
@@ -450,7 +450,7 @@ int parnn_replica_upload_epoch(parnn_replica* r, const uint32_t* rows, const flo
                 throw std::runtime_error("Dataset::select: index " + std::to_string(rows[i]) + " out of range " +
                                          std::to_string(R.bound->n));
         for (uint64_t i = 0; i < steps; ++i)
-            if (lrs[i] < 0.f) throw std::runtime_error("sgd_step: negative learning rate " + std::to_string(lrs[i]));
+            if (lrs[i] < 0.f) throw std::runtime_error("sgd_step: negative learning rate " + host::fmt_num(lrs[i]));
         R.upload_epoch(rows, lrs, static_cast<long>(steps));
     });
 }

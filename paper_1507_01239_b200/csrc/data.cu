@@ -184,8 +184,9 @@ void generate_device(Context* ctx, uint64_t classes, uint64_t dim, uint64_t per_
                      DeviceDataset** cv) {
     if (classes == 0 || dim == 0 || per_class == 0)
         throw std::runtime_error("generate_synthetic: classes, dim and per_class must be >= 1");
-    if (sep < 0.0) throw std::runtime_error("generate_synthetic: separation must be >= 0");
-    if (cv_fraction <= 0.0 || cv_fraction >= 1.0) throw std::runtime_error("split_cv: cv_fraction must be in (0,1)");
+    if (sep < 0.0) throw std::runtime_error("generate_synthetic: separation must be >= 0, got " + host::fmt_num(sep));
+    if (cv_fraction <= 0.0 || cv_fraction >= 1.0)
+        throw std::runtime_error("split_cv: cv_fraction must be in (0,1), got " + host::fmt_num(cv_fraction));
     const uint64_t n = classes * per_class;
     if (n < 10) throw std::runtime_error("split_cv: need at least 10 examples, got " + std::to_string(n));
     CUDA_THROW(cudaSetDevice(ctx->device));

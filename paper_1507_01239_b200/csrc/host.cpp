@@ -8,11 +8,19 @@
 #include <cstring>
 #include <fstream>
 #include <iterator>
+#include <sstream>
 #include <stdexcept>
 #include <thread>
 
 namespace pnb {
 namespace host {
+
+std::string fmt_num(double v) {
+    std::ostringstream os;
+    if (std::isnan(v)) os << (std::signbit(v) ? "-nan" : "nan");  // as glibc prints it
+    else os << v;
+    return os.str();
+}
 
 namespace {
 inline uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
@@ -158,7 +166,7 @@ std::vector<uint64_t> minibatch_rows(uint64_t n, uint64_t b, uint64_t seed) {
 HostData generate_synthetic(uint64_t classes, uint64_t dim, uint64_t per_class, double sep, uint64_t seed) {
     if (classes == 0 || dim == 0 || per_class == 0)
         fail("generate_synthetic: classes, dim and per_class must be >= 1");
-    if (sep < 0.0) fail("generate_synthetic: separation must be >= 0");
+    if (sep < 0.0) fail("generate_synthetic: separation must be >= 0, got " + fmt_num(sep));
     Rng rng(seed);
     std::vector<double> mu(classes * dim);
     for (uint64_t k = 0; k < classes; ++k) {
@@ -188,7 +196,7 @@ HostData generate_synthetic(uint64_t classes, uint64_t dim, uint64_t per_class, 
 }
 
 void split_cv(const HostData& all, double f, uint64_t seed, HostData& train, HostData& cv) {
-    if (f <= 0.0 || f >= 1.0) fail("split_cv: cv_fraction must be in (0,1)");
+    if (f <= 0.0 || f >= 1.0) fail("split_cv: cv_fraction must be in (0,1), got " + fmt_num(f));
     if (all.n < 10) fail("split_cv: need at least 10 examples, got " + std::to_string(all.n));
     const std::vector<uint64_t> idx = shuffled_indices(all.n, seed);
     const uint64_t c = static_cast<uint64_t>(std::ceil(f * static_cast<double>(all.n)));
@@ -393,7 +401,7 @@ std::vector<double> init_random(const std::vector<uint64_t>& dims, Rng& rng) {
 }
 
 Schedule make_schedule(bool newbob, double lr_init, uint64_t epochs) {
-    if (lr_init <= 0.0) fail("make_schedule: lr_init must be positive, got " + std::to_string(lr_init));
+    if (lr_init <= 0.0) fail("make_schedule: lr_init must be positive, got " + fmt_num(lr_init));
     if (epochs == 0) fail("make_schedule: planned_epochs must be positive");
     Schedule s;
     s.newbob = newbob;
@@ -405,12 +413,13 @@ Schedule make_schedule(bool newbob, double lr_init, uint64_t epochs) {
 
 double exponential_lr(const Schedule& s, double progress) {
     if (progress < 0.0 || progress > 1.0)
-        fail("exponential_lr: progress must be in [0,1], got " + std::to_string(progress));
+        fail("exponential_lr: progress must be in [0,1], got " + fmt_num(progress));
     return s.lr_init * std::pow(s.final_ratio, progress);
 }
 
 bool newbob_next(Schedule& s, double prev, double acc, double* lr_out) {
-    if (prev < 0.0 || prev > 1.0 || acc < 0.0 || acc > 1.0) fail("newbob_next: accuracies must be in [0,1]");
+    if (prev < 0.0 || prev > 1.0 || acc < 0.0 || acc > 1.0)
+        fail("newbob_next: accuracies must be in [0,1], got " + fmt_num(prev) + " and " + fmt_num(acc));
     const double gain = acc - prev;
     bool stop = false;
     if (s.halving) {

@@ -14,6 +14,10 @@
 namespace pnb {
 namespace host {
 
+// A double as the reference's error messages print it (operator<< with the
+// default stream format: 6 significant digits, "1.5", "1e-07", "nan" / "-nan").
+std::string fmt_num(double v);
+
 // xoshiro256** advances its 256-bit state linearly over GF(2); a Jump holds
 // the columns of T^n so n draws can be skipped in O(256) word operations.
 struct Jump {

@@ -47,9 +47,9 @@ void train(Context* ctx, Comm* comm, const TrainConfig& cfg, const std::vector<l
     const uint64_t nb = B <= S ? S / B : 0;
     // ng_init runs for every worker whatever the optimizer (parallel.cpp:178)
     if (cfg.ng_decay <= 0.0 || cfg.ng_decay >= 1.0)
-        throw std::runtime_error("ng_init: decay must be in (0,1), got " + std::to_string(cfg.ng_decay));
+        throw std::runtime_error("ng_init: decay must be in (0,1), got " + host::fmt_num(cfg.ng_decay));
     if (cfg.ng_smoothing <= 0.0)
-        throw std::runtime_error("ng_init: smoothing must be positive, got " + std::to_string(cfg.ng_smoothing));
+        throw std::runtime_error("ng_init: smoothing must be positive, got " + host::fmt_num(cfg.ng_smoothing));
     host::Schedule sched = host::make_schedule(cfg.newbob != 0, cfg.lr_init, cfg.epochs);
     const host::Schedule exp_sched = host::make_schedule(false, cfg.lr_init, cfg.epochs);
     if (cfg.epochs > 0 && B > S) {  // raised by minibatches() inside worker_epoch (data.cpp:188-191)

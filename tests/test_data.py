@@ -139,3 +139,33 @@ def test_dataset_load_csv_device(ctx, tmp_path):
     assert dd.num_classes == int(ds.labels.max()) + 1
     assert np.array_equal(back.labels, ds.labels)
     assert np.array_equal(back.features, ds.features.astype(np.float32))
+
+
+@pytest.mark.parametrize("args", [(0, 5, 3, 2.0, 1, 0.1, 2), (3, 5, 3, 2.0, 1, 1.0, 2), (3, 5, 3, 2.0, 1, 0.0, 2),
+                                  (3, 5, 3, -1.5, 1, 0.1, 2), (3, 5, 3, 2.0, 1, -1e-9, 2), (2, 4, 1, 2.0, 1, 0.5, 2)])
+def test_generate_errors_match_reference(reflib, args):
+    """generate_synthetic / split_cv validation (data.cpp:124-183): the same
+    message, doubles formatted as the reference's operator<< prints them."""
+    msgs = []
+    for f in (lambda: reflib.make_data(*args, True), lambda: P.make_data(*args, True)):
+        with pytest.raises((RuntimeError, P.ParnnError)) as e:
+            f()
+        msgs.append(str(e.value))
+    assert msgs[0] == msgs[1]
+
+
+def test_schedule_errors_match_reference(reflib):
+    """LR schedule validation (optimizer.cpp:159-208), the same text incl. the
+    values: newbob against the compiled reference; exponential_lr /
+    make_schedule against the reference's literal messages (its shim returns a
+    value instead of raising)."""
+    msgs = []
+    for lib in (reflib, P):
+        with pytest.raises((RuntimeError, P.ParnnError)) as e:
+            lib.newbob_sequence(0.32, [0.5, 1.2])
+        msgs.append(str(e.value))
+    assert msgs[0] == msgs[1] == "newbob_next: accuracies must be in [0,1], got 0.5 and 1.2"
+    with pytest.raises(P.ParnnError, match=r"^exponential_lr: progress must be in \[0,1\], got 1\.5$"):
+        P.exponential_lr(0.32, 5, 1.5)
+    with pytest.raises(P.ParnnError, match=r"^make_schedule: lr_init must be positive, got -0\.25$"):
+        P.exponential_lr(-0.25, 5, 0.5)
