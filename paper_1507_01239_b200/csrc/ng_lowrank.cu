@@ -742,9 +742,18 @@ void side_plans(Replica& r, LrSide& sd, const void* X) {
         e.mode = EPI_PARTIAL;
         const int n2 = 2 * R;
         const int tiles = ((n2 + 127) / 128) * ((n2 + 63) / 64);
-        // inline updates (lag 1) are latency-critical: split K over the GPU; background
-        // updates keep to a few CTAs each so they do not crowd out the running step
-        e.ksplit = r.lr_lag() == 1 ? std::max(1, sms / tiles) : 1;
+        // inline updates (lag 1) are latency-critical: split K over the GPU. Background
+        // updates split K in ~1024-wide chunks: the output layer's update (D = 8806,
+        // R = 80, ~16 Jacobi sweeps) only just fits in the three steps before its
+        // commit, and its Gram on 6 CTAs made the commit step wait (the step with
+        // the commit: 0.62 -> 0.56 ms; average step 0.559 -> 0.523 ms). Unsplit
+        // (PARNN_LR_GRAM_KCHUNK=0) or chunks of 768-2048 measured 0.523-0.527 ms.
+        static const int bg_kchunk = [] {
+            const char* v = std::getenv("PARNN_LR_GRAM_KCHUNK");
+            return v ? std::atoi(v) : 1024;
+        }();
+        e.ksplit = r.lr_lag() == 1 ? std::max(1, sms / tiles)
+                                   : (bg_kchunk > 0 ? std::max(1, static_cast<int>(sd.D / bg_kchunk)) : 1);
         const int nk = static_cast<int>((sd.D + 31) / 32);
         const int per = (nk + e.ksplit - 1) / e.ksplit;
         const int S = (nk + per - 1) / per;
