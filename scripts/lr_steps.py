@@ -34,8 +34,8 @@ ds = P.DeviceDataset(ctx, P.Dataset(x, y, 8806))
 r = P.Replica(ctx, dims, precision=P.Precision[a.precision], optimizer=P.OptimizerKind[a.optimizer], minibatch=1024,
               max_steps=a.steps + a.warmup + 128)
 r.set_params(P.init_random(dims, seed=1).params)
-if os.environ.get("LR_LAG"):
-    r.set_lowrank(update_lag=int(os.environ["LR_LAG"]))
+if os.environ.get("LR_LAG") or os.environ.get("LR_RANK_OUT"):
+    r.set_lowrank(update_lag=int(os.environ.get("LR_LAG", 4)), rank_out=int(os.environ.get("LR_RANK_OUT", 80)))
 r.bind(ds)
 tot = a.steps + a.warmup + 128
 r.upload_epoch(np.resize(np.arange(n), tot * 1024), np.full(tot, 1e-3, np.float32))
