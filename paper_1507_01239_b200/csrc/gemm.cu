@@ -172,6 +172,8 @@ void ensure_smem_attr(const void* fn, int bytes) {
 }
 
 void gemm_set_grid_cap(int cap) { g_grid_cap = cap; }
+thread_local bool g_pdl_off = false;
+void gemm_set_pdl(bool on) { g_pdl_off = !on; }
 
 dim3 gemm_launch_grid(const GemmPlan& p) {
     // the persistent kernel covers every tile with any grid (tile = blockIdx + k * gridDim;
@@ -210,7 +212,7 @@ void gemm_launch(const GemmPlan& p, cudaStream_t s) {
         attr[na].val.clusterDim.z = 1;
         ++na;
     }
-    if (pdl) {
+    if (pdl && !g_pdl_off) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;

@@ -724,10 +724,18 @@ void enqueue_lowrank(Replica& r, cudaStream_t s) {
             return v ? std::atoi(v) : 0;
         }();
         CUDA_THROW(cudaEventRecord(r.ev_act[0], s));
+        // the gather's successors start ~8 us late as programmatic dependents in this
+        // graph (measured; not so in the SGD step): plain launches for them
+        static const int pdl_head = [] {
+            const char* v = std::getenv("PARNN_LR_PDL_HEAD");
+            return v ? std::atoi(v) : 0;
+        }();
+        gemm_set_pdl(pdl_head != 0);
         if (!in_late) lr_side_chain(r, r.lrl[0].in, r.ev_act[0], S(r.lrl[0].in.stream));
         for (int l = 0; l < L; ++l) {
             if (r.variant & GATE_WAIT) wait_ext(s, r.ev_gate[l]);  // layer l's pending average is done
             gemm_launch(r.fwd[l], s);
+            gemm_set_pdl(true);
             if (l + 1 < L) {
                 CUDA_THROW(cudaEventRecord(r.ev_act[l + 1], s));
                 if (!in_late) lr_side_chain(r, r.lrl[l + 1].in, r.ev_act[l + 1], S(r.lrl[l + 1].in.stream));

@@ -78,6 +78,8 @@ void gemm_launch(const GemmPlan& p, cudaStream_t s);
 // steps that run long single-CTA kernels (the NG subspace eigensolves) beside
 // the GEMMs keep those SMs out of the GEMM grids, so no GEMM CTA waits for them.
 void gemm_set_grid_cap(int cap);
+// PDL on / off for the GEMMs this thread launches next (default on)
+void gemm_set_pdl(bool on);
 dim3 gemm_launch_grid(const GemmPlan& p);
 
 enum Precision : int { PREC_BF16 = 0, PREC_TF32 = 1, PREC_FP32 = 2 };

@@ -1,4 +1,6 @@
-"""First start / last end / count / summed duration per kernel kind in one traced step."""
+"""First start / last end / count / summed duration per kernel kind in one traced step.
+
+    python scripts/kind_timeline.py trace.csv [k]   (k: the k-th last complete step, default 1)"""
 import csv
 import re
 import subprocess
@@ -7,7 +9,8 @@ from collections import defaultdict
 
 rows = sorted((int(r[0]), int(r[1]), int(r[4]), ",".join(r[5:])) for r in csv.reader(open(sys.argv[1])) if len(r) >= 6)
 g = [i for i, r in enumerate(rows) if "gather_kernel" in r[3]]
-lo, hi = g[-2], g[-1]
+kb = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+lo, hi = g[-1 - kb], g[-kb]
 step = rows[lo:hi]
 t0 = step[0][0]
 dm = {}

@@ -62,8 +62,8 @@ if os.environ.get("LR_EIGTIME"):
             d = r.lowrank_diag(l, side)
             rows.append((d["eig_start_ns"], d["eig_end_ns"], l, side, d["sweeps"]))
     t0 = min(x[0] for x in rows)
-    for a, b, l, side, sw in sorted(rows):
-        print(f"layer {l} {'in ' if side == 0 else 'out'} eig {((a - t0) / 1e3):8.1f} .. {((b - t0) / 1e3):8.1f} us  sweeps {sw}")
+    for e0, e1, l, side, sw in sorted(rows):
+        print(f"layer {l} {'in ' if side == 0 else 'out'} eig {((e0 - t0) / 1e3):8.1f} .. {((e1 - t0) / 1e3):8.1f} us  sweeps {sw}")
 if os.environ.get("LR_PERSTEP"):
     import collections
     acc = collections.defaultdict(list)
