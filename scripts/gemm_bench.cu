@@ -19,6 +19,7 @@
 #include "../paper_1507_01239_b200/csrc/gemm_k_bf16_t_mc.cu"
 #include "../paper_1507_01239_b200/csrc/gemm_k_bf16_r_sk.cu"
 #include "../paper_1507_01239_b200/csrc/gemm_k_bf16_t_sk.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_group.cu"
 using namespace pnb;
 
 __device__ __forceinline__ float hash_uniform(unsigned long long i, unsigned seed) {
