@@ -609,7 +609,16 @@ void cholesky(Replica& r, int l, NgFactor& f, DevErr* err, cudaStream_t fs, cuda
         }
         if (f.rest[blk].M > 0) {
             if (conc) CUDA_THROW(cudaStreamWaitEvent(ts, f.ev_panel[blk], 0));
+            // the bulk update's persistent grid leaves SMs free, so the chain's diag / panel /
+            // look-ahead kernels never wait for one (13.39 -> 13.28 ms per config-2 step;
+            // 2 / 4 / 16 free: 13.32-13.35 / 13.29-13.32 / 13.28-13.31)
+            static const int rest_free = [] {
+                const char* v = std::getenv("PARNN_NG_REST_FREE");
+                return v ? std::atoi(v) : 8;
+            }();
+            if (rest_free > 0) gemm_set_grid_cap(r.ctx->num_sms - rest_free);
             gemm_launch(f.rest[blk], ts);
+            if (rest_free > 0) gemm_set_grid_cap(0);
             r.mark("ng_potrf_trail", l, 1.0 * f.rest[blk].M * f.rest[blk].N * f.rest[blk].K, ts);
             if (conc) CUDA_THROW(cudaEventRecord(f.ev_trail[blk], ts));
         }
