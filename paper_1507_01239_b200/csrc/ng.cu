@@ -152,6 +152,10 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(float* __restrict__ a, l
     float* V = sm + NB * LDS;      // [NB][LDS]  L^-1
     float* col = V + NB * LDS;     // [32] column broadcast of the 32x32 factorizations (16-byte aligned)
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    // PDL: the previous kernel of the chain (the look-ahead update of this block) is complete
+    // and visible. (No early launch_dependents: the panel GEMM's CTAs would then hold SMs for
+    // the whole factorization, 13.3 -> 14.4 ms per config-2 step.)
+    grid_dep_wait();
     PNB_CLK(0);
     {
         // 16 rows of 128 per pass: all loads issued before the shared stores
@@ -594,8 +598,21 @@ void cholesky(Replica& r, int l, NgFactor& f, DevErr* err, cudaStream_t fs, cuda
     size_t blk = 0;
     for (long j = 0; j < f.n; j += NB, ++blk) {
         const int b = (int)std::min<long>(NB, f.n - j);
-        chol_diag_kernel<<<1, 256, kDiagSmem, fs>>>(f.a, f.ld, j, b, linv_blk(f, j), err);
-        CUDA_THROW(cudaGetLastError());
+        {
+            static const bool pdl = !std::getenv("PARNN_NG_DIAG_PDL") || std::atoi(std::getenv("PARNN_NG_DIAG_PDL"));
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(1);
+            cfg.blockDim = dim3(256);
+            cfg.dynamicSmemBytes = kDiagSmem;
+            cfg.stream = fs;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = pdl ? 1 : 0;
+            float* lb = linv_blk(f, j);
+            CUDA_THROW(cudaLaunchKernelEx(&cfg, chol_diag_kernel, f.a, f.ld, j, b, lb, err));
+        }
         r.mark("ng_potrf_diag", l, static_cast<double>(b) * b * b / 3.0 * 2.0, fs);
         if (f.panel[blk].M > 0) {
             gemm_launch(f.panel[blk], fs);
