@@ -158,19 +158,27 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(float* __restrict__ a, l
     grid_dep_wait();
     PNB_CLK(0);
     {
-        // 16 rows of 128 per pass: all loads issued before the shared stores
-        float v[64];
+        // 16-byte loads (rows are 128-B aligned: ld and j are multiples of 32), all issued
+        // before the shared stores; a column group past b stays inside the padded row
+        float4 v[16];
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-            const int idx = t + 256 * i, r = idx >> 7, c = idx & (NB - 1);
-            v[i] = (r < b && c <= r) ? a[(j + r) * ld + j + c] : 0.f;
+        for (int i = 0; i < 16; ++i) {
+            const int idx = t + 256 * i, r = idx >> 5, c = (idx & 31) * 4;
+            v[i] = (r < b && c < b && c <= r) ? *reinterpret_cast<const float4*>(a + (j + r) * ld + j + c)
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-            const int idx = t + 256 * i, r = idx >> 7, c = idx & (NB - 1);
-            S[r * LDS + c] = (r >= b && r == c) ? 1.f : v[i];
-            V[r * LDS + c] = 0.f;
+        for (int i = 0; i < 16; ++i) {
+            const int idx = t + 256 * i, r = idx >> 5, c = (idx & 31) * 4;
+            const float e[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int cc = c + q;
+                S[r * LDS + cc] = (r >= b && r == cc) ? 1.f : ((cc <= r && cc < b) ? e[q] : 0.f);
+            }
         }
+        float4* v4 = reinterpret_cast<float4*>(V);  // 16-byte aligned: NB * LDS floats precede it
+        for (int i = t; i < NB * LDS / 4; i += 256) v4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
     PNB_CLK(1);
@@ -314,11 +322,26 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(float* __restrict__ a, l
         __syncthreads();
     }
     PNB_CLK(14);
-#pragma unroll 8
-    for (int i = 0; i < 64; ++i) {
-        const int idx = t + 256 * i, r = idx >> 7, c = idx & (NB - 1);
-        if (r < b && c < b) a[(j + r) * ld + j + c] = c <= r ? S[r * LDS + c] : 0.f;
-        linv[idx] = (r < b && c < b && c <= r) ? V[r * LDS + c] : 0.f;
+    // 16-byte stores; a column group that straddles b (ragged last block) goes element-wise
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {
+        const int idx = t + 256 * i, r = idx >> 5, c = (idx & 31) * 4;
+        float l4[4], v4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const bool in = r < b && c + q < b && c + q <= r;
+            l4[q] = in ? S[r * LDS + c + q] : 0.f;
+            v4[q] = in ? V[r * LDS + c + q] : 0.f;
+        }
+        *reinterpret_cast<float4*>(linv + r * NB + c) = make_float4(v4[0], v4[1], v4[2], v4[3]);
+        if (r < b) {
+            float* dst = a + (j + r) * ld + j + c;
+            if (c + 4 <= b) {
+                *reinterpret_cast<float4*>(dst) = make_float4(l4[0], l4[1], l4[2], l4[3]);
+            } else {
+                for (int q = 0; q < 4 && c + q < b; ++q) dst[q] = l4[q];
+            }
+        }
     }
     PNB_CLK(15);
 }
@@ -413,9 +436,14 @@ __global__ void ng_update_kernel(float* __restrict__ w, long ldw, float* __restr
 int grid_for(long total) { return (int)std::max<long>(1, std::min<long>((total + 255) / 256, 148L * 8)); }
 
 constexpr int kDiagSmem = 2 * NB * LDS * 4 + 48 * 4;
+// tuning aid: PARNN_NG_DIAG_SMEM=bytes requests more shared memory than the kernel uses (an SM of its own)
+int diag_smem_req() {
+    static const int v = std::getenv("PARNN_NG_DIAG_SMEM") ? std::atoi(std::getenv("PARNN_NG_DIAG_SMEM")) : 0;
+    return v;
+}
 
 void ensure_diag_attr() {
-    ensure_smem_attr(reinterpret_cast<const void*>(chol_diag_kernel), kDiagSmem);
+    ensure_smem_attr(reinterpret_cast<const void*>(chol_diag_kernel), std::max(kDiagSmem, diag_smem_req()));
 }
 
 float* linv_blk(NgFactor& f, long j) { return f.linv + (j / NB) * NB * NB; }
@@ -603,7 +631,7 @@ void cholesky(Replica& r, int l, NgFactor& f, DevErr* err, cudaStream_t fs, cuda
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(1);
             cfg.blockDim = dim3(256);
-            cfg.dynamicSmemBytes = kDiagSmem;
+            cfg.dynamicSmemBytes = std::max(kDiagSmem, diag_smem_req());
             cfg.stream = fs;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
