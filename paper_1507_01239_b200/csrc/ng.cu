@@ -158,18 +158,20 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(float* __restrict__ a, l
     grid_dep_wait();
     PNB_CLK(0);
     {
-        // 16-byte loads (rows are 128-B aligned: ld and j are multiples of 32), all issued
-        // before the shared stores; a column group past b stays inside the padded row
+        // 16-byte loads, all issued before the shared stores (fewer memory requests: inside
+        // the factorization chain, beside the bulk updates' traffic, that is what counts).
+        // A warp covers 4 rows x 32 columns: lane -> row (lane >> 3), columns 4 (lane & 7) ..,
+        // so each store instruction hits 32 distinct banks of the padded rows (bank r + c).
         float4 v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            const int idx = t + 256 * i, r = idx >> 5, c = (idx & 31) * 4;
+            const int tile = i * 8 + warp, r = 4 * (tile >> 2) + (lane >> 3), c = 32 * (tile & 3) + 4 * (lane & 7);
             v[i] = (r < b && c < b && c <= r) ? *reinterpret_cast<const float4*>(a + (j + r) * ld + j + c)
                                               : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            const int idx = t + 256 * i, r = idx >> 5, c = (idx & 31) * 4;
+            const int tile = i * 8 + warp, r = 4 * (tile >> 2) + (lane >> 3), c = 32 * (tile & 3) + 4 * (lane & 7);
             const float e[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
