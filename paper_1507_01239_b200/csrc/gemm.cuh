@@ -31,7 +31,7 @@ namespace pnb {
 #ifdef PNB_GEMM_TRACE
 // per-CTA %globaltimer stamps: entry, setup done, first operands in smem,
 // last MMA issued, accumulator ready, epilogue done, exit
-__device__ unsigned long long g_gemm_trace[1024][8];
+__device__ unsigned long long g_gemm_trace[1024][12];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -952,6 +952,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     if (warp == 2) PNB_TRACE(7);
                 }
                 mbar_wait(wbar, 0);  // the peer's partial of my chunks has landed (bulk copy, like TMA)
+                if (warp == 2 && lane == 0) PNB_TRACE(8);
             }
 #pragma unroll 1
             for (int c = c_begin; c < c_end; c += 2) {
@@ -992,6 +993,7 @@ __global__ void __launch_bounds__(GemmSmem<BN, STAGES, T, SPLIT, TE>::kThreads, 
                     xhave = nhave;
                 }
             }
+            if (warp == 2 && lane == 0) PNB_TRACE(9);
             tc_fence_before();
             if constexpr (MC == 2) {
                 __syncwarp();

@@ -17,6 +17,7 @@
 #include "../paper_1507_01239_b200/csrc/gemm_k_bf16_t_mc.cu"
 #include "../paper_1507_01239_b200/csrc/gemm_k_bf16_r_sk.cu"
 #include "../paper_1507_01239_b200/csrc/gemm_k_bf16_t_sk.cu"
+#include "../paper_1507_01239_b200/csrc/gemm_k_group.cu"
 
 using namespace pnb;
 
@@ -96,14 +97,14 @@ int main() {
                 float ms;
                 cudaEventElapsedTime(&ms, e0, e1);
                 if (rep < 2) continue;
-                unsigned long long tr[1024][8];
+                unsigned long long tr[1024][12];
                 cudaMemcpyFromSymbol(tr, g_gemm_trace, sizeof(tr));
                 const int g = p.grid.x;
                 unsigned long long t0 = ~0ull;
                 for (int b = 0; b < g; ++b) t0 = std::min(t0, tr[b][0]);
                 printf("%-30s %s grid=%d bn=%d  %.2f us (events)\n", c.name, cold ? "cold" : "warm", g, p.bn, ms * 1e3);
-                const char* nm[8] = {"entry", "setup", "first-data", "last-mma", "acc-ready", "epi-done", "exit", "sent"};
-                for (int i = 0; i < 8; ++i) {
+                const char* nm[10] = {"entry", "setup", "first-data", "last-mma", "acc-ready", "epi-done", "exit", "sent", "recv(w2)", "chunks(w2)"};
+                for (int i = 0; i < 10; ++i) {
                     double mn = 1e30, mx = 0, av = 0;
                     for (int b = 0; b < g; ++b) {
                         const double v = (tr[b][i] - t0) * 1e-3;
